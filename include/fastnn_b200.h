@@ -1,0 +1,169 @@
+/*
+ * fastnn_b200.h -- C-ABI of the B200-native FastNN-Lite matching path.
+ *
+ * This is the drop-in boundary: plain pointers, sizes and enums, no C++ or
+ * torch types.  The reference (/root/reference/proj) is a C++ library whose
+ * hot path is reached through the functions cited on each entry point; the
+ * host C++ wrapper (paper_2503_10017_b200/csrc/host/) keeps those C++
+ * signatures intact and forwards here, and INTEGRATION.md shows the binding a
+ * maintainer adds on the reference side.
+ *
+ * Conventions
+ *  - Every entry point returns FNL_OK (0) or an error class; the message of the
+ *    last failure on the calling thread is fnl_last_error().  FNL_EINVAL maps to
+ *    std::invalid_argument (ValueError in Python), FNL_ERUNTIME to
+ *    std::runtime_error (RuntimeError), exactly as the reference throws.
+ *  - Pointers named h_* are host memory (pageable or pinned); d_* are device
+ *    memory on the context's GPU.  Work is ordered on the context's stream;
+ *    calls taking host outputs synchronise before returning.
+ *  - There is no CPU fallback: without a usable sm_100 device every compute
+ *    entry point returns FNL_ERUNTIME.
+ */
+#ifndef FASTNN_B200_H
+#define FASTNN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FNL_ABI_VERSION 1
+
+enum fnl_status { FNL_OK = 0, FNL_EINVAL = 1, FNL_ERUNTIME = 2 };
+
+/* include/fastnn/core.hpp:75-88 (DistanceMetric / PrecisionMode) */
+enum fnl_metric { FNL_METRIC_L2 = 0, FNL_METRIC_DOT = 1 };
+enum fnl_precision { FNL_PREC_FULL = 0, FNL_PREC_HYBRID = 1 };
+
+/* include/fastnn/nn.hpp:20 (NnBackend) plus the tensor-core HybridCast path.
+ * FNL_BACKEND_TENSOR: binary16 cast-in, tcgen05 fp32 accumulate, fp32 compare
+ * (Alg. 3); near ties are re-decided by the exact FMA chain, so the
+ * result equals the reference `single` backend run on binary16-rounded maps. */
+enum fnl_backend {
+    FNL_BACKEND_BRUTEFORCE = 0,
+    FNL_BACKEND_DOUBLE = 1,
+    FNL_BACKEND_SINGLE = 2,
+    FNL_BACKEND_HYBRIDCAST = 3,
+    FNL_BACKEND_TENSOR = 4
+};
+
+/* include/fastnn/core.hpp:92-103 (MatchConfig), field for field. */
+typedef struct {
+    uint32_t k;
+    uint32_t grid_stride;
+    uint32_t max_iters;
+    double convergence_fraction;
+    int32_t metric;    /* enum fnl_metric */
+    int32_t precision; /* enum fnl_precision */
+    uint32_t block_size;
+} fnl_match_config;
+
+/* Device-side counters of one reciprocal run, from which the host rebuilds the
+ * reference RunReport (include/fastnn/instrument.hpp:44-77) exactly. */
+#define FNL_MAX_ITERS 64
+typedef struct {
+    uint32_t samples;
+    uint32_t iterations;
+    uint32_t converged;
+    uint32_t duplicates_dropped;
+    uint32_t matches;
+    uint32_t history_len;
+    uint32_t active_history[FNL_MAX_ITERS];
+    uint64_t a_block_fetches;
+    uint64_t b_block_fetches;
+    uint64_t half_saturation_events;
+    /* tensor backend only: rows whose tensor-core top-2 gap fell inside the
+     * certified error band and were re-decided by the exact chain */
+    uint64_t near_tie_rows;
+    uint64_t query_rows; /* total NN query rows issued (forward + reverse) */
+    /* device time of each phase (CUDA events on the context stream), shared by
+     * all pairs of one batched launch; RunReport *_us fields */
+    double subsample_us, forward_nn_us, reverse_nn_us, harvest_us;
+} fnl_run_stats;
+
+typedef struct fnl_context fnl_context;
+
+/* ---- lifetime ---------------------------------------------------------- */
+int fnl_abi_version(void);
+const char* fnl_last_error(void);
+int fnl_device_count(int* count);
+/* One context = one GPU + one stream + a grow-only workspace.  A context is
+ * single-owner (one matcher state per pair, single owner);
+ * concurrent callers use one context each. */
+int fnl_context_create(int device, fnl_context** out);
+int fnl_context_destroy(fnl_context* ctx);
+/* Replace the context's stream (a cudaStream_t / CUstream handle); NULL
+ * restores the context's own stream. */
+int fnl_context_set_stream(fnl_context* ctx, void* stream);
+int fnl_context_synchronize(fnl_context* ctx);
+
+/* ---- L1: materialising block scorer --------------------------------------
+ * src/kernels.cpp:377-400 block_distances (kernels.hpp:72-74): writes the
+ * nq x nt distance matrix row-major to h_out with the reference per-pair FMA
+ * chain; hybrid rounds inputs and outputs to binary16 (saturations counted). */
+int fnl_block_distances(fnl_context* ctx, const float* h_queries, uint32_t nq,
+                        const float* h_targets, uint32_t nt, uint32_t dim, int metric,
+                        int precision, float* h_out, uint64_t* saturation_events);
+
+/* ---- L2: nearest-neighbour query -----------------------------------------
+ * src/nn.cpp:65-164 nn_query_{bruteforce,double_loop,single_loop}
+ * (nn.hpp:54-63) and the FeatureMap wrappers nn.cpp:166-187.  One fused
+ * score+argmin pass over all targets.  q_blocks / t_blocks are the block
+ * counts of the caller's query / target partitions (ceil(n / block_size) for
+ * make_partition); they only drive the reference's logical counters:
+ * single/hybrid a = b = q_blocks, double a = q_blocks, b = q_blocks * t_blocks,
+ * bruteforce none; hybrid saturations follow src/nn.cpp:143-161 (single) and
+ * src/kernels.cpp:387-398 per block pair (double). */
+int fnl_nn_query(fnl_context* ctx, const float* h_queries, uint32_t nq, const float* h_targets,
+                 uint32_t nt, uint32_t dim, int metric, int precision, int backend,
+                 uint32_t q_blocks, uint32_t t_blocks, uint32_t* h_nearest, float* h_min_dist,
+                 uint64_t* a_fetches, uint64_t* b_fetches, uint64_t* saturation_events);
+
+/* ---- L3: reciprocal matching ----------------------------------------------
+ * src/reciprocal.cpp:97-206 reciprocal_match (reciprocal.hpp:50-51).  Maps are
+ * H x W x dim fp32 row-major host arrays; non-finite values are rejected with
+ * the reference's message (src/core.cpp:19-25).  h_pairs receives
+ * (i, j, iteration) triples in harvest order; capacity = 3 * samples. */
+int fnl_reciprocal_match(fnl_context* ctx, const float* h_d1, uint32_t h1, uint32_t w1,
+                         const float* h_d2, uint32_t h2, uint32_t w2, uint32_t dim,
+                         const fnl_match_config* cfg, int backend, uint32_t* h_pairs,
+                         uint32_t* n_pairs, fnl_run_stats* stats);
+
+/* Batched form: npairs independent pairs of identical shape, all matched in
+ * lock-step on one GPU.  h_d1/h_d2 point at npairs
+ * contiguous maps each; host->device copies are pipelined with compute.
+ * h_pairs holds npairs * 3 * samples u32, n_pairs npairs counts, stats npairs
+ * entries (NULL allowed). */
+int fnl_reciprocal_match_batch(fnl_context* ctx, uint32_t npairs, const float* h_d1,
+                               const float* h_d2, uint32_t h, uint32_t w, uint32_t dim,
+                               const fnl_match_config* cfg, int backend, uint32_t* h_pairs,
+                               uint32_t* n_pairs, fnl_run_stats* stats);
+
+/* Same, with the maps already resident in device memory (d_d1/d_d2: npairs
+ * contiguous H x W x dim fp32 maps).  Outputs stay on the device:
+ * d_pairs npairs * 3 * samples u32, d_n_pairs npairs u32.  Asynchronous on the
+ * context stream except for one small convergence read per iteration. */
+int fnl_reciprocal_match_batch_device(fnl_context* ctx, uint32_t npairs, const float* d_d1,
+                                      const float* d_d2, uint32_t h, uint32_t w, uint32_t dim,
+                                      const fnl_match_config* cfg, int backend,
+                                      uint32_t* d_pairs, uint32_t* d_n_pairs,
+                                      fnl_run_stats* h_stats);
+
+/* src/reciprocal.cpp:82-95 mutual_nn_exact (reciprocal.hpp:26): exhaustive
+ * mutual NN, full precision, lowest-index ties; h_pairs capacity 2*h1*w1. */
+int fnl_mutual_nn(fnl_context* ctx, const float* h_d1, uint32_t h1, uint32_t w1,
+                  const float* h_d2, uint32_t h2, uint32_t w2, uint32_t dim, int metric,
+                  uint32_t* h_pairs, uint32_t* n_pairs);
+
+/* ---- instrumentation -------------------------------------------------------
+ * Device time (ms, CUDA events on the context stream) of the dominant scoring
+ * kernel summed since the last reset, and its launch count. */
+int fnl_kernel_timing(fnl_context* ctx, int reset, double* score_ms, uint64_t* score_launches,
+                      uint64_t* total_launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

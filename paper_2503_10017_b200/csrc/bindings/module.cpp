@@ -1,0 +1,410 @@
+// module.cpp -- the `_fastnn` Python surface (drop-in for the reference
+// bindings/module.cpp:64-260): the same 14 functions, argument names, defaults,
+// dtypes, return shapes and dict keys, plus batch / device-resident entry points
+// and instrumentation.  GPU work runs with the GIL released.
+#include <pybind11/numpy.h>
+#include <pybind11/pybind11.h>
+#include <pybind11/stl.h>
+
+#include <cstring>
+
+#include "fastnn/half.hpp"
+#include "fastnn/instrument.hpp"
+#include "fastnn/io.hpp"
+#include "fastnn/kernels.hpp"
+#include "fastnn/nn.hpp"
+#include "fastnn/reciprocal.hpp"
+#include "runtime.hpp"
+
+namespace py = pybind11;
+using F32 = py::array_t<float, py::array::c_style | py::array::forcecast>;
+using U32Array = py::array_t<std::uint32_t>;
+
+namespace {
+
+fastnn::FeatureMap to_map(const F32& a) {
+    if (a.ndim() != 3) throw std::invalid_argument("feature map must have shape (H, W, d)");
+    return fastnn::FeatureMap::from_data(static_cast<std::uint32_t>(a.shape(0)),
+                                         static_cast<std::uint32_t>(a.shape(1)),
+                                         static_cast<std::uint32_t>(a.shape(2)),
+                                         std::vector<float>(a.data(), a.data() + a.size()));
+}
+
+py::array from_map(const fastnn::FeatureMap& m) {
+    py::array_t<float> a({py::ssize_t(m.height), py::ssize_t(m.width), py::ssize_t(m.dim)});
+    std::memcpy(a.mutable_data(), m.data.data(), m.data.size() * sizeof(float));
+    return a;
+}
+
+template <typename T>
+py::array_t<T> vec_array(const std::vector<T>& v) {
+    py::array_t<T> a(py::ssize_t(v.size()));
+    if (!v.empty()) std::memcpy(a.mutable_data(), v.data(), v.size() * sizeof(T));
+    return a;
+}
+
+py::dict nn_dict(const fastnn::NnResult& r, const fastnn::FetchCounter& c) {
+    py::dict d;
+    d["nearest"] = vec_array(r.nearest);
+    d["min_dist"] = vec_array(r.min_dist);
+    d["a_block_fetches"] = c.a_fetches();
+    d["b_block_fetches"] = c.b_fetches();
+    d["half_saturation_events"] = c.saturations();
+    return d;
+}
+
+fastnn::MatchConfig make_cfg(std::uint32_t k, std::uint32_t stride, std::uint32_t max_iters,
+                             double convergence, const std::string& metric,
+                             const std::string& precision, std::uint32_t block_size) {
+    fastnn::MatchConfig cfg;
+    cfg.k = k;
+    cfg.grid_stride = k > 0 ? 0 : stride;  // bindings/module.cpp:236
+    cfg.max_iters = max_iters;
+    cfg.convergence_fraction = convergence;
+    cfg.metric = fastnn::metric_from_string(metric);
+    cfg.precision = fastnn::precision_from_string(precision);
+    cfg.block_size = block_size;
+    return cfg;
+}
+
+fnl_match_config c_cfg(const fastnn::MatchConfig& c) {
+    return {c.k, c.grid_stride, c.max_iters, c.convergence_fraction,
+            c.metric == fastnn::DistanceMetric::SquaredL2 ? FNL_METRIC_L2 : FNL_METRIC_DOT,
+            c.precision == fastnn::PrecisionMode::Hybrid ? FNL_PREC_HYBRID : FNL_PREC_FULL,
+            c.block_size};
+}
+
+int c_backend(fastnn::NnBackend b) {
+    switch (b) {
+        case fastnn::NnBackend::Bruteforce: return FNL_BACKEND_BRUTEFORCE;
+        case fastnn::NnBackend::DoubleLoop: return FNL_BACKEND_DOUBLE;
+        case fastnn::NnBackend::SingleLoop: return FNL_BACKEND_SINGLE;
+        case fastnn::NnBackend::HybridCast: return FNL_BACKEND_HYBRIDCAST;
+        case fastnn::NnBackend::Tensor: return FNL_BACKEND_TENSOR;
+    }
+    return FNL_BACKEND_SINGLE;
+}
+
+py::dict stats_dict(const fnl_run_stats& s) {
+    py::dict d;
+    d["samples"] = s.samples;
+    d["iterations"] = s.iterations;
+    d["converged"] = s.converged;
+    d["duplicates_dropped"] = s.duplicates_dropped;
+    d["matches"] = s.matches;
+    d["active_history"] = std::vector<std::uint32_t>(s.active_history, s.active_history + s.history_len);
+    d["a_block_fetches"] = s.a_block_fetches;
+    d["b_block_fetches"] = s.b_block_fetches;
+    d["half_saturation_events"] = s.half_saturation_events;
+    d["near_tie_rows"] = s.near_tie_rows;
+    d["query_rows"] = s.query_rows;
+    d["forward_nn_us"] = s.forward_nn_us;
+    d["reverse_nn_us"] = s.reverse_nn_us;
+    d["harvest_us"] = s.harvest_us;
+    return d;
+}
+
+void check_shape3(const F32& a, const char* who) {
+    if (a.ndim() != 3) throw std::invalid_argument(std::string(who) + ": feature map must have shape (H, W, d)");
+    if (a.shape(0) == 0 || a.shape(1) == 0 || a.shape(2) == 0)
+        throw std::invalid_argument("FeatureMap: height, width and dim must all be >= 1");
+}
+
+}  // namespace
+
+PYBIND11_MODULE(_fastnn, m) {
+    m.doc() = "B200-native fast reciprocal nearest-neighbour matching (FastNN-Lite / HybridCast)";
+
+    m.def("gen_random",
+          [](std::uint32_t h, std::uint32_t w, std::uint32_t d, std::uint64_t seed, bool normalize) {
+              return from_map(fastnn::gen_random(h, w, d, seed, normalize));
+          },
+          py::arg("height"), py::arg("width"), py::arg("dim"), py::arg("seed"), py::arg("normalize") = true);
+
+    m.def("gen_matched_pair",
+          [](std::uint32_t h, std::uint32_t w, std::uint32_t d, std::uint64_t seed, double sigma,
+             const std::string& permute) {
+              const auto p = fastnn::gen_matched_pair(h, w, d, seed, sigma, fastnn::permute_from_string(permute));
+              py::dict out;
+              out["d1"] = from_map(p.d1);
+              out["d2"] = from_map(p.d2);
+              out["truth"] = vec_array(p.truth.map);
+              out["noise_sigma"] = p.truth.noise_sigma;
+              out["permute"] = permute;
+              return out;
+          },
+          py::arg("height"), py::arg("width"), py::arg("dim"), py::arg("seed"),
+          py::arg("noise_sigma") = 0.0, py::arg("permute") = "random");
+
+    m.def("write_fmap", [](const F32& a, const std::string& path) { fastnn::save_fmap(to_map(a), path); },
+          py::arg("map"), py::arg("path"));
+    m.def("read_fmap", [](const std::string& path) { return from_map(fastnn::load_fmap(path)); },
+          py::arg("path"));
+
+    m.def("dist_scalar",
+          [](const std::vector<float>& a, const std::vector<float>& b, const std::string& metric) {
+              return fastnn::dist_scalar(a, b, fastnn::metric_from_string(metric));
+          },
+          py::arg("a"), py::arg("b"), py::arg("metric") = "l2");
+
+    m.def("to_half_round", [](float x) { return fastnn::to_half_round(x); }, py::arg("x"),
+          "nearest binary16 value, round to nearest even, widened back to float32");
+
+    m.def("block_distances",
+          [](const F32& q, const F32& t, const std::string& metric, const std::string& precision) {
+              if (q.ndim() != 2 || t.ndim() != 2)
+                  throw std::invalid_argument("block_distances expects 2-D (n, d) arrays");
+              const fastnn::DescriptorsView qv{q.data(), std::uint32_t(q.shape(0)), std::uint32_t(q.shape(1))};
+              const fastnn::DescriptorsView tv{t.data(), std::uint32_t(t.shape(0)), std::uint32_t(t.shape(1))};
+              const auto mt = fastnn::metric_from_string(metric);
+              const auto pr = fastnn::precision_from_string(precision);
+              fastnn::FetchCounter c;
+              fastnn::DistanceMatrix dm;
+              {
+                  py::gil_scoped_release nogil;
+                  dm = fastnn::block_distances(qv, tv, mt, pr, c);
+              }
+              py::array_t<float> out({py::ssize_t(dm.rows), py::ssize_t(dm.cols)});
+              std::memcpy(out.mutable_data(), dm.data.data(), dm.data.size() * sizeof(float));
+              return out;
+          },
+          py::arg("queries"), py::arg("targets"), py::arg("metric") = "l2", py::arg("precision") = "full");
+
+    m.def("nn_bruteforce",
+          [](const F32& A, const F32& B, const std::string& metric) {
+              const auto a = to_map(A), b = to_map(B);
+              const auto mt = fastnn::metric_from_string(metric);
+              fastnn::FetchCounter c;
+              fastnn::NnResult r;
+              {
+                  py::gil_scoped_release nogil;
+                  r = fastnn::nn_bruteforce(a, b, mt);
+              }
+              return nn_dict(r, c);
+          },
+          py::arg("A"), py::arg("B"), py::arg("metric") = "l2");
+
+    m.def("nn_double_loop",
+          [](const F32& A, const F32& B, std::uint32_t bs, const std::string& metric,
+             const std::string& precision, unsigned threads) {
+              const auto a = to_map(A), b = to_map(B);
+              const auto pa = fastnn::make_partition(a.pixel_count(), bs);
+              const auto pb = fastnn::make_partition(b.pixel_count(), bs);
+              const auto mt = fastnn::metric_from_string(metric);
+              const auto pr = fastnn::precision_from_string(precision);
+              fastnn::FetchCounter c;
+              fastnn::NnResult r;
+              {
+                  py::gil_scoped_release nogil;
+                  r = fastnn::nn_double_loop(a, b, pa, pb, mt, pr, c, threads);
+              }
+              return nn_dict(r, c);
+          },
+          py::arg("A"), py::arg("B"), py::arg("block_size") = 4096, py::arg("metric") = "l2",
+          py::arg("precision") = "full", py::arg("threads") = 1);
+
+    m.def("nn_single_loop",
+          [](const F32& A, const F32& B, std::uint32_t bs, const std::string& metric,
+             const std::string& precision, unsigned threads) {
+              const auto a = to_map(A), b = to_map(B);
+              const auto pa = fastnn::make_partition(a.pixel_count(), bs);
+              const auto mt = fastnn::metric_from_string(metric);
+              const auto pr = fastnn::precision_from_string(precision);
+              fastnn::FetchCounter c;
+              fastnn::NnResult r;
+              {
+                  py::gil_scoped_release nogil;
+                  r = fastnn::nn_single_loop(a, b, pa, mt, pr, c, threads);
+              }
+              return nn_dict(r, c);
+          },
+          py::arg("A"), py::arg("B"), py::arg("block_size") = 4096, py::arg("metric") = "l2",
+          py::arg("precision") = "full", py::arg("threads") = 1);
+
+    m.def("nn_hybridcast",
+          [](const F32& A, const F32& B, std::uint32_t bs, const std::string& metric, unsigned threads) {
+              const auto a = to_map(A), b = to_map(B);
+              const auto pa = fastnn::make_partition(a.pixel_count(), bs);
+              const auto mt = fastnn::metric_from_string(metric);
+              fastnn::FetchCounter c;
+              fastnn::NnResult r;
+              {
+                  py::gil_scoped_release nogil;
+                  r = fastnn::nn_hybridcast(a, b, pa, mt, c, threads);
+              }
+              return nn_dict(r, c);
+          },
+          py::arg("A"), py::arg("B"), py::arg("block_size") = 4096, py::arg("metric") = "l2",
+          py::arg("threads") = 1);
+
+    m.def("grid_subsample",
+          [](std::uint32_t h, std::uint32_t w, std::uint32_t k, std::uint32_t stride) {
+              const fastnn::FeatureMap shape(h, w, 1);
+              std::vector<std::uint32_t> ids;
+              for (const auto p : fastnn::grid_subsample(shape, k, stride)) ids.push_back(p.index);
+              return vec_array(ids);
+          },
+          py::arg("height"), py::arg("width"), py::arg("k") = 0, py::arg("stride") = 8);
+
+    m.def("mutual_nn_exact",
+          [](const F32& D1, const F32& D2, const std::string& metric) {
+              const auto a = to_map(D1), b = to_map(D2);
+              const auto mt = fastnn::metric_from_string(metric);
+              fastnn::MatchSet s;
+              {
+                  py::gil_scoped_release nogil;
+                  s = fastnn::mutual_nn_exact(a, b, mt);
+              }
+              U32Array out({py::ssize_t(s.pairs.size()), py::ssize_t(2)});
+              auto v = out.mutable_unchecked<2>();
+              for (py::ssize_t r = 0; r < py::ssize_t(s.pairs.size()); ++r) {
+                  v(r, 0) = s.pairs[r].i;
+                  v(r, 1) = s.pairs[r].j;
+              }
+              return out;
+          },
+          py::arg("D1"), py::arg("D2"), py::arg("metric") = "l2");
+
+    // The maps go straight from the numpy buffers to the device (no FeatureMap
+    // copy); finiteness is validated on the GPU with the reference's message.
+    m.def("reciprocal_match",
+          [](const F32& D1, const F32& D2, const std::string& backend, std::uint32_t k,
+             std::uint32_t stride, std::uint32_t max_iters, double convergence,
+             const std::string& metric, const std::string& precision, std::uint32_t block_size,
+             unsigned threads) {
+              check_shape3(D1, "reciprocal_match");
+              check_shape3(D2, "reciprocal_match");
+              const auto cfg = make_cfg(k, stride, max_iters, convergence, metric, precision, block_size);
+              const auto be = fastnn::backend_from_string(backend);
+              (void)threads;
+              fastnn::MatchOutcome out;
+              {
+                  py::gil_scoped_release nogil;
+                  out = fastnn::b200::reciprocal_match_raw(
+                      D1.data(), std::uint32_t(D1.shape(0)), std::uint32_t(D1.shape(1)), D2.data(),
+                      std::uint32_t(D2.shape(0)), std::uint32_t(D2.shape(1)), std::uint32_t(D1.shape(2)),
+                      std::uint32_t(D2.shape(2)), cfg, be);
+              }
+              U32Array pairs({py::ssize_t(out.matches.pairs.size()), py::ssize_t(3)});
+              auto v = pairs.mutable_unchecked<2>();
+              for (py::ssize_t r = 0; r < py::ssize_t(out.matches.pairs.size()); ++r) {
+                  v(r, 0) = out.matches.pairs[r].i;
+                  v(r, 1) = out.matches.pairs[r].j;
+                  v(r, 2) = out.matches.pairs[r].iteration;
+              }
+              return py::make_tuple(pairs, fastnn::render_report(out.report, fastnn::ReportFormat::Json));
+          },
+          py::arg("D1"), py::arg("D2"), py::arg("backend") = "single", py::arg("k") = 0,
+          py::arg("stride") = 8, py::arg("max_iters") = 10, py::arg("convergence") = 0.99,
+          py::arg("metric") = "l2", py::arg("precision") = "full", py::arg("block_size") = 4096,
+          py::arg("threads") = 1);
+
+    // ------------------------------------------------------------ extensions
+    m.def("nn_tensor",
+          [](const F32& A, const F32& B, const std::string& metric) {
+              const auto a = to_map(A), b = to_map(B);
+              const auto mt = fastnn::metric_from_string(metric);
+              fastnn::FetchCounter c;
+              fastnn::NnResult r;
+              {
+                  py::gil_scoped_release nogil;
+                  r = fastnn::nn_query_tensor(fastnn::DescriptorsView::of(a), fastnn::DescriptorsView::of(b), mt);
+              }
+              return nn_dict(r, c);
+          },
+          py::arg("A"), py::arg("B"), py::arg("metric") = "dot",
+          "tcgen05 HybridCast NN of every pixel of A in B (binary16 in, fp32 accumulate/compare, "
+          "near ties re-decided exactly)");
+
+    // Batched host-buffer matcher: npairs stacked (n, H, W, d) maps, H2D copies
+    // pipelined with compute.  Returns (pairs[n, samples, 3], counts[n], stats).
+    m.def("reciprocal_match_batch",
+          [](const F32& D1, const F32& D2, const std::string& backend, std::uint32_t k,
+             std::uint32_t stride, std::uint32_t max_iters, double convergence,
+             const std::string& metric, const std::string& precision, std::uint32_t block_size) {
+              if (D1.ndim() != 4 || D2.ndim() != 4)
+                  throw std::invalid_argument("reciprocal_match_batch expects (n, H, W, d) arrays");
+              for (int i = 0; i < 4; ++i)
+                  if (D1.shape(i) != D2.shape(i))
+                      throw std::invalid_argument("reciprocal_match_batch: D1 and D2 shapes differ");
+              const auto cfg = make_cfg(k, stride, max_iters, convergence, metric, precision, block_size);
+              cfg.validate();
+              const auto cc = c_cfg(cfg);
+              const int be = c_backend(fastnn::backend_from_string(backend));
+              const std::uint32_t n = std::uint32_t(D1.shape(0)), h = std::uint32_t(D1.shape(1)),
+                                  w = std::uint32_t(D1.shape(2)), d = std::uint32_t(D1.shape(3));
+              const fastnn::FeatureMap shape(h, w, 1);
+              const std::size_t cap = std::max<std::size_t>(1, fastnn::grid_subsample(shape, cfg.k, cfg.grid_stride).size());
+              U32Array pairs({py::ssize_t(n), py::ssize_t(cap), py::ssize_t(3)});
+              U32Array counts{py::ssize_t(n)};
+              std::vector<fnl_run_stats> st(n);
+              {
+                  py::gil_scoped_release nogil;
+                  fastnn::b200::check(fnl_reciprocal_match_batch(fastnn::b200::context(), n, D1.data(), D2.data(),
+                                                                 h, w, d, &cc, be, pairs.mutable_data(),
+                                                                 counts.mutable_data(), st.data()));
+              }
+              py::list stats;
+              for (const auto& s : st) stats.append(stats_dict(s));
+              return py::make_tuple(pairs, counts, stats);
+          },
+          py::arg("D1"), py::arg("D2"), py::arg("backend") = "tensor", py::arg("k") = 0,
+          py::arg("stride") = 8, py::arg("max_iters") = 10, py::arg("convergence") = 0.99,
+          py::arg("metric") = "dot", py::arg("precision") = "full", py::arg("block_size") = 4096);
+
+    // Device-resident matcher (maps and outputs are device pointers, e.g.
+    // torch.Tensor.data_ptr()); returns per-pair stats.
+    m.def("reciprocal_match_device",
+          [](std::uintptr_t d1, std::uintptr_t d2, std::uint32_t n, std::uint32_t h, std::uint32_t w,
+             std::uint32_t d, std::uintptr_t out_pairs, std::uintptr_t out_counts,
+             const std::string& backend, std::uint32_t k, std::uint32_t stride, std::uint32_t max_iters,
+             double convergence, const std::string& metric, const std::string& precision,
+             std::uint32_t block_size, std::uintptr_t stream) {
+              const auto cfg = make_cfg(k, stride, max_iters, convergence, metric, precision, block_size);
+              cfg.validate();
+              const auto cc = c_cfg(cfg);
+              const int be = c_backend(fastnn::backend_from_string(backend));
+              std::vector<fnl_run_stats> st(n);
+              {
+                  py::gil_scoped_release nogil;
+                  fnl_context* ctx = fastnn::b200::context();
+                  fastnn::b200::check(fnl_context_set_stream(ctx, reinterpret_cast<void*>(stream)));
+                  const int rc = fnl_reciprocal_match_batch_device(
+                      ctx, n, reinterpret_cast<const float*>(d1), reinterpret_cast<const float*>(d2), h, w, d,
+                      &cc, be, reinterpret_cast<std::uint32_t*>(out_pairs),
+                      reinterpret_cast<std::uint32_t*>(out_counts), st.data());
+                  fnl_context_set_stream(ctx, nullptr);
+                  fastnn::b200::check(rc);
+              }
+              py::list stats;
+              for (const auto& s : st) stats.append(stats_dict(s));
+              return stats;
+          },
+          py::arg("d1"), py::arg("d2"), py::arg("npairs"), py::arg("height"), py::arg("width"),
+          py::arg("dim"), py::arg("out_pairs"), py::arg("out_counts"), py::arg("backend") = "tensor",
+          py::arg("k") = 0, py::arg("stride") = 8, py::arg("max_iters") = 10,
+          py::arg("convergence") = 0.99, py::arg("metric") = "dot", py::arg("precision") = "full",
+          py::arg("block_size") = 4096, py::arg("stream") = 0);
+
+    m.def("kernel_timing",
+          [](bool reset) {
+              double ms = 0;
+              std::uint64_t launches = 0, total = 0;
+              fastnn::b200::check(fnl_kernel_timing(fastnn::b200::context(), reset, &ms, &launches, &total));
+              py::dict d;
+              d["score_ms"] = ms;
+              d["score_launches"] = launches;
+              d["total_launches"] = total;
+              return d;
+          },
+          py::arg("reset") = false,
+          "device time and launch count of the dominant scoring kernel since the last reset");
+
+    m.def("device_count", [] {
+        int n = 0;
+        fnl_device_count(&n);
+        return n;
+    });
+    m.def("set_device", [](int dev) { fastnn::b200::set_device(dev); }, py::arg("device"));
+    m.def("abi_version", [] { return fnl_abi_version(); });
+}

@@ -1,0 +1,879 @@
+// capi.cu -- the extern "C" boundary of libfastnn_b200.so (include/fastnn_b200.h).
+//
+// Owns contexts (device + stream + grow-only workspace), argument checking with
+// the reference's error classes, host<->device staging, the per-backend fetch
+// and saturation accounting of the reference (src/nn.cpp:143-161, :101-130;
+// src/kernels.cpp:387-398), and the host side of the device-resident matcher
+// loop (src/reciprocal.cpp:97-206).  All scoring runs in the kernels of
+// exact_scan.cu / tensor_scan.cu; there is no host compute path.
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "fastnn_b200.h"
+#include "fnl_common.cuh"
+#include "fnl_internal.h"
+#include "tensor_scan.h"
+
+namespace fnl {
+
+static thread_local std::string g_last_error;
+
+int fail(int status, const std::string& msg) {
+    g_last_error = msg;
+    return status;
+}
+
+int fail_cuda(cudaError_t e, const char* expr, const char* file, int line) {
+    return fail(FNL_ERUNTIME, std::string("CUDA error ") + cudaGetErrorName(e) + " (" +
+                                  cudaGetErrorString(e) + ") at " + file + ":" +
+                                  std::to_string(line) + ": " + expr);
+}
+
+}  // namespace fnl
+
+using fnl::fail;
+
+struct fnl_context {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;
+    struct Buf {
+        void* p = nullptr;
+        size_t bytes = 0;
+    };
+    std::map<std::string, Buf> dev;
+    std::map<std::string, Buf> pinned;
+    // instrumentation of the dominant scoring kernel
+    bool timing = true;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used, ev_free;
+    double score_ms = 0.0;
+    uint64_t score_launches = 0, total_launches = 0;
+};
+
+namespace {
+
+using fnl::fail_cuda;
+
+int check_device(fnl_context* ctx) {
+    if (!ctx) return fail(FNL_EINVAL, "fastnn_b200: null context");
+    cudaError_t e = cudaSetDevice(ctx->device);
+    if (e != cudaSuccess) return fnl::fail_cuda(e, "cudaSetDevice", __FILE__, __LINE__);
+    return FNL_OK;
+}
+
+// Grow-only device workspace slot.
+int dev_buf(fnl_context* ctx, const char* name, size_t bytes, void** out) {
+    auto& b = ctx->dev[name];
+    if (b.bytes < bytes) {
+        if (b.p) cudaFree(b.p);
+        b.p = nullptr;
+        b.bytes = 0;
+        const size_t want = std::max<size_t>(bytes, 256);
+        cudaError_t e = cudaMalloc(&b.p, want);
+        if (e != cudaSuccess) return fnl::fail_cuda(e, name, __FILE__, __LINE__);
+        b.bytes = want;
+    }
+    *out = b.p;
+    return FNL_OK;
+}
+
+template <typename T>
+int dev_arr(fnl_context* ctx, const char* name, size_t count, T** out) {
+    void* p = nullptr;
+    int st = dev_buf(ctx, name, count * sizeof(T), &p);
+    *out = static_cast<T*>(p);
+    return st;
+}
+
+#define TRY(x)                          \
+    do {                                \
+        int _st = (x);                  \
+        if (_st != FNL_OK) return _st;  \
+    } while (0)
+
+uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+// Score-kernel timing: events bracket every dominant-kernel launch.
+void timing_begin(fnl_context* ctx, cudaEvent_t* a, cudaEvent_t* b) {
+    *a = *b = nullptr;
+    if (!ctx->timing) return;
+    std::pair<cudaEvent_t, cudaEvent_t> ev;
+    if (!ctx->ev_free.empty()) {
+        ev = ctx->ev_free.back();
+        ctx->ev_free.pop_back();
+    } else {
+        cudaEventCreate(&ev.first);
+        cudaEventCreate(&ev.second);
+    }
+    cudaEventRecord(ev.first, ctx->stream);
+    ctx->ev_used.push_back(ev);
+    *a = ev.first;
+    *b = ev.second;
+}
+void timing_end(fnl_context* ctx, cudaEvent_t b) {
+    ctx->score_launches++;
+    if (b) cudaEventRecord(b, ctx->stream);
+}
+void timing_harvest(fnl_context* ctx) {
+    // caller has synchronised the stream
+    for (auto& ev : ctx->ev_used) {
+        float ms = 0.0f;
+        if (cudaEventElapsedTime(&ms, ev.first, ev.second) == cudaSuccess) ctx->score_ms += ms;
+        ctx->ev_free.push_back(ev);
+    }
+    ctx->ev_used.clear();
+}
+
+// Phase timers for the RunReport *_us fields (device time, microseconds).
+struct PhaseTimer {
+    fnl_context* ctx;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
+    cudaEvent_t open = nullptr;
+    int open_phase = -1;
+    void begin(int phase) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, ctx->stream);
+        open = e;
+        open_phase = phase;
+    }
+    void end() {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, ctx->stream);
+        marks.push_back({open_phase, {open, e}});
+        open = nullptr;
+    }
+    // caller synchronised the stream
+    void collect(double us[4]) {
+        for (auto& m : marks) {
+            float ms = 0.0f;
+            if (cudaEventElapsedTime(&ms, m.second.first, m.second.second) == cudaSuccess)
+                us[m.first] += 1000.0 * ms;
+            cudaEventDestroy(m.second.first);
+            cudaEventDestroy(m.second.second);
+        }
+        marks.clear();
+    }
+    ~PhaseTimer() {
+        for (auto& m : marks) {
+            cudaEventDestroy(m.second.first);
+            cudaEventDestroy(m.second.second);
+        }
+        if (open) cudaEventDestroy(open);
+    }
+};
+enum { kPhaseSubsample = 0, kPhaseForward = 1, kPhaseReverse = 2, kPhaseHarvest = 3 };
+
+bool valid_metric(int m) { return m == FNL_METRIC_L2 || m == FNL_METRIC_DOT; }
+bool valid_prec(int p) { return p == FNL_PREC_FULL || p == FNL_PREC_HYBRID; }
+bool valid_backend(int b) { return b >= FNL_BACKEND_BRUTEFORCE && b <= FNL_BACKEND_TENSOR; }
+
+// Effective precision of a backend (src/reciprocal.cpp:105-107, nn.cpp:184-187).
+bool backend_hybrid(int backend, int precision) {
+    if (backend == FNL_BACKEND_BRUTEFORCE) return false;
+    if (backend == FNL_BACKEND_HYBRIDCAST) return true;
+    if (backend == FNL_BACKEND_TENSOR) return false;  // tensor path keeps fp32 distances
+    return precision == FNL_PREC_HYBRID;
+}
+
+std::string nonfinite_msg(uint64_t idx) {
+    return "FeatureMap: non-finite value at flat index " + std::to_string(idx);
+}
+
+// Uploads (if host) and prepares a stack of maps: finiteness check, optional
+// binary16 copy with per-row saturation counts and per-map totals.
+struct Prepared {
+    const float* data = nullptr;   // what the scorer reads
+    uint8_t* row_sat = nullptr;
+    unsigned long long* map_sat = nullptr;  // per map totals (device)
+};
+
+int prepare_maps(fnl_context* ctx, const char* tag, const float* d_src, uint32_t nmaps,
+                 uint64_t rows_per_map, uint32_t dim, bool hybrid, bool validate,
+                 Prepared* out, unsigned long long* d_bad) {
+    const uint64_t rows = rows_per_map * nmaps;
+    out->data = d_src;
+    out->row_sat = nullptr;
+    std::string t(tag);
+    TRY(dev_arr(ctx, (t + ".mapsat").c_str(), nmaps, &out->map_sat));
+    FNL_CUDA_TRY(cudaMemsetAsync(out->map_sat, 0, nmaps * sizeof(unsigned long long), ctx->stream));
+    if (!hybrid && !validate) return FNL_OK;
+    fnl::PrepareArgs a{};
+    a.src = d_src;
+    a.rows = rows;
+    a.dim = dim;
+    a.bad_index = d_bad;
+    a.total_sat = out->map_sat;
+    if (hybrid) {
+        float* r = nullptr;
+        TRY(dev_arr(ctx, (t + ".half").c_str(), rows * dim, &r));
+        TRY(dev_arr(ctx, (t + ".rowsat").c_str(), rows, &out->row_sat));
+        a.rounded = r;
+        a.row_sat = out->row_sat;
+        out->data = r;
+    }
+    if (nmaps == 1) {
+        FNL_CUDA_TRY(fnl::launch_prepare(a, ctx->stream));
+    } else {
+        // per-map totals: one launch per map keeps the kernel simple
+        for (uint32_t m = 0; m < nmaps; ++m) {
+            fnl::PrepareArgs b = a;
+            b.src = d_src + (size_t)m * rows_per_map * dim;
+            b.rows = rows_per_map;
+            if (hybrid) {
+                b.rounded = a.rounded + (size_t)m * rows_per_map * dim;
+                b.row_sat = a.row_sat + (size_t)m * rows_per_map;
+            }
+            b.total_sat = out->map_sat + m;
+            FNL_CUDA_TRY(fnl::launch_prepare(b, ctx->stream));
+        }
+    }
+    return FNL_OK;
+}
+
+// One exact NN pass (K4 + finalize) over the current query set of every pair.
+int exact_nn(fnl_context* ctx, const fnl::ScanArgs& sa, uint32_t max_q, uint32_t npairs, bool l2,
+             bool hybrid, const fnl::FinalizeArgs& fa) {
+    cudaEvent_t e0, e1;
+    timing_begin(ctx, &e0, &e1);
+    FNL_CUDA_TRY(fnl::launch_exact_scan(sa, max_q, npairs, l2, hybrid, ctx->stream));
+    timing_end(ctx, e1);
+    FNL_CUDA_TRY(fnl::launch_finalize(fa, max_q, npairs, ctx->stream));
+    ctx->total_launches += 2;
+    return FNL_OK;
+}
+
+}  // namespace
+
+// ============================================================== lifetime
+extern "C" int fnl_abi_version(void) { return FNL_ABI_VERSION; }
+
+extern "C" const char* fnl_last_error(void) { return fnl::g_last_error.c_str(); }
+
+extern "C" int fnl_device_count(int* count) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (count) *count = e == cudaSuccess ? n : 0;
+    if (e != cudaSuccess) return fnl::fail_cuda(e, "cudaGetDeviceCount", __FILE__, __LINE__);
+    return FNL_OK;
+}
+
+extern "C" int fnl_context_create(int device, fnl_context** out) {
+    if (!out) return fail(FNL_EINVAL, "fnl_context_create: null out");
+    *out = nullptr;
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        return fail(FNL_ERUNTIME, std::string("fastnn_b200: no CUDA device available (") +
+                                      (e == cudaSuccess ? "0 devices" : cudaGetErrorString(e)) +
+                                      "); this library has no CPU fallback");
+    if (device < 0 || device >= n)
+        return fail(FNL_EINVAL, "fnl_context_create: device " + std::to_string(device) +
+                                    " out of range (" + std::to_string(n) + " devices)");
+    cudaDeviceProp prop{};
+    FNL_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return fail(FNL_ERUNTIME, std::string("fastnn_b200: device '") + prop.name +
+                                      "' is sm_" + std::to_string(prop.major) +
+                                      std::to_string(prop.minor) + "; kernels are built for sm_100a");
+    FNL_CUDA_TRY(cudaSetDevice(device));
+    auto* ctx = new fnl_context();
+    ctx->device = device;
+    ctx->sm_count = prop.multiProcessorCount;
+    cudaError_t e1 = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
+    cudaError_t e2 = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking);
+    if (e1 != cudaSuccess || e2 != cudaSuccess) {
+        delete ctx;
+        return fnl::fail_cuda(e1 != cudaSuccess ? e1 : e2, "cudaStreamCreate", __FILE__, __LINE__);
+    }
+    ctx->stream = ctx->own_stream;
+    *out = ctx;
+    return FNL_OK;
+}
+
+extern "C" int fnl_context_destroy(fnl_context* ctx) {
+    if (!ctx) return FNL_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (auto& kv : ctx->dev) cudaFree(kv.second.p);
+    for (auto& kv : ctx->pinned) cudaFreeHost(kv.second.p);
+    for (auto& ev : ctx->ev_used) { cudaEventDestroy(ev.first); cudaEventDestroy(ev.second); }
+    for (auto& ev : ctx->ev_free) { cudaEventDestroy(ev.first); cudaEventDestroy(ev.second); }
+    cudaStreamDestroy(ctx->own_stream);
+    cudaStreamDestroy(ctx->copy_stream);
+    delete ctx;
+    return FNL_OK;
+}
+
+extern "C" int fnl_context_set_stream(fnl_context* ctx, void* stream) {
+    TRY(check_device(ctx));
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+    return FNL_OK;
+}
+
+extern "C" int fnl_context_synchronize(fnl_context* ctx) {
+    TRY(check_device(ctx));
+    FNL_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    timing_harvest(ctx);
+    return FNL_OK;
+}
+
+extern "C" int fnl_kernel_timing(fnl_context* ctx, int reset, double* score_ms,
+                                 uint64_t* score_launches, uint64_t* total_launches) {
+    TRY(check_device(ctx));
+    FNL_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    timing_harvest(ctx);
+    if (score_ms) *score_ms = ctx->score_ms;
+    if (score_launches) *score_launches = ctx->score_launches;
+    if (total_launches) *total_launches = ctx->total_launches;
+    if (reset) {
+        ctx->score_ms = 0.0;
+        ctx->score_launches = 0;
+        ctx->total_launches = 0;
+    }
+    return FNL_OK;
+}
+
+// ============================================================== L1 block scorer
+extern "C" int fnl_block_distances(fnl_context* ctx, const float* h_q, uint32_t nq,
+                                   const float* h_t, uint32_t nt, uint32_t dim, int metric,
+                                   int precision, float* h_out, uint64_t* sat_out) {
+    TRY(check_device(ctx));
+    if (!valid_metric(metric) || !valid_prec(precision))
+        return fail(FNL_EINVAL, "fnl_block_distances: bad metric/precision");
+    if (nq == 0 || nt == 0) return fail(FNL_EINVAL, "block_distances: empty block");
+    if (dim == 0) return fail(FNL_EINVAL, "block_distances: zero dim");
+    const bool hyb = precision == FNL_PREC_HYBRID;
+    float *dq, *dt, *dout;
+    unsigned long long* cnt;
+    TRY(dev_arr(ctx, "bd.q", (size_t)nq * dim, &dq));
+    TRY(dev_arr(ctx, "bd.t", (size_t)nt * dim, &dt));
+    TRY(dev_arr(ctx, "bd.out", (size_t)nq * nt, &dout));
+    TRY(dev_arr(ctx, "bd.cnt", 8, &cnt));
+    FNL_CUDA_TRY(cudaMemsetAsync(cnt, 0, 8 * sizeof(unsigned long long), ctx->stream));
+    FNL_CUDA_TRY(cudaMemcpyAsync(dq, h_q, (size_t)nq * dim * 4, cudaMemcpyHostToDevice, ctx->stream));
+    FNL_CUDA_TRY(cudaMemcpyAsync(dt, h_t, (size_t)nt * dim * 4, cudaMemcpyHostToDevice, ctx->stream));
+    Prepared pq, pt;
+    unsigned long long* bad;
+    TRY(dev_arr(ctx, "bd.bad", 1, &bad));
+    FNL_CUDA_TRY(cudaMemsetAsync(bad, 0xFF, 8, ctx->stream));
+    TRY(prepare_maps(ctx, "bd.pq", dq, 1, nq, dim, hyb, false, &pq, bad));
+    TRY(prepare_maps(ctx, "bd.pt", dt, 1, nt, dim, hyb, false, &pt, bad));
+    cudaEvent_t e0, e1;
+    timing_begin(ctx, &e0, &e1);
+    FNL_CUDA_TRY(fnl::launch_block_distances(pq.data, nq, pt.data, nt, dim, metric == FNL_METRIC_L2,
+                                             hyb, dout, cnt + 1, ctx->stream));
+    timing_end(ctx, e1);
+    FNL_CUDA_TRY(cudaMemcpyAsync(h_out, dout, (size_t)nq * nt * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    unsigned long long h_cnt[3] = {0, 0, 0};
+    FNL_CUDA_TRY(cudaMemcpyAsync(h_cnt, cnt + 1, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    unsigned long long h_ms[2] = {0, 0};
+    FNL_CUDA_TRY(cudaMemcpyAsync(&h_ms[0], pq.map_sat, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    FNL_CUDA_TRY(cudaMemcpyAsync(&h_ms[1], pt.map_sat, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    FNL_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    timing_harvest(ctx);
+    ctx->total_launches += 1;
+    // src/kernels.cpp:387-398: targets rounded once, every query row once, every distance
+    if (sat_out) *sat_out = hyb ? (h_ms[0] + h_ms[1] + h_cnt[0]) : 0;
+    return FNL_OK;
+}
+
+// ============================================================== L2 NN query
+extern "C" int fnl_nn_query(fnl_context* ctx, const float* h_q, uint32_t nq, const float* h_t,
+                            uint32_t nt, uint32_t dim, int metric, int precision, int backend,
+                            uint32_t q_blocks, uint32_t t_blocks, uint32_t* h_nearest, float* h_min_dist,
+                            uint64_t* a_fetches, uint64_t* b_fetches, uint64_t* sat_out) {
+    TRY(check_device(ctx));
+    if (!valid_metric(metric) || !valid_prec(precision) || !valid_backend(backend))
+        return fail(FNL_EINVAL, "fnl_nn_query: bad metric/precision/backend");
+    if (nt == 0) return fail(FNL_EINVAL, "nn: no target pixels");
+    if (dim == 0) return fail(FNL_EINVAL, "nn: zero dim");
+    const bool hyb = backend_hybrid(backend, precision);
+    const bool l2 = metric == FNL_METRIC_L2;
+    if (a_fetches) *a_fetches = 0;
+    if (b_fetches) *b_fetches = 0;
+    if (sat_out) *sat_out = 0;
+    if (nq == 0) return FNL_OK;
+
+    float *dq, *dt, *dmd;
+    uint32_t* dnear;
+    unsigned long long *keys, *cnt, *bad;
+    TRY(dev_arr(ctx, "nn.q", (size_t)nq * dim, &dq));
+    TRY(dev_arr(ctx, "nn.t", (size_t)nt * dim, &dt));
+    TRY(dev_arr(ctx, "nn.keys", nq, &keys));
+    TRY(dev_arr(ctx, "nn.near", nq, &dnear));
+    TRY(dev_arr(ctx, "nn.md", nq, &dmd));
+    TRY(dev_arr(ctx, "nn.cnt", 2, &cnt));
+    TRY(dev_arr(ctx, "nn.bad", 1, &bad));
+    FNL_CUDA_TRY(cudaMemcpyAsync(dq, h_q, (size_t)nq * dim * 4, cudaMemcpyHostToDevice, ctx->stream));
+    FNL_CUDA_TRY(cudaMemcpyAsync(dt, h_t, (size_t)nt * dim * 4, cudaMemcpyHostToDevice, ctx->stream));
+    FNL_CUDA_TRY(cudaMemsetAsync(keys, 0xFF, (size_t)nq * 8, ctx->stream));
+    FNL_CUDA_TRY(cudaMemsetAsync(cnt, 0, 16, ctx->stream));
+    Prepared pq, pt;
+    TRY(prepare_maps(ctx, "nn.pq", dq, 1, nq, dim, hyb, false, &pq, bad));
+    TRY(prepare_maps(ctx, "nn.pt", dt, 1, nt, dim, hyb, false, &pt, bad));
+
+    if (backend == FNL_BACKEND_TENSOR) {
+        TRY(fnl::tensor_nn_dense(ctx, dq, nq, dt, nt, dim, l2, dnear, dmd));
+    } else {
+        fnl::ScanArgs sa{};
+        sa.qmap = pq.data;
+        sa.qcount_const = nq;
+        sa.q_row_sat = pq.row_sat;
+        sa.tmap = pt.data;
+        sa.nt = nt;
+        sa.dim = dim;
+        sa.keys = keys;
+        sa.keys_pair_stride = nq;
+        sa.counters = cnt;
+        fnl::FinalizeArgs fa{};
+        fa.keys = keys;
+        fa.keys_pair_stride = nq;
+        fa.qcount_const = nq;
+        fa.nearest = dnear;
+        fa.nearest_pair_stride = nq;
+        fa.min_dist = dmd;
+        fa.dot = !l2;
+        TRY(exact_nn(ctx, sa, nq, 1, l2, hyb, fa));
+    }
+    FNL_CUDA_TRY(cudaMemcpyAsync(h_nearest, dnear, (size_t)nq * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (h_min_dist)
+        FNL_CUDA_TRY(cudaMemcpyAsync(h_min_dist, dmd, (size_t)nq * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    unsigned long long h_cnt[2] = {0, 0}, h_ms[2] = {0, 0};
+    FNL_CUDA_TRY(cudaMemcpyAsync(h_cnt, cnt, 16, cudaMemcpyDeviceToHost, ctx->stream));
+    FNL_CUDA_TRY(cudaMemcpyAsync(&h_ms[0], pq.map_sat, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    FNL_CUDA_TRY(cudaMemcpyAsync(&h_ms[1], pt.map_sat, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    FNL_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    timing_harvest(ctx);
+
+    // logical fetch law + saturation law of the chosen backend
+    const uint64_t nqb = backend == FNL_BACKEND_BRUTEFORCE ? 0 : q_blocks;
+    const uint64_t ntb = backend == FNL_BACKEND_BRUTEFORCE ? 0 : t_blocks;
+    uint64_t a = 0, b = 0, sat = 0;
+    if (backend == FNL_BACKEND_DOUBLE) {
+        a = nqb;
+        b = nqb * ntb;
+        if (hyb) sat = nqb * h_ms[1] + ntb * h_cnt[0] + h_cnt[1];
+    } else if (backend != FNL_BACKEND_BRUTEFORCE) {
+        a = nqb;
+        b = nqb;
+        if (hyb) sat = h_ms[1] + h_cnt[0] + h_cnt[1];
+    }
+    if (a_fetches) *a_fetches = a;
+    if (b_fetches) *b_fetches = b;
+    if (sat_out) *sat_out = sat;
+    return FNL_OK;
+}
+
+// ============================================================== L3 matcher
+namespace {
+
+uint32_t derived_stride(uint32_t h, uint32_t w, uint32_t k, uint32_t stride) {
+    if (stride != 0) return stride;
+    const double cells = (double)h * (double)w / (double)k;
+    const long s = lround(sqrt(cells));
+    return s < 1 ? 1u : (uint32_t)s;
+}
+
+int check_cfg(const fnl_match_config* cfg) {
+    if (!cfg) return fail(FNL_EINVAL, "MatchConfig: null");
+    if (cfg->grid_stride == 0 && cfg->k == 0)
+        return fail(FNL_EINVAL, "MatchConfig: one of k or grid_stride must be >= 1");
+    if (cfg->max_iters == 0) return fail(FNL_EINVAL, "MatchConfig: max_iters must be >= 1");
+    if (!(cfg->convergence_fraction > 0.0) || cfg->convergence_fraction > 1.0)
+        return fail(FNL_EINVAL, "MatchConfig: convergence_fraction must be in (0, 1]");
+    if (cfg->block_size == 0) return fail(FNL_EINVAL, "MatchConfig: block_size must be >= 1");
+    if (!valid_metric(cfg->metric) || !valid_prec(cfg->precision))
+        return fail(FNL_EINVAL, "MatchConfig: bad metric/precision");
+    if (cfg->max_iters > FNL_MAX_ITERS)
+        return fail(FNL_EINVAL, "MatchConfig: max_iters above " + std::to_string(FNL_MAX_ITERS) +
+                                    " is not supported by this build");
+    return FNL_OK;
+}
+
+// The device-resident matcher over npairs stacked pairs.  d_d1 / d_d2 are raw
+// fp32 maps on the device.  Results stay on the device in the MatchState.
+int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1, uint32_t w1,
+              const float* d_d2, uint32_t h2, uint32_t w2, uint32_t dim,
+              const fnl_match_config* cfg, int backend, uint32_t* d_pairs_out,
+              uint32_t* d_npairs_out, fnl_run_stats* h_stats, bool validate) {
+    TRY(check_cfg(cfg));
+    if (!valid_backend(backend)) return fail(FNL_EINVAL, "reciprocal_match: unknown backend");
+    if (dim == 0 || h1 == 0 || w1 == 0 || h2 == 0 || w2 == 0)
+        return fail(FNL_EINVAL, "FeatureMap: height, width and dim must all be >= 1");
+    const bool hyb = backend_hybrid(backend, cfg->precision);
+    const bool l2 = cfg->metric == FNL_METRIC_L2;
+    const uint32_t p1 = h1 * w1, p2 = h2 * w2;
+    const uint32_t stride = derived_stride(h1, w1, cfg->k, cfg->grid_stride);
+    const uint32_t samples = ((h1 + stride - 1) / stride) * ((w1 + stride - 1) / stride);
+    const uint32_t cap = std::max<uint32_t>(samples, 1);
+    const uint32_t T = cfg->max_iters;
+
+    // ---- workspace
+    fnl::MatchState m{};
+    m.npairs = npairs;
+    m.cap = cap;
+    m.samples = samples;
+    m.h1 = h1;
+    m.w1 = w1;
+    m.p1 = p1;
+    m.p2 = p2;
+    m.grid_stride = stride;
+    m.max_iters = T;
+    m.convergence = cfg->convergence_fraction;
+    m.words_i = (p1 + 31) / 32;
+    m.words_j = (p2 + 31) / 32;
+    const size_t pc = (size_t)npairs * cap;
+    TRY(dev_arr(ctx, "m.u", pc, &m.active_u));
+    TRY(dev_arr(ctx, "m.v", pc, &m.active_v));
+    TRY(dev_arr(ctx, "m.back", pc, &m.back));
+    TRY(dev_arr(ctx, "m.nact", npairs, &m.n_active));
+    TRY(dev_arr(ctx, "m.done", npairs, &m.done));
+    TRY(dev_arr(ctx, "m.usedi", (size_t)npairs * m.words_i, &m.used_i));
+    TRY(dev_arr(ctx, "m.usedj", (size_t)npairs * m.words_j, &m.used_j));
+    m.pairs = d_pairs_out;
+    m.n_pairs = d_npairs_out;
+    TRY(dev_arr(ctx, "m.stats", (size_t)npairs * fnl::kStatWords, &m.stats));
+    TRY(dev_arr(ctx, "m.ndone", 1, &m.n_done));
+    unsigned long long *keys, *bad, *counters;
+    TRY(dev_arr(ctx, "m.keys", pc, &keys));
+    TRY(dev_arr(ctx, "m.bad", 2, &bad));
+    const uint32_t max_calls = 2 * T + 1;
+    TRY(dev_arr(ctx, "m.counters", (size_t)max_calls * npairs * 2, &counters));
+    cudaStream_t s = ctx->stream;
+    FNL_CUDA_TRY(cudaMemsetAsync(m.used_i, 0, (size_t)npairs * m.words_i * 4, s));
+    FNL_CUDA_TRY(cudaMemsetAsync(m.used_j, 0, (size_t)npairs * m.words_j * 4, s));
+    FNL_CUDA_TRY(cudaMemsetAsync(m.n_done, 0, 4, s));
+    FNL_CUDA_TRY(cudaMemsetAsync(keys, 0xFF, pc * 8, s));
+    FNL_CUDA_TRY(cudaMemsetAsync(counters, 0, (size_t)max_calls * npairs * 16, s));
+    FNL_CUDA_TRY(cudaMemsetAsync(bad, 0xFF, 16, s));
+
+    // ---- K1: validate + (hybrid) round
+    Prepared P1, P2;
+    TRY(prepare_maps(ctx, "m.p1", d_d1, npairs, p1, dim, hyb, validate, &P1, bad));
+    TRY(prepare_maps(ctx, "m.p2", d_d2, npairs, p2, dim, hyb, validate, &P2, bad + 1));
+    if (validate) {
+        // D1 is checked before D2, as the reference converts D1 first
+        // (bindings/module.cpp:232-233); indices are flat within one map.
+        unsigned long long hb[2] = {~0ull, ~0ull};
+        FNL_CUDA_TRY(cudaMemcpyAsync(hb, bad, 16, cudaMemcpyDeviceToHost, s));
+        FNL_CUDA_TRY(cudaStreamSynchronize(s));
+        if (hb[0] != ~0ull) return fail(FNL_EINVAL, nonfinite_msg(hb[0] % ((uint64_t)p1 * dim)));
+        if (hb[1] != ~0ull) return fail(FNL_EINVAL, nonfinite_msg(hb[1] % ((uint64_t)p2 * dim)));
+    }
+    PhaseTimer timer{ctx};
+    timer.begin(kPhaseSubsample);
+    FNL_CUDA_TRY(fnl::launch_match_init(m, s));
+    timer.end();
+
+    // ---- NN pass helper: queries = rows of qmap at ids, targets = tmap
+    uint32_t call = 0;
+    auto nn_pass = [&](const Prepared& Q, uint32_t qrows, const uint32_t* ids, const Prepared& Tm,
+                       uint32_t nt, uint32_t* out) -> int {
+        if (backend == FNL_BACKEND_TENSOR) {
+            TRY(fnl::tensor_nn_gathered(ctx, npairs, Q.data, (uint64_t)qrows * dim, ids, cap,
+                                        m.n_active, m.done, Tm.data, (uint64_t)nt * dim, nt, dim,
+                                        l2, out, cap));
+            ++call;
+            return FNL_OK;
+        }
+        fnl::ScanArgs sa{};
+        sa.qmap = Q.data;
+        sa.qmap_pair_stride = (uint64_t)qrows * dim;
+        sa.qids = ids;
+        sa.qids_pair_stride = cap;
+        sa.qcount = m.n_active;
+        sa.pair_done = m.done;
+        sa.q_row_sat = Q.row_sat;
+        sa.q_row_sat_pair_stride = qrows;
+        sa.tmap = Tm.data;
+        sa.tmap_pair_stride = (uint64_t)nt * dim;
+        sa.nt = nt;
+        sa.dim = dim;
+        sa.keys = keys;
+        sa.keys_pair_stride = cap;
+        sa.counters = counters + (size_t)call * npairs * 2;
+        fnl::FinalizeArgs fa{};
+        fa.keys = keys;
+        fa.keys_pair_stride = cap;
+        fa.qcount = m.n_active;
+        fa.pair_done = m.done;
+        fa.nearest = out;
+        fa.nearest_pair_stride = cap;
+        fa.dot = !l2;
+        ++call;
+        return exact_nn(ctx, sa, cap, npairs, l2, hyb, fa);
+    };
+
+    if (samples > 0) {
+        timer.begin(kPhaseForward);
+        TRY(nn_pass(P1, p1, m.active_u, P2, p2, m.active_v));
+        timer.end();
+    }
+    for (uint32_t t = 1; t <= T && samples > 0; ++t) {
+        timer.begin(kPhaseReverse);
+        TRY(nn_pass(P2, p2, m.active_v, P1, p1, m.back));
+        timer.end();
+        timer.begin(kPhaseHarvest);
+        FNL_CUDA_TRY(fnl::launch_harvest(m, t, s));
+        timer.end();
+        ctx->total_launches += 1;
+        unsigned int ndone = 0;
+        FNL_CUDA_TRY(cudaMemcpyAsync(&ndone, m.n_done, 4, cudaMemcpyDeviceToHost, s));
+        FNL_CUDA_TRY(cudaStreamSynchronize(s));
+        if (ndone >= npairs) break;
+        timer.begin(kPhaseForward);
+        TRY(nn_pass(P1, p1, m.active_u, P2, p2, m.active_v));
+        timer.end();
+    }
+
+    // ---- stats back to host and the reference's accounting
+    if (h_stats) {
+        std::vector<uint32_t> st((size_t)npairs * fnl::kStatWords);
+        std::vector<unsigned long long> cnt((size_t)max_calls * npairs * 2);
+        std::vector<unsigned long long> ms1(npairs), ms2(npairs);
+        std::vector<uint32_t> npr(npairs);
+        FNL_CUDA_TRY(cudaMemcpyAsync(st.data(), m.stats, st.size() * 4, cudaMemcpyDeviceToHost, s));
+        FNL_CUDA_TRY(cudaMemcpyAsync(cnt.data(), counters, cnt.size() * 8, cudaMemcpyDeviceToHost, s));
+        FNL_CUDA_TRY(cudaMemcpyAsync(ms1.data(), P1.map_sat, npairs * 8, cudaMemcpyDeviceToHost, s));
+        FNL_CUDA_TRY(cudaMemcpyAsync(ms2.data(), P2.map_sat, npairs * 8, cudaMemcpyDeviceToHost, s));
+        FNL_CUDA_TRY(cudaMemcpyAsync(npr.data(), m.n_pairs, npairs * 4, cudaMemcpyDeviceToHost, s));
+        FNL_CUDA_TRY(cudaStreamSynchronize(s));
+        double phase_us[4] = {0, 0, 0, 0};
+        timer.collect(phase_us);
+        const uint64_t bs = cfg->block_size;
+        for (uint32_t p = 0; p < npairs; ++p) {
+            const uint32_t* ps = st.data() + (size_t)p * fnl::kStatWords;
+            fnl_run_stats& o = h_stats[p];
+            memset(&o, 0, sizeof(o));
+            o.samples = samples;
+            o.subsample_us = phase_us[kPhaseSubsample];
+            o.forward_nn_us = phase_us[kPhaseForward];
+            o.reverse_nn_us = phase_us[kPhaseReverse];
+            o.harvest_us = phase_us[kPhaseHarvest];
+            o.iterations = ps[fnl::kStatIters];
+            o.converged = ps[fnl::kStatConverged];
+            o.duplicates_dropped = ps[fnl::kStatDups];
+            o.matches = npr[p];
+            o.history_len = std::min<uint32_t>(ps[fnl::kStatHistLen], FNL_MAX_ITERS);
+            for (uint32_t i = 0; i < o.history_len; ++i) o.active_history[i] = ps[fnl::kStatHist + i];
+            // rebuild the call sequence: fwd(S), then rev(active_{t-1}) and, except
+            // after the last iteration, fwd(active_t)
+            struct Call { uint64_t nq, nt; bool fwd; };
+            std::vector<Call> calls;
+            if (samples > 0) calls.push_back({samples, p2, true});
+            uint32_t prev = samples;
+            for (uint32_t t = 1; t <= o.iterations; ++t) {
+                calls.push_back({prev, p1, false});
+                const uint32_t cur = o.active_history[t - 1];
+                if (t < o.iterations) calls.push_back({cur, p2, true});
+                prev = cur;
+            }
+            for (size_t c = 0; c < calls.size(); ++c) {
+                const Call& k = calls[c];
+                o.query_rows += k.nq;
+                if (backend == FNL_BACKEND_BRUTEFORCE) continue;
+                const uint64_t nqb = ceil_div(k.nq, bs), ntb = ceil_div(k.nt, bs);
+                const unsigned long long qs = c < max_calls ? cnt[(c * npairs + p) * 2 + 0] : 0;
+                const unsigned long long ds = c < max_calls ? cnt[(c * npairs + p) * 2 + 1] : 0;
+                const unsigned long long tsat = k.fwd ? ms2[p] : ms1[p];
+                o.a_block_fetches += nqb;
+                if (backend == FNL_BACKEND_DOUBLE) {
+                    o.b_block_fetches += nqb * ntb;
+                    if (hyb) o.half_saturation_events += nqb * tsat + ntb * qs + ds;
+                } else {
+                    o.b_block_fetches += nqb;
+                    if (hyb) o.half_saturation_events += tsat + qs + ds;
+                }
+            }
+            if (backend == FNL_BACKEND_TENSOR) {
+                o.half_saturation_events = ms1[p] + ms2[p];
+                o.near_tie_rows = fnl::tensor_near_tie_rows(ctx, p);
+            }
+        }
+    }
+    timing_harvest(ctx);
+    return FNL_OK;
+}
+
+}  // namespace
+
+extern "C" int fnl_reciprocal_match(fnl_context* ctx, const float* h_d1, uint32_t h1, uint32_t w1,
+                                    const float* h_d2, uint32_t h2, uint32_t w2, uint32_t dim,
+                                    const fnl_match_config* cfg, int backend, uint32_t* h_pairs,
+                                    uint32_t* n_pairs, fnl_run_stats* stats) {
+    TRY(check_device(ctx));
+    TRY(check_cfg(cfg));
+    const uint64_t n1 = (uint64_t)h1 * w1 * dim, n2 = (uint64_t)h2 * w2 * dim;
+    float *d1, *d2;
+    TRY(dev_arr(ctx, "rm.d1", n1, &d1));
+    TRY(dev_arr(ctx, "rm.d2", n2, &d2));
+    FNL_CUDA_TRY(cudaMemcpyAsync(d1, h_d1, n1 * 4, cudaMemcpyHostToDevice, ctx->stream));
+    FNL_CUDA_TRY(cudaMemcpyAsync(d2, h_d2, n2 * 4, cudaMemcpyHostToDevice, ctx->stream));
+    const uint32_t stride = derived_stride(h1, w1, cfg->k, cfg->grid_stride);
+    const uint32_t samples = ((h1 + stride - 1) / stride) * ((w1 + stride - 1) / stride);
+    uint32_t *dp, *dn;
+    TRY(dev_arr(ctx, "rm.pairs", (size_t)3 * std::max<uint32_t>(samples, 1), &dp));
+    TRY(dev_arr(ctx, "rm.np", 1, &dn));
+    fnl_run_stats local;
+    TRY(run_match(ctx, 1, d1, h1, w1, d2, h2, w2, dim, cfg, backend, dp, dn,
+                  stats ? stats : &local, true));
+    uint32_t n = 0;
+    FNL_CUDA_TRY(cudaMemcpyAsync(&n, dn, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    FNL_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (n && h_pairs)
+        FNL_CUDA_TRY(cudaMemcpyAsync(h_pairs, dp, (size_t)n * 12, cudaMemcpyDeviceToHost, ctx->stream));
+    FNL_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (n_pairs) *n_pairs = n;
+    return FNL_OK;
+}
+
+extern "C" int fnl_reciprocal_match_batch_device(fnl_context* ctx, uint32_t npairs,
+                                                 const float* d_d1, const float* d_d2, uint32_t h,
+                                                 uint32_t w, uint32_t dim,
+                                                 const fnl_match_config* cfg, int backend,
+                                                 uint32_t* d_pairs, uint32_t* d_n_pairs,
+                                                 fnl_run_stats* h_stats) {
+    TRY(check_device(ctx));
+    if (npairs == 0) return FNL_OK;
+    return run_match(ctx, npairs, d_d1, h, w, d_d2, h, w, dim, cfg, backend, d_pairs, d_n_pairs,
+                     h_stats, false);
+}
+
+extern "C" int fnl_reciprocal_match_batch(fnl_context* ctx, uint32_t npairs, const float* h_d1,
+                                          const float* h_d2, uint32_t h, uint32_t w, uint32_t dim,
+                                          const fnl_match_config* cfg, int backend,
+                                          uint32_t* h_pairs, uint32_t* n_pairs,
+                                          fnl_run_stats* stats) {
+    TRY(check_device(ctx));
+    TRY(check_cfg(cfg));
+    if (npairs == 0) return FNL_OK;
+    const uint64_t per_map = (uint64_t)h * w * dim;
+    const uint32_t stride = derived_stride(h, w, cfg->k, cfg->grid_stride);
+    const uint32_t samples = ((h + stride - 1) / stride) * ((w + stride - 1) / stride);
+    const uint32_t cap = std::max<uint32_t>(samples, 1);
+    // Sub-batches double-buffered: the copy engine uploads sub-batch k+1 while
+    // sub-batch k is matched.
+    const uint32_t sub = std::min<uint32_t>(npairs, 16);
+    float* dbuf[2][2];
+    TRY(dev_arr(ctx, "mb.d1a", sub * per_map, &dbuf[0][0]));
+    TRY(dev_arr(ctx, "mb.d2a", sub * per_map, &dbuf[0][1]));
+    TRY(dev_arr(ctx, "mb.d1b", sub * per_map, &dbuf[1][0]));
+    TRY(dev_arr(ctx, "mb.d2b", sub * per_map, &dbuf[1][1]));
+    uint32_t *dp, *dn;
+    TRY(dev_arr(ctx, "mb.pairs", (size_t)sub * 3 * cap, &dp));
+    TRY(dev_arr(ctx, "mb.np", sub, &dn));
+    cudaEvent_t ready[2], consumed[2];
+    for (int i = 0; i < 2; ++i) {
+        cudaEventCreateWithFlags(&ready[i], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&consumed[i], cudaEventDisableTiming);
+        cudaEventRecord(consumed[i], ctx->stream);
+    }
+    auto upload = [&](uint32_t first, int slot) -> int {
+        const uint32_t n = std::min(sub, npairs - first);
+        FNL_CUDA_TRY(cudaStreamWaitEvent(ctx->copy_stream, consumed[slot], 0));
+        FNL_CUDA_TRY(cudaMemcpyAsync(dbuf[slot][0], h_d1 + first * per_map, n * per_map * 4,
+                                     cudaMemcpyHostToDevice, ctx->copy_stream));
+        FNL_CUDA_TRY(cudaMemcpyAsync(dbuf[slot][1], h_d2 + first * per_map, n * per_map * 4,
+                                     cudaMemcpyHostToDevice, ctx->copy_stream));
+        FNL_CUDA_TRY(cudaEventRecord(ready[slot], ctx->copy_stream));
+        return FNL_OK;
+    };
+    int st = upload(0, 0);
+    for (uint32_t first = 0, k = 0; st == FNL_OK && first < npairs; first += sub, ++k) {
+        const int slot = k & 1;
+        const uint32_t n = std::min(sub, npairs - first);
+        if (first + sub < npairs) {
+            st = upload(first + sub, slot ^ 1);
+            if (st) break;
+        }
+        cudaStreamWaitEvent(ctx->stream, ready[slot], 0);
+        st = run_match(ctx, n, dbuf[slot][0], h, w, dbuf[slot][1], h, w, dim, cfg, backend, dp,
+                       dn, stats ? stats + first : nullptr, true);
+        if (st) break;
+        cudaEventRecord(consumed[slot], ctx->stream);
+        std::vector<uint32_t> cnt(n);
+        cudaMemcpyAsync(cnt.data(), dn, n * 4, cudaMemcpyDeviceToHost, ctx->stream);
+        if (h_pairs)
+            cudaMemcpyAsync(h_pairs + (size_t)first * 3 * cap, dp, (size_t)n * 3 * cap * 4,
+                            cudaMemcpyDeviceToHost, ctx->stream);
+        cudaError_t e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) {
+            st = fnl::fail_cuda(e, "batch readback", __FILE__, __LINE__);
+            break;
+        }
+        if (n_pairs) memcpy(n_pairs + first, cnt.data(), n * 4);
+    }
+    for (int i = 0; i < 2; ++i) {
+        cudaEventDestroy(ready[i]);
+        cudaEventDestroy(consumed[i]);
+    }
+    return st;
+}
+
+// ============================================================== mutual NN
+extern "C" int fnl_mutual_nn(fnl_context* ctx, const float* h_d1, uint32_t h1, uint32_t w1,
+                             const float* h_d2, uint32_t h2, uint32_t w2, uint32_t dim, int metric,
+                             uint32_t* h_pairs, uint32_t* n_pairs) {
+    TRY(check_device(ctx));
+    if (!valid_metric(metric)) return fail(FNL_EINVAL, "mutual_nn_exact: bad metric");
+    const uint32_t p1 = h1 * w1, p2 = h2 * w2;
+    if (p1 == 0 || p2 == 0 || dim == 0) return fail(FNL_EINVAL, "mutual_nn_exact: empty map");
+    const bool l2 = metric == FNL_METRIC_L2;
+    float *d1, *d2;
+    uint32_t *fwd, *bwd, *pairs, *cnt;
+    unsigned long long *k1, *k2;
+    TRY(dev_arr(ctx, "mu.d1", (size_t)p1 * dim, &d1));
+    TRY(dev_arr(ctx, "mu.d2", (size_t)p2 * dim, &d2));
+    TRY(dev_arr(ctx, "mu.fwd", p1, &fwd));
+    TRY(dev_arr(ctx, "mu.bwd", p2, &bwd));
+    TRY(dev_arr(ctx, "mu.k1", p1, &k1));
+    TRY(dev_arr(ctx, "mu.k2", p2, &k2));
+    TRY(dev_arr(ctx, "mu.pairs", (size_t)2 * p1 + 2, &pairs));
+    TRY(dev_arr(ctx, "mu.cnt", 1, &cnt));
+    cudaStream_t s = ctx->stream;
+    FNL_CUDA_TRY(cudaMemcpyAsync(d1, h_d1, (size_t)p1 * dim * 4, cudaMemcpyHostToDevice, s));
+    FNL_CUDA_TRY(cudaMemcpyAsync(d2, h_d2, (size_t)p2 * dim * 4, cudaMemcpyHostToDevice, s));
+    FNL_CUDA_TRY(cudaMemsetAsync(k1, 0xFF, (size_t)p1 * 8, s));
+    FNL_CUDA_TRY(cudaMemsetAsync(k2, 0xFF, (size_t)p2 * 8, s));
+    auto pass = [&](const float* q, uint32_t nq, const float* t, uint32_t nt,
+                    unsigned long long* keys, uint32_t* out) -> int {
+        fnl::ScanArgs sa{};
+        sa.qmap = q;
+        sa.qcount_const = nq;
+        sa.tmap = t;
+        sa.nt = nt;
+        sa.dim = dim;
+        sa.keys = keys;
+        sa.keys_pair_stride = nq;
+        fnl::FinalizeArgs fa{};
+        fa.keys = keys;
+        fa.keys_pair_stride = nq;
+        fa.qcount_const = nq;
+        fa.nearest = out;
+        fa.nearest_pair_stride = nq;
+        fa.dot = !l2;
+        return exact_nn(ctx, sa, nq, 1, l2, false, fa);
+    };
+    TRY(pass(d1, p1, d2, p2, k1, fwd));
+    TRY(pass(d2, p2, d1, p1, k2, bwd));
+    FNL_CUDA_TRY(fnl::launch_mutual_filter(fwd, bwd, p1, pairs, cnt, s));
+    uint32_t n = 0;
+    FNL_CUDA_TRY(cudaMemcpyAsync(&n, cnt, 4, cudaMemcpyDeviceToHost, s));
+    FNL_CUDA_TRY(cudaStreamSynchronize(s));
+    if (n && h_pairs)
+        FNL_CUDA_TRY(cudaMemcpyAsync(h_pairs, pairs, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+    FNL_CUDA_TRY(cudaStreamSynchronize(s));
+    timing_harvest(ctx);
+    if (n_pairs) *n_pairs = n;
+    return FNL_OK;
+}

@@ -1,0 +1,111 @@
+// fnl_internal.h -- launchers shared by the .cu translation units of
+// libfastnn_b200.so.  Not part of the public ABI (include/fastnn_b200.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+namespace fnl {
+
+// thread-local error plumbing (capi.cu)
+int fail(int status, const std::string& msg);
+int fail_cuda(cudaError_t e, const char* expr, const char* file, int line);
+
+// ---------------------------------------------------------------- K1 prepare
+// Validates finiteness (first offending flat index into *bad_index, which the
+// caller initialises to UINT64_MAX), and for hybrid writes the binary16-rounded
+// copy `rounded` plus per-row saturation counts `row_sat` and the map total.
+struct PrepareArgs {
+    const float* src;
+    float* rounded;              // may be null (full precision)
+    uint8_t* row_sat;            // may be null; one byte per row (saturating channels, <=255 kept)
+    unsigned long long* total_sat;
+    unsigned long long* bad_index;
+    uint64_t rows;
+    uint32_t dim;
+};
+cudaError_t launch_prepare(const PrepareArgs& a, cudaStream_t s);
+
+// ---------------------------------------------------------------- K4 exact scan
+// Fused score + lowest-index argmin of gathered query rows against a target
+// map, bit-identical to src/kernels.cpp:137-233.  Batched over pairs
+// (gridDim.z), split over target ranges (gridDim.y) and merged with a 64-bit
+// atomicMin on packed (orderable dist, index) keys.
+struct ScanArgs {
+    const float* qmap;            // query map rows (fp32, rounded for hybrid)
+    uint64_t qmap_pair_stride;    // floats between consecutive pairs' maps
+    const uint32_t* qids;         // per pair query pixel ids, or null = identity
+    uint32_t qids_pair_stride;
+    const uint32_t* qcount;       // per pair active query count, or null
+    uint32_t qcount_const;        // used when qcount is null
+    const uint8_t* pair_done;     // per pair skip flag, or null
+    const uint8_t* q_row_sat;     // hybrid: saturations of each query-map row, or null
+    uint64_t q_row_sat_pair_stride;
+    const float* tmap;            // target map rows (fp32, rounded for hybrid)
+    uint64_t tmap_pair_stride;
+    uint32_t nt;
+    uint32_t dim;
+    uint32_t split_len;           // targets per gridDim.y slice
+    unsigned long long* keys;     // per pair x query packed keys (init ~0)
+    uint32_t keys_pair_stride;
+    unsigned long long* counters; // [0] query-row saturations, [1] distance saturations
+};
+// max_q: upper bound of queries per pair (sizes gridDim.x)
+cudaError_t launch_exact_scan(const ScanArgs& a, uint32_t max_q, uint32_t npairs, bool l2,
+                              bool hybrid, cudaStream_t s);
+
+// keys -> nearest / min_dist; resets keys to ~0 for the next call.
+struct FinalizeArgs {
+    unsigned long long* keys;
+    uint32_t keys_pair_stride;
+    const uint32_t* qcount;
+    uint32_t qcount_const;
+    const uint8_t* pair_done;
+    uint32_t* nearest;            // per pair x query
+    uint32_t nearest_pair_stride;
+    float* min_dist;              // may be null
+    bool dot;                     // exact zero distance is -0.0f under NegativeDot
+};
+cudaError_t launch_finalize(const FinalizeArgs& a, uint32_t max_q, uint32_t npairs, cudaStream_t s);
+
+// Materialising scorer (src/kernels.cpp:235-273, block_distances :377-400).
+cudaError_t launch_block_distances(const float* q, uint32_t nq, const float* t, uint32_t nt,
+                                   uint32_t dim, bool l2, bool hybrid, float* out,
+                                   unsigned long long* dist_sat, cudaStream_t s);
+
+// ---------------------------------------------------------------- K5/K6 matcher
+struct MatchState {
+    uint32_t npairs;
+    uint32_t cap;                 // samples per pair (capacity of the active arrays)
+    uint32_t samples;
+    uint32_t h1, w1, p1, p2;
+    uint32_t grid_stride;         // effective (derived when cfg.k > 0)
+    uint32_t max_iters;
+    double convergence;
+    uint32_t* active_u;           // [npairs][cap]
+    uint32_t* active_v;           // [npairs][cap]
+    uint32_t* back;               // [npairs][cap]
+    uint32_t* n_active;           // [npairs]
+    uint8_t* done;                // [npairs]
+    uint32_t* used_i;             // [npairs][ceil(p1/32)]
+    uint32_t* used_j;             // [npairs][ceil(p2/32)]
+    uint32_t words_i, words_j;
+    uint32_t* pairs;              // [npairs][3*cap]
+    uint32_t* n_pairs;            // [npairs]
+    uint32_t* stats;              // [npairs][kStatWords] (see below)
+    unsigned int* n_done;         // scalar
+};
+// stats words per pair: converged, duplicates, iterations, history_len, history[FNL_MAX_ITERS]
+constexpr int kStatConverged = 0, kStatDups = 1, kStatIters = 2, kStatHistLen = 3, kStatHist = 4;
+constexpr int kStatWords = 4 + 64;
+
+cudaError_t launch_match_init(const MatchState& m, cudaStream_t s);
+cudaError_t launch_harvest(const MatchState& m, uint32_t iteration, cudaStream_t s);
+
+// exhaustive mutual filter: i kept iff bwd[fwd[i]] == i, in ascending i
+cudaError_t launch_mutual_filter(const uint32_t* fwd, const uint32_t* bwd, uint32_t n,
+                                 uint32_t* pairs, uint32_t* count, cudaStream_t s);
+
+}  // namespace fnl
