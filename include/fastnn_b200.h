@@ -157,6 +157,14 @@ int fnl_mutual_nn(fnl_context* ctx, const float* h_d1, uint32_t h1, uint32_t w1,
                   const float* h_d2, uint32_t h2, uint32_t w2, uint32_t dim, int metric,
                   uint32_t* h_pairs, uint32_t* n_pairs);
 
+/* ---- diagnostics -------------------------------------------------------------
+ * Raw tensor-core scores (fp32 TMEM accumulators) of 256 query rows against 128
+ * target rows after the binary16 pack: h_scores[256][128].  dot: q.t;
+ * l2: q.t - |t|^2/2.  Used by the tests to pin the UMMA operand layout and to
+ * measure the accumulation error the certification margin must cover. */
+int fnl_tensor_selftest(fnl_context* ctx, const float* h_queries, const float* h_targets,
+                        uint32_t dim, int metric, float* h_scores);
+
 /* ---- instrumentation -------------------------------------------------------
  * Device time (ms, CUDA events on the context stream) of the dominant scoring
  * kernel summed since the last reset, and its launch count. */

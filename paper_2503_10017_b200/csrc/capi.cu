@@ -254,6 +254,35 @@ int exact_nn(fnl_context* ctx, const fnl::ScanArgs& sa, uint32_t max_q, uint32_t
 
 }  // namespace
 
+// ============================================================== services
+namespace fnl {
+cudaStream_t ctx_stream(fnl_context* ctx) { return ctx->stream; }
+int ctx_sm_count(fnl_context* ctx) { return ctx->sm_count; }
+int ws_device(fnl_context* ctx, const char* name, size_t bytes, void** out) {
+    return dev_buf(ctx, name, bytes, out);
+}
+int ws_pinned(fnl_context* ctx, const char* name, size_t bytes, void** out) {
+    auto& b = ctx->pinned[name];
+    if (b.bytes < bytes) {
+        if (b.p) cudaFreeHost(b.p);
+        b.p = nullptr;
+        b.bytes = 0;
+        const size_t want = std::max<size_t>(bytes, 256);
+        cudaError_t e = cudaMallocHost(&b.p, want);
+        if (e != cudaSuccess) return fail_cuda(e, name, __FILE__, __LINE__);
+        b.bytes = want;
+    }
+    *out = b.p;
+    return FNL_OK;
+}
+void ctx_score_begin(fnl_context* ctx, cudaEvent_t* end_event) {
+    cudaEvent_t a;
+    timing_begin(ctx, &a, end_event);
+}
+void ctx_score_end(fnl_context* ctx, cudaEvent_t end_event) { timing_end(ctx, end_event); }
+void ctx_count_launches(fnl_context* ctx, int n) { ctx->total_launches += n; }
+}  // namespace fnl
+
 // ============================================================== lifetime
 extern "C" int fnl_abi_version(void) { return FNL_ABI_VERSION; }
 
@@ -557,11 +586,36 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
     FNL_CUDA_TRY(cudaMemsetAsync(counters, 0, (size_t)max_calls * npairs * 16, s));
     FNL_CUDA_TRY(cudaMemsetAsync(bad, 0xFF, 16, s));
 
-    // ---- K1: validate + (hybrid) round
+    // ---- K1: validate + (hybrid) round, or binary16 pack for the tensor path
+    const bool tensor = backend == FNL_BACKEND_TENSOR;
     Prepared P1, P2;
-    TRY(prepare_maps(ctx, "m.p1", d_d1, npairs, p1, dim, hyb, validate, &P1, bad));
-    TRY(prepare_maps(ctx, "m.p2", d_d2, npairs, p2, dim, hyb, validate, &P2, bad + 1));
-    if (validate) {
+    fnl::PackedMaps T1, T2;
+    unsigned long long *near_ties = nullptr, *tsat = nullptr;
+    TRY(dev_arr(ctx, "m.neartie", npairs, &near_ties));
+    TRY(dev_arr(ctx, "m.tsat", 2 * (size_t)npairs, &tsat));
+    FNL_CUDA_TRY(cudaMemsetAsync(near_ties, 0, (size_t)npairs * 8, s));
+    FNL_CUDA_TRY(cudaMemsetAsync(tsat, 0, (size_t)npairs * 16, s));
+    if (tensor) {
+        unsigned long long* tbad;
+        TRY(dev_arr(ctx, "m.tbad", 2 * (size_t)npairs, &tbad));
+        FNL_CUDA_TRY(cudaMemsetAsync(tbad, 0xFF, (size_t)npairs * 16, s));
+        TRY(fnl::tensor_pack(ctx, "m.t1", d_d1, npairs, p1, dim, l2, tbad, tsat, &T1));
+        TRY(fnl::tensor_pack(ctx, "m.t2", d_d2, npairs, p2, dim, l2, tbad + npairs, tsat + npairs, &T2));
+        // fold the per-pair first bad index into the shared slots (min over pairs)
+        std::vector<unsigned long long> hb(2 * (size_t)npairs);
+        FNL_CUDA_TRY(cudaMemcpyAsync(hb.data(), tbad, hb.size() * 8, cudaMemcpyDeviceToHost, s));
+        FNL_CUDA_TRY(cudaStreamSynchronize(s));
+        if (validate) {
+            for (uint32_t p = 0; p < npairs; ++p)
+                if (hb[p] != ~0ull) return fail(FNL_EINVAL, nonfinite_msg(hb[p]));
+            for (uint32_t p = 0; p < npairs; ++p)
+                if (hb[npairs + p] != ~0ull) return fail(FNL_EINVAL, nonfinite_msg(hb[npairs + p]));
+        }
+    } else {
+        TRY(prepare_maps(ctx, "m.p1", d_d1, npairs, p1, dim, hyb, validate, &P1, bad));
+        TRY(prepare_maps(ctx, "m.p2", d_d2, npairs, p2, dim, hyb, validate, &P2, bad + 1));
+    }
+    if (validate && !tensor) {
         // D1 is checked before D2, as the reference converts D1 first
         // (bindings/module.cpp:232-233); indices are flat within one map.
         unsigned long long hb[2] = {~0ull, ~0ull};
@@ -577,14 +631,17 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
 
     // ---- NN pass helper: queries = rows of qmap at ids, targets = tmap
     uint32_t call = 0;
+    // host mirror of the per-pair active counts / done flags (tensor work lists)
+    std::vector<uint32_t> h_active(npairs, samples);
+    std::vector<uint8_t> h_done(npairs, samples == 0 ? 1 : 0);
     auto nn_pass = [&](const Prepared& Q, uint32_t qrows, const uint32_t* ids, const Prepared& Tm,
                        uint32_t nt, uint32_t* out) -> int {
-        if (backend == FNL_BACKEND_TENSOR) {
-            TRY(fnl::tensor_nn_gathered(ctx, npairs, Q.data, (uint64_t)qrows * dim, ids, cap,
-                                        m.n_active, m.done, Tm.data, (uint64_t)nt * dim, nt, dim,
-                                        l2, out, cap));
+        if (tensor) {
+            const fnl::PackedMaps& TQ = (qrows == p1 && ids == m.active_u) ? T1 : T2;
+            const fnl::PackedMaps& TT = (qrows == p1 && ids == m.active_u) ? T2 : T1;
             ++call;
-            return FNL_OK;
+            return fnl::tensor_nn_pass(ctx, npairs, TQ, ids, cap, h_active.data(), h_done.data(), TT, dim,
+                                       l2, out, cap, nullptr, near_ties);
         }
         fnl::ScanArgs sa{};
         sa.qmap = Q.data;
@@ -629,6 +686,10 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
         ctx->total_launches += 1;
         unsigned int ndone = 0;
         FNL_CUDA_TRY(cudaMemcpyAsync(&ndone, m.n_done, 4, cudaMemcpyDeviceToHost, s));
+        if (tensor) {
+            FNL_CUDA_TRY(cudaMemcpyAsync(h_active.data(), m.n_active, npairs * 4, cudaMemcpyDeviceToHost, s));
+            FNL_CUDA_TRY(cudaMemcpyAsync(h_done.data(), m.done, npairs, cudaMemcpyDeviceToHost, s));
+        }
         FNL_CUDA_TRY(cudaStreamSynchronize(s));
         if (ndone >= npairs) break;
         timer.begin(kPhaseForward);
@@ -647,6 +708,9 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
         FNL_CUDA_TRY(cudaMemcpyAsync(ms1.data(), P1.map_sat, npairs * 8, cudaMemcpyDeviceToHost, s));
         FNL_CUDA_TRY(cudaMemcpyAsync(ms2.data(), P2.map_sat, npairs * 8, cudaMemcpyDeviceToHost, s));
         FNL_CUDA_TRY(cudaMemcpyAsync(npr.data(), m.n_pairs, npairs * 4, cudaMemcpyDeviceToHost, s));
+        std::vector<unsigned long long> tsat_h(2 * (size_t)npairs), ties_h(npairs);
+        FNL_CUDA_TRY(cudaMemcpyAsync(tsat_h.data(), tsat, tsat_h.size() * 8, cudaMemcpyDeviceToHost, s));
+        FNL_CUDA_TRY(cudaMemcpyAsync(ties_h.data(), near_ties, ties_h.size() * 8, cudaMemcpyDeviceToHost, s));
         FNL_CUDA_TRY(cudaStreamSynchronize(s));
         double phase_us[4] = {0, 0, 0, 0};
         timer.collect(phase_us);
@@ -695,9 +759,9 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
                     if (hyb) o.half_saturation_events += tsat + qs + ds;
                 }
             }
-            if (backend == FNL_BACKEND_TENSOR) {
-                o.half_saturation_events = ms1[p] + ms2[p];
-                o.near_tie_rows = fnl::tensor_near_tie_rows(ctx, p);
+            if (tensor) {
+                o.half_saturation_events = tsat_h[p] + tsat_h[npairs + p];
+                o.near_tie_rows = ties_h[p];
             }
         }
     }
@@ -818,6 +882,21 @@ extern "C" int fnl_reciprocal_match_batch(fnl_context* ctx, uint32_t npairs, con
         cudaEventDestroy(consumed[i]);
     }
     return st;
+}
+
+// ============================================================== diagnostics
+extern "C" int fnl_tensor_selftest(fnl_context* ctx, const float* h_q, const float* h_t, uint32_t dim,
+                                   int metric, float* h_scores) {
+    TRY(check_device(ctx));
+    float *dq, *dt, *dout;
+    TRY(dev_arr(ctx, "st.q", (size_t)256 * dim, &dq));
+    TRY(dev_arr(ctx, "st.t", (size_t)128 * dim, &dt));
+    TRY(dev_arr(ctx, "st.out", (size_t)256 * 128, &dout));
+    FNL_CUDA_TRY(cudaMemcpyAsync(dq, h_q, (size_t)256 * dim * 4, cudaMemcpyHostToDevice, ctx->stream));
+    FNL_CUDA_TRY(cudaMemcpyAsync(dt, h_t, (size_t)128 * dim * 4, cudaMemcpyHostToDevice, ctx->stream));
+    TRY(fnl::tensor_selftest_scores(ctx, dq, dt, dim, metric == FNL_METRIC_L2, dout));
+    FNL_CUDA_TRY(cudaMemcpy(h_scores, dout, (size_t)256 * 128 * 4, cudaMemcpyDeviceToHost));
+    return FNL_OK;
 }
 
 // ============================================================== mutual NN

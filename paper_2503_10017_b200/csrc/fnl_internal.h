@@ -13,6 +13,27 @@ namespace fnl {
 int fail(int status, const std::string& msg);
 int fail_cuda(cudaError_t e, const char* expr, const char* file, int line);
 
+// context services (capi.cu) for the other translation units
+}  // namespace fnl
+struct fnl_context;
+namespace fnl {
+cudaStream_t ctx_stream(fnl_context* ctx);
+int ctx_sm_count(fnl_context* ctx);
+// grow-only named device / pinned-host workspace slots
+int ws_device(fnl_context* ctx, const char* name, size_t bytes, void** out);
+int ws_pinned(fnl_context* ctx, const char* name, size_t bytes, void** out);
+template <typename T>
+int ws_arr(fnl_context* ctx, const char* name, size_t count, T** out) {
+    void* p = nullptr;
+    const int st = ws_device(ctx, name, count * sizeof(T), &p);
+    *out = static_cast<T*>(p);
+    return st;
+}
+// brackets one launch of the dominant scoring kernel (CUDA events)
+void ctx_score_begin(fnl_context* ctx, cudaEvent_t* end_event);
+void ctx_score_end(fnl_context* ctx, cudaEvent_t end_event);
+void ctx_count_launches(fnl_context* ctx, int n);
+
 // ---------------------------------------------------------------- K1 prepare
 // Validates finiteness (first offending flat index into *bad_index, which the
 // caller initialises to UINT64_MAX), and for hybrid writes the binary16-rounded

@@ -1,4 +1,13 @@
-// tensor_scan.h -- K3: tcgen05 HybridCast score + certified argmax (tensor_scan.cu).
+// tensor_scan.h -- K1 pack, K2 gather, K3 tcgen05 HybridCast score + certified
+// argmax, K3b merge, K4' exact re-decision of near ties (tensor_scan.cu).
+//
+// Numeric contract of the tensor backend: descriptors are cast to binary16 once
+// (RNE, +-65504 saturation), scored on the 5th-gen tensor cores with fp32
+// accumulation (Alg. 3, HybridCast), and every row whose tensor-core
+// top-2 gap is not provably larger than the accumulated rounding error is
+// re-decided by the reference FMA chain on the same binary16 values.  The
+// nearest indices are therefore identical to the reference `single` backend run
+// on binary16-rounded maps (src/nn.cpp:134-164 on to_half_round(D)).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -8,19 +17,49 @@ struct fnl_context;
 
 namespace fnl {
 
-// Dense: every row of d_q (nq x dim fp32) against d_t (nt x dim fp32).
+constexpr uint32_t kPackK = 32;            // binary16 channels per packed row
+constexpr uint32_t kPackRowBytes = 64;     // 32 x 2 B
+constexpr uint32_t kTileRows = 128;        // rows per UMMA operand tile
+constexpr uint32_t kTileBytes = kTileRows * kPackRowBytes;  // 8 KB
+constexpr uint32_t kQueryTilePair = 256;   // query rows per CTA (two M=128 tiles)
+
+// Maps in the UMMA canonical K-major no-swizzle layout: rows grouped by 8
+// (512 B per group), inside a group channel chunk kc (8 halves, 16 B) at
+// kc*128 and row r%8 at (r%8)*16.  A run of 128 rows is one contiguous 8 KB
+// operand tile, so a single cp.async.bulk stages it.
+struct PackedMaps {
+    uint8_t* data = nullptr;
+    uint64_t pair_bytes = 0;  // bytes per pair's map (rows padded to 128)
+    uint32_t rows = 0;        // real rows per map
+    uint32_t npairs = 0;
+    float* max_norm = nullptr;  // per pair: max L2 norm of a binary16 row (device)
+};
+
+// K1: fp32 maps (npairs x rows x dim, device) -> packed binary16.  Role
+// "target" stores -|t|^2/2 split over channels dim, dim+1 for the l2 metric.
+// Non-finite values: first flat index per map into d_bad[pair] (init ~0).
+// Saturations per pair added into d_sat[pair].
+int tensor_pack(fnl_context* ctx, const char* tag, const float* d_src, uint32_t npairs, uint32_t rows,
+                uint32_t dim, bool l2, unsigned long long* d_bad, unsigned long long* d_sat,
+                PackedMaps* out);
+
+// One NN pass of gathered query rows against target maps, batched over pairs.
+// Query rows of pair p: ids[p*cap + i] (or i when ids is null), i < h_active[p];
+// pairs with h_active[p] == 0 or h_done[p] are skipped.  Winner indices land in
+// out[p*out_stride + i]; if min_dist is non-null the exact reference distance of
+// the winner is written beside it.  d_near_ties[p] counts re-decided rows.
+int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const uint32_t* ids,
+                   uint32_t cap, const uint32_t* h_active, const uint8_t* h_done,
+                   const PackedMaps& T, uint32_t dim, bool l2, uint32_t* out, uint32_t out_stride,
+                   float* min_dist, unsigned long long* d_near_ties);
+
+// Dense convenience (fnl_nn_query backend TENSOR): all rows of d_q against d_t.
 int tensor_nn_dense(fnl_context* ctx, const float* d_q, uint32_t nq, const float* d_t, uint32_t nt,
                     uint32_t dim, bool l2, uint32_t* d_nearest, float* d_min_dist);
 
-// Gathered, batched over pairs, driven by the matcher state: queries of pair p
-// are rows ids[p*cap + i] (i < n_active[p]) of qmap + p*q_stride; pairs with
-// done[p] are skipped.  Winners land in out[p*out_stride + i].
-int tensor_nn_gathered(fnl_context* ctx, uint32_t npairs, const float* qmap, uint64_t q_stride,
-                       const uint32_t* ids, uint32_t cap, const uint32_t* n_active,
-                       const uint8_t* done, const float* tmap, uint64_t t_stride, uint32_t nt,
-                       uint32_t dim, bool l2, uint32_t* out, uint32_t out_stride);
-
-// Rows of pair p re-decided by the exact chain since the matcher started.
-uint64_t tensor_near_tie_rows(fnl_context* ctx, uint32_t pair);
+// Self-test: raw tensor-core scores of a packed query tile pair (256 rows)
+// against one packed target tile (128 rows) -> out[256][128] fp32.
+int tensor_selftest_scores(fnl_context* ctx, const float* d_q, const float* d_t, uint32_t dim,
+                           bool l2, float* d_out);
 
 }  // namespace fnl
