@@ -705,8 +705,10 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
         std::vector<uint32_t> npr(npairs);
         FNL_CUDA_TRY(cudaMemcpyAsync(st.data(), m.stats, st.size() * 4, cudaMemcpyDeviceToHost, s));
         FNL_CUDA_TRY(cudaMemcpyAsync(cnt.data(), counters, cnt.size() * 8, cudaMemcpyDeviceToHost, s));
-        FNL_CUDA_TRY(cudaMemcpyAsync(ms1.data(), P1.map_sat, npairs * 8, cudaMemcpyDeviceToHost, s));
-        FNL_CUDA_TRY(cudaMemcpyAsync(ms2.data(), P2.map_sat, npairs * 8, cudaMemcpyDeviceToHost, s));
+        if (!tensor) {
+            FNL_CUDA_TRY(cudaMemcpyAsync(ms1.data(), P1.map_sat, npairs * 8, cudaMemcpyDeviceToHost, s));
+            FNL_CUDA_TRY(cudaMemcpyAsync(ms2.data(), P2.map_sat, npairs * 8, cudaMemcpyDeviceToHost, s));
+        }
         FNL_CUDA_TRY(cudaMemcpyAsync(npr.data(), m.n_pairs, npairs * 4, cudaMemcpyDeviceToHost, s));
         std::vector<unsigned long long> tsat_h(2 * (size_t)npairs), ties_h(npairs);
         FNL_CUDA_TRY(cudaMemcpyAsync(tsat_h.data(), tsat, tsat_h.size() * 8, cudaMemcpyDeviceToHost, s));
