@@ -1,0 +1,359 @@
+#!/usr/bin/env python3
+"""FastNN-Lite pair-matching throughput on B200 (BASELINE.json metric).
+
+A step = the full reciprocal matching hot path (K1 pack -> iterative K2 gather /
+K3 tcgen05 score+argmax / merge / near-tie rescan / K5 harvest until
+convergence) over one batch of PAIRS_PER_GPU synthetic 512x384 d=24 pairs per
+GPU (config C2 shape, batched as in C4).  Pairs are independent, so ranks
+shard them with no data-path collective ("scaling": "weak").
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--pairs B]
+  python bench.py --impl reference ...   # the reference CPU path on the host
+
+value : device-resident throughput (maps already in HBM), CUDA events on the
+        launching stream, barrier + synchronize on both sides, max over ranks.
+e2e   : the public batch API (paper_2503_10017_b200.reciprocal_match_batch) on
+        pinned HOST maps: H2D of every step's inputs and D2H of its matches are
+        inside the timed region.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+H, W, D, STRIDE = 512, 384, 24, 8
+METRIC = "dot"                     # MASt3R descriptors are unit norm
+NT = H * W
+FLOP_PER_SCORE = 2 * D             # algorithmic: 2d per (query, target) score, d=24 unpadded
+POOL = 64                          # distinct synthetic maps, seeds 1000.. (gen_random, reference generator)
+METRIC_NAME = "image pairs/sec FastNN-Lite @512x384 d=24 (1/2/4/8 B200); % tensor-pipe peak"
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["bf16_tflops"]), float(p.get("bf16_tflops_sustained", 0) or 0), "measured"
+    except Exception:
+        return 1590.0, 1400.0, "fallback"
+
+
+def gen_pool(gen_random):
+    return [gen_random(H, W, D, 1000 + i) for i in range(POOL)]
+
+
+def pair_maps(k):
+    """Pair k of the synthetic stream: two distinct pool maps."""
+    a = k % POOL
+    b = (a + 1 + (k // POOL) * 7 + (k % 5)) % POOL
+    if b == a:
+        b = (a + 1) % POOL
+    return a, b
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                try:
+                    rows.append((float(parts[0]), float(parts[1]), parts[3:7]))
+                except ValueError:
+                    pass
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v.lower() == "active"})
+        loaded = [r[0] for r in rows if r[0] > 300] or [r[0] for r in rows]
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_setup():
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    return world, rank, local
+
+
+def allreduce(vals, op):
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return vals
+    dev = "cuda" if torch.cuda.is_available() and dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor(vals, dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=op)
+    return t.tolist()
+
+
+def barrier():
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        dist.barrier()
+
+
+# ---------------------------------------------------------------- reference arm
+def ref_threads():
+    return max(1, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1))
+
+
+def run_reference_pairs(ref, pool, first, count):
+    """The unmodified reference FastNN path (oracle/_ref, compiled from
+    /root/reference): reciprocal_match backend=single, dot, all host threads,
+    block_size = ceil(samples / threads) so every thread gets a query block."""
+    threads = ref_threads()
+    samples = math.ceil(H / STRIDE) * math.ceil(W / STRIDE)
+    bs = math.ceil(samples / threads)
+    t0 = time.perf_counter()
+    for k in range(first, first + count):
+        a, b = pair_maps(k)
+        ref.reciprocal_match(pool[a], pool[b], backend="single", metric=METRIC, stride=STRIDE,
+                             block_size=bs, threads=threads)
+    return time.perf_counter() - t0, threads
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def main_reference(args):
+    world, rank, _ = dist_setup()
+    if rank != 0:
+        return
+    from oracle import oracle
+    ref = oracle.reference()
+    pool = gen_pool(ref.gen_random)
+    per_step = 1
+    for i in range(args.warmup):
+        run_reference_pairs(ref, pool, i, per_step)
+    total, threads = 0.0, ref_threads()
+    for i in range(args.steps):
+        dt, threads = run_reference_pairs(ref, pool, args.warmup + i, per_step)
+        total += dt
+    pairs = args.steps * per_step
+    value = pairs / total
+    line = {
+        "impl": "reference", "metric": METRIC_NAME, "value": value, "unit": "pairs/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference gen_random, 64-map pool)",
+        "config": {"workload": "C2: FastNN reciprocal match, 512x384 d=24, stride 8, dot; reference "
+                               "CPU path (backend single), 1 pair per step", "pairs_per_step": per_step,
+                   "threads": threads, "cpu": cpu_model()},
+        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": threads, "kind": "reference",
+                         "sample": f"{pairs} C2 pairs, reference reciprocal_match single/dot, "
+                                   f"{threads} threads"},
+        "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- B200 arm
+def main_b200(args):
+    import torch
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    import paper_2503_10017_b200 as fnl
+    fnl.set_device(local)
+    B = args.pairs
+    first_pair = rank * B
+    pool = gen_pool(fnl.gen_random)
+    samples = math.ceil(H / STRIDE) * math.ceil(W / STRIDE)
+
+    # device-resident inputs (value) and pinned host copies (e2e)
+    h1 = torch.empty((B, H, W, D), dtype=torch.float32, pin_memory=True)
+    h2 = torch.empty((B, H, W, D), dtype=torch.float32, pin_memory=True)
+    for i in range(B):
+        a, b = pair_maps(first_pair + i)
+        h1[i].copy_(torch.from_numpy(pool[a]))
+        h2[i].copy_(torch.from_numpy(pool[b]))
+    d1 = h1.to("cuda", non_blocking=False)
+    d2 = h2.to("cuda", non_blocking=False)
+    out_pairs = torch.empty((B, samples, 3), dtype=torch.int32, device="cuda")
+    out_counts = torch.empty((B,), dtype=torch.int32, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step_device():
+        return fnl.reciprocal_match_device(d1.data_ptr(), d2.data_ptr(), B, H, W, D, out_pairs.data_ptr(),
+                                           out_counts.data_ptr(), backend=args.backend, stride=STRIDE,
+                                           metric=METRIC, stream=stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize()
+    fnl.kernel_timing(reset=True)
+    query_rows, near_ties = 0, 0
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            stats = step_device()
+            query_rows += sum(s["query_rows"] for s in stats)
+            near_ties += sum(s["near_tie_rows"] for s in stats)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    elapsed_ms = ev0.elapsed_time(ev1)
+    timing = fnl.kernel_timing(reset=True)
+    matches_last = int(out_counts.sum().item())
+
+    # ---- e2e through the public host-buffer batch API
+    n1, n2 = h1.numpy(), h2.numpy()
+    for _ in range(max(1, args.warmup // 2)):
+        fnl.reciprocal_match_batch(n1, n2, backend=args.backend, stride=STRIDE, metric=METRIC)
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        pairs_h, counts_h, _ = fnl.reciprocal_match_batch(n1, n2, backend=args.backend, stride=STRIDE,
+                                                          metric=METRIC)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    barrier()
+
+    # ---- max over ranks
+    max_ms, max_e2e = allreduce([elapsed_ms, e2e_s], op=__import__("torch").distributed.ReduceOp.MAX) \
+        if world > 1 else (elapsed_ms, e2e_s)
+    tot_rows, tot_score_ms, tot_launch = allreduce([query_rows, timing["score_ms"], timing["score_launches"]],
+                                                   op=__import__("torch").distributed.ReduceOp.SUM) \
+        if world > 1 else (query_rows, timing["score_ms"], timing["score_launches"])
+
+    # ---- CPU baseline (rank 0, N=1 only): the reference on a bounded sample
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle
+        ref = oracle.reference()
+        done, spent, threads = 0, 0.0, ref_threads()
+        while done < 1 or (spent < args.cpu_seconds and done < 64):
+            dt, threads = run_reference_pairs(ref, pool, done, 1)
+            spent += dt
+            done += 1
+        cpu = {"value": done / spent, "unit": "pairs/s", "cores": threads, "kind": "reference",
+               "sample": f"{done} C2 pairs (512x384 d=24 stride 8, dot), reference reciprocal_match "
+                         f"backend=single, {threads} threads, {spent:.1f} s; host CPU {cpu_model()}"}
+
+    if rank != 0:
+        return
+    pairs_total = B * world * args.steps
+    value = pairs_total / (max_ms / 1000.0)
+    e2e_value = B * world * args.e2e_steps / max_e2e
+    peak_burst, peak_sust, peak_kind = peaks()
+    flops = FLOP_PER_SCORE * NT * tot_rows
+    achieved = flops / (tot_score_ms / 1000.0) / 1e12 if tot_score_ms > 0 else None
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "tc_scan_ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC_NAME, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f16", "data": "synthetic",
+        "config": {"workload": "C2/C4: FastNN-Lite reciprocal matching of 512x384 d=24 pairs, stride 8 "
+                               "(3072 samples), T=10, convergence 0.99, dot metric, tensor backend "
+                               "(binary16 in / fp32 accumulate, exact near-tie re-decision)",
+                   "pairs_per_gpu_per_step": B, "global_batch": B * world, "height": H, "width": W,
+                   "dim": D, "stride": STRIDE, "backend": args.backend, "parallelism": f"pairs dp{world}",
+                   "inputs": f"pool of {POOL} gen_random maps (seeds 1000..{1000 + POOL - 1}), pair k = "
+                             f"(map k%64, distinct partner); {B * 2 * H * W * D * 4 / 1e9:.2f} GB fp32 "
+                             "per GPU per step > 126 MB L2 (no L2 flush needed)",
+                   "query_rows_per_step": tot_rows / args.steps,
+                   "near_tie_rows_per_step": near_ties / args.steps if world == 1 else None,
+                   "matches_per_step_rank0": matches_last},
+        "e2e": {"value": e2e_value, "unit": "pairs/s",
+                "h2d_bytes_per_step": int(2 * B * H * W * D * 4),
+                "d2h_bytes_per_step": int(B * samples * 3 * 4 + B * 4)},
+        "gpu_launches": int(timing["total_launches"]),
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_burst, "unit": "TFLOP/s",
+                     "frac": (achieved / peak_burst) if achieved else None, "traffic": traffic,
+                     "kernel": "tc_scan_kernel (tcgen05 score + running argmax)",
+                     "flop_per_score": FLOP_PER_SCORE, "peak_kind": f"{peak_kind} bf16 dense burst",
+                     "frac_of_sustained": (achieved / peak_sust) if (achieved and peak_sust) else None,
+                     "kernel_share_of_step": (tot_score_ms / world) / max_ms / 1.0,
+                     "avg_launch_ms": tot_score_ms / max(1, tot_launch)},
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--pairs", type=int, default=128, help="pairs per GPU per step")
+    ap.add_argument("--backend", default="tensor")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        main_reference(args)
+    else:
+        main_b200(args)
+
+
+if __name__ == "__main__":
+    main()
