@@ -161,9 +161,11 @@ int fnl_mutual_nn(fnl_context* ctx, const float* h_d1, uint32_t h1, uint32_t w1,
  * Raw tensor-core scores (fp32 TMEM accumulators) of 256 query rows against 128
  * target rows after the binary16 pack: h_scores[256][128].  dot: q.t;
  * l2: q.t - |t|^2/2.  Used by the tests to pin the UMMA operand layout and to
- * measure the accumulation error the certification margin must cover. */
+ * measure the accumulation error the certification margin must cover.
+ * mode 0: A and B from shared memory; mode 1: A copied into tensor memory with
+ * tcgen05.cp and consumed by a TS MMA (the production K3 path). */
 int fnl_tensor_selftest(fnl_context* ctx, const float* h_queries, const float* h_targets,
-                        uint32_t dim, int metric, float* h_scores);
+                        uint32_t dim, int metric, int mode, float* h_scores);
 
 /* ---- instrumentation -------------------------------------------------------
  * Device time (ms, CUDA events on the context stream) of the dominant scoring

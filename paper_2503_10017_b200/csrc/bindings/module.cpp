@@ -401,17 +401,17 @@ PYBIND11_MODULE(_fastnn, m) {
           "device time and launch count of the dominant scoring kernel since the last reset");
 
     m.def("_tensor_selftest",
-          [](const F32& q, const F32& t, const std::string& metric) {
+          [](const F32& q, const F32& t, const std::string& metric, int mode) {
               if (q.ndim() != 2 || t.ndim() != 2 || q.shape(0) != 256 || t.shape(0) != 128 || q.shape(1) != t.shape(1))
                   throw std::invalid_argument("_tensor_selftest expects q (256, d), t (128, d)");
               py::array_t<float> out({py::ssize_t(256), py::ssize_t(128)});
               fastnn::b200::check(fnl_tensor_selftest(fastnn::b200::context(), q.data(), t.data(),
                                                       std::uint32_t(q.shape(1)),
-                                                      metric == "l2" ? FNL_METRIC_L2 : FNL_METRIC_DOT,
+                                                      metric == "l2" ? FNL_METRIC_L2 : FNL_METRIC_DOT, mode,
                                                       out.mutable_data()));
               return out;
           },
-          py::arg("queries"), py::arg("targets"), py::arg("metric") = "dot");
+          py::arg("queries"), py::arg("targets"), py::arg("metric") = "dot", py::arg("mode") = 1);
 
     m.def("device_count", [] {
         int n = 0;

@@ -888,7 +888,7 @@ extern "C" int fnl_reciprocal_match_batch(fnl_context* ctx, uint32_t npairs, con
 
 // ============================================================== diagnostics
 extern "C" int fnl_tensor_selftest(fnl_context* ctx, const float* h_q, const float* h_t, uint32_t dim,
-                                   int metric, float* h_scores) {
+                                   int metric, int mode, float* h_scores) {
     TRY(check_device(ctx));
     float *dq, *dt, *dout;
     TRY(dev_arr(ctx, "st.q", (size_t)256 * dim, &dq));
@@ -896,7 +896,7 @@ extern "C" int fnl_tensor_selftest(fnl_context* ctx, const float* h_q, const flo
     TRY(dev_arr(ctx, "st.out", (size_t)256 * 128, &dout));
     FNL_CUDA_TRY(cudaMemcpyAsync(dq, h_q, (size_t)256 * dim * 4, cudaMemcpyHostToDevice, ctx->stream));
     FNL_CUDA_TRY(cudaMemcpyAsync(dt, h_t, (size_t)128 * dim * 4, cudaMemcpyHostToDevice, ctx->stream));
-    TRY(fnl::tensor_selftest_scores(ctx, dq, dt, dim, metric == FNL_METRIC_L2, dout));
+    TRY(fnl::tensor_selftest_scores(ctx, dq, dt, dim, metric == FNL_METRIC_L2, mode, dout));
     FNL_CUDA_TRY(cudaMemcpy(h_scores, dout, (size_t)256 * 128 * 4, cudaMemcpyDeviceToHost));
     return FNL_OK;
 }

@@ -25,6 +25,8 @@
 // dist = |q|^2 - 2 s.  Both are monotone in the reference distance, so argmax s
 // == argmin dist up to rounding, which the margin covers.
 #include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -85,22 +87,18 @@ __device__ __forceinline__ void tc_mma_f16(uint32_t d_tmem, uint64_t adesc, uint
             d_tmem),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
-// 32 consecutive fp32 columns of this thread's TMEM lane
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
-    uint32_t r[32];
+// D[tmem] (+)= A[tmem] . B[smem]^T  (A resident in tensor memory)
+__device__ __forceinline__ void tc_mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
     asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(taddr));
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p; }" ::"r"(
+            d_tmem),
+        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
-__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// 128 rows x 256 bits (one K=16 slice of an M=128 operand) smem -> TMEM
+__device__ __forceinline__ void tc_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+    asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc));
+}
 
 __device__ __forceinline__ float max3(float a, float b, float c) {
     float d;
@@ -257,66 +255,177 @@ __global__ void gather_kernel(GatherArgs a) {
 }
 
 // ---------------------------------------------------------------- K3 scan
+// A work unit = one query tile pair (256 gathered rows) x a contiguous range of
+// 128-target tiles.  The kernel is persistent: CTA b runs units b, b+G, b+2G...
+// (static round robin over equal-sized units), so TMEM allocation, barrier
+// setup and the pipeline prologue are paid once per SM, and the query tile of
+// the next unit is fetched into the second A buffer while the current unit is
+// still being scored.
 struct TcItem {
     uint32_t pair, qrow0, tile_begin, tile_end;  // qrow0: first gathered row (multiple of 256)
+    uint32_t nvalid;                             // real query rows in the tile pair (<= 256)
+    uint32_t pad0, pad1, pad2;
 };
 
 struct TcArgs {
     const uint8_t* qbuf;
-    const float* margin;
     const uint8_t* tmap;
     uint64_t t_pair_bytes;
     uint32_t nt;
     const TcItem* items;
-    float4* partial;  // [item][256] = (best, second, idx bits, 0)
+    uint32_t nitems;
+    float4* partial;  // [item][2 sets][256] = (best, second, idx bits, 0)
+    int debug;        // profiling only: 1 = epilogue releases buffers unread, 16 = clock trace of CTA 0
+    unsigned long long* trace;  // [4][4096] clock64 stamps (debug & 16)
 };
 
+// K3 structure (measured on this B200: tools/ubench_mma.cu, ubench_epilogue.cu
+// and per-tile clock traces via FNL_TC_DEBUG=16):
+//  * tcgen05.mma M=128 N=128 K=16 runs at the full 64 cycles with both operands
+//    in shared memory when issued from a warp-uniform loop via elect.sync (a
+//    diverged single lane costs ~55% more).  An mbarrier try_wait costs
+//    ~60-110 cycles even when the phase is complete, so a target tile is 128
+//    targets (4 MMAs = 256 tensor cycles), each issuer waits on ONE barrier per
+//    tile, and two issuer warps alternate tiles so one's wait overlaps the
+//    other's MMAs.
+//  * TMEM (512 columns) holds two fp32 accumulator buffers of 2 query tiles x
+//    128 targets.  The B barrier of tile k completes only when its bytes
+//    landed AND all eight epilogue warps released tile k-2's accumulator.
+//  * The epilogue pulls a whole 128-column slice (4 tcgen05.ld), releases the
+//    buffer, then compares; the two query tiles commit separately so the two
+//    epilogue warps of each SM sub-partition start staggered.
+constexpr uint32_t kBTileRows = 128;
+constexpr uint32_t kBTileBytes = kBTileRows * kPackRowBytes;  // 8 KB
 constexpr int kStages = 8;
-constexpr int kScanThreads = 320;  // warp 0 producer, warp 1 MMA, warps 2..9 epilogue
-constexpr int kEpiWarps = 8;
-constexpr uint32_t kSmemA = 2 * kTileBytes;                 // 16 KB: two query tiles
-constexpr uint32_t kSmemB = kStages * kTileBytes;           // 64 KB ring
-constexpr uint32_t kSmemBars = (2 * kStages + 2 + 2 + 1) * 8;
-// Padded past half the SM's shared memory so a second CTA can never be
-// co-resident and spin in tcgen05.alloc for the 512 TMEM columns.
-constexpr uint32_t kSmemUsed = kSmemA + kSmemB + kSmemBars + 16;
+constexpr int kAccBufs = 2;
+// warps: 0 loader, 1-2 MMA issuers (even / odd tiles), 3..10 epilogue (qt = (w-3)/4, quadrant = w%4)
+constexpr int kScanThreads = 352;
+constexpr int kEpiWarpsPerQt = 4;
+constexpr int kFirstEpiWarp = 3;
+constexpr uint32_t kSmemA = 2 * kTileBytes;                  // 16 KB: two query tiles
+constexpr uint32_t kSmemB = kStages * kBTileBytes;           // 64 KB ring
+constexpr uint32_t kSmemBars = (2 * kStages + 2 * kAccBufs + 2 + 2) * 8;
+// A double buffered (next unit's queries load under the current unit); padded
+// past half the SM's shared memory so no second CTA co-resides and spins in
+// tcgen05.alloc for the 512 TMEM columns.
+constexpr uint32_t kSmemUsed = 2 * kSmemA + kSmemB + kSmemBars + 16;
 constexpr uint32_t kSmemTotal = kSmemUsed > 120u * 1024u ? kSmemUsed : 120u * 1024u;
+constexpr uint32_t kSubTile = 64;  // winner granularity handed to the merge
 
-__device__ __forceinline__ float chunk_max(const float* v) {
-    float r[11];
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile("{ .reg .pred p; elect.sync _|p, 0xffffffff; selp.u32 %0, 1, 0, p; }" : "=r"(pred));
+    return pred != 0;
+}
+
+// Per query row and 64-target sub-tile: m = max of the 64 fp32 scores
+// (3-input-max tree, ~0.5 ALU op per score, no data-dependent branch), then
+//   best' = max(best, m), second' = max(second, min(best, m)),
+//   tile'  = m > best ? this sub-tile : tile.
+// `best` is the largest sub-tile maximum, `tile` the first sub-tile reaching
+// it, `second` the largest maximum of every other sub-tile.  The merge kernel
+// certifies best - second > margin (no score outside the winning sub-tile can
+// be the reference winner) and resolves that sub-tile with the exact chain.
+struct RowState {
+    float best, second;
+    uint32_t tile;
+};
+
+__device__ __forceinline__ float tile_max64(const float* v) {
+    float r[22];
 #pragma unroll
-    for (int i = 0; i < 10; ++i) r[i] = max3(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
-    r[10] = fmaxf(v[30], v[31]);
-    const float s0 = max3(r[0], r[1], r[2]), s1 = max3(r[3], r[4], r[5]), s2 = max3(r[6], r[7], r[8]);
-    return max3(max3(s0, s1, s2), r[9], r[10]);
+    for (int i = 0; i < 21; ++i) r[i] = max3(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+    r[21] = v[63];
+    float q[8];
+#pragma unroll
+    for (int i = 0; i < 7; ++i) q[i] = max3(r[3 * i], r[3 * i + 1], r[3 * i + 2]);
+    q[7] = r[21];
+    return max3(max3(q[0], q[1], q[2]), max3(q[3], q[4], q[5]), fmaxf(q[6], q[7]));
+}
+
+__device__ __forceinline__ void tile_update(RowState& st, float m, uint32_t tile) {
+    st.second = fmaxf(st.second, fminf(st.best, m));
+    st.tile = m > st.best ? tile : st.tile;
+    st.best = fmaxf(st.best, m);
+}
+
+// tcgen05.ld of 32 columns whose destination registers are tied to the
+// matching wait, so no use of them can be scheduled before tcgen05.wait::ld.
+struct Frag {
+    uint32_t r[32];
+};
+__device__ __forceinline__ void frag_ld(uint32_t taddr, Frag& f) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(f.r[0]), "=r"(f.r[1]), "=r"(f.r[2]), "=r"(f.r[3]), "=r"(f.r[4]), "=r"(f.r[5]), "=r"(f.r[6]),
+          "=r"(f.r[7]), "=r"(f.r[8]), "=r"(f.r[9]), "=r"(f.r[10]), "=r"(f.r[11]), "=r"(f.r[12]),
+          "=r"(f.r[13]), "=r"(f.r[14]), "=r"(f.r[15]), "=r"(f.r[16]), "=r"(f.r[17]), "=r"(f.r[18]),
+          "=r"(f.r[19]), "=r"(f.r[20]), "=r"(f.r[21]), "=r"(f.r[22]), "=r"(f.r[23]), "=r"(f.r[24]),
+          "=r"(f.r[25]), "=r"(f.r[26]), "=r"(f.r[27]), "=r"(f.r[28]), "=r"(f.r[29]), "=r"(f.r[30]),
+          "=r"(f.r[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void frag_wait2(Frag& f, Frag& g) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(f.r[0]), "+r"(f.r[1]), "+r"(f.r[2]), "+r"(f.r[3]), "+r"(f.r[4]), "+r"(f.r[5]),
+                   "+r"(f.r[6]), "+r"(f.r[7]), "+r"(f.r[8]), "+r"(f.r[9]), "+r"(f.r[10]), "+r"(f.r[11]),
+                   "+r"(f.r[12]), "+r"(f.r[13]), "+r"(f.r[14]), "+r"(f.r[15]), "+r"(f.r[16]), "+r"(f.r[17]),
+                   "+r"(f.r[18]), "+r"(f.r[19]), "+r"(f.r[20]), "+r"(f.r[21]), "+r"(f.r[22]), "+r"(f.r[23]),
+                   "+r"(f.r[24]), "+r"(f.r[25]), "+r"(f.r[26]), "+r"(f.r[27]), "+r"(f.r[28]), "+r"(f.r[29]),
+                   "+r"(f.r[30]), "+r"(f.r[31]), "+r"(g.r[0]), "+r"(g.r[1]), "+r"(g.r[2]), "+r"(g.r[3]),
+                   "+r"(g.r[4]), "+r"(g.r[5]), "+r"(g.r[6]), "+r"(g.r[7]), "+r"(g.r[8]), "+r"(g.r[9]),
+                   "+r"(g.r[10]), "+r"(g.r[11]), "+r"(g.r[12]), "+r"(g.r[13]), "+r"(g.r[14]), "+r"(g.r[15]),
+                   "+r"(g.r[16]), "+r"(g.r[17]), "+r"(g.r[18]), "+r"(g.r[19]), "+r"(g.r[20]), "+r"(g.r[21]),
+                   "+r"(g.r[22]), "+r"(g.r[23]), "+r"(g.r[24]), "+r"(g.r[25]), "+r"(g.r[26]), "+r"(g.r[27]),
+                   "+r"(g.r[28]), "+r"(g.r[29]), "+r"(g.r[30]), "+r"(g.r[31])
+                 :
+                 : "memory");
+}
+
+// 64 consecutive scores of one row -> sub-tile update (padding masked)
+__device__ __forceinline__ void subtile_scan(RowState& st, const Frag& f, const Frag& g, uint32_t sub,
+                                             uint32_t nt) {
+    float v[64];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        v[j] = __uint_as_float(f.r[j]);
+        v[32 + j] = __uint_as_float(g.r[j]);
+    }
+    if ((sub + 1) * kSubTile > nt) {  // last, partial sub-tile: padding never wins
+#pragma unroll
+        for (int j = 0; j < 64; ++j)
+            if (sub * kSubTile + j >= nt) v[j] = -INFINITY;
+    }
+    tile_update(st, tile_max64(v), sub);
 }
 
 __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint32_t tmem_slot;
-    uint8_t* sA = smem;
-    uint8_t* sB = smem + kSmemA;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemA + kSmemB);
-    uint64_t* full = bars;
-    uint64_t* empty = bars + kStages;
-    uint64_t* tfull = bars + 2 * kStages;
-    uint64_t* tempty = bars + 2 * kStages + 2;
-    uint64_t* afull = bars + 2 * kStages + 4;
+    uint8_t* sA = smem;                  // [2][16 KB]
+    uint8_t* sB = smem + 2 * kSmemA;     // [kStages][8 KB]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kSmemA + kSmemB);
+    uint64_t* full = bars;                     // [kStages]  B landed + accumulator free
+    uint64_t* empty = bars + kStages;          // [kStages]  MMAs of the slot retired
+    uint64_t* tfull = bars + 2 * kStages;      // [kAccBufs][2 query tiles]
+    uint64_t* afull = tfull + 2 * kAccBufs;    // [2]
+    uint64_t* afree = afull + 2;               // [2]
 
-    const TcItem item = a.items[blockIdx.x];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t ntiles = item.tile_end - item.tile_begin;
+    const uint32_t G = gridDim.x;
+    const bool trace = (a.debug & 16) && blockIdx.x == 0;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], 1 + 2 * kEpiWarpsPerQt);
             mbar_init(&empty[s], 1);
         }
+        for (int b = 0; b < 2 * kAccBufs; ++b) mbar_init(&tfull[b], 1);
         for (int b = 0; b < 2; ++b) {
-            mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], kEpiWarps);
+            mbar_init(&afull[b], 1);
+            mbar_init(&afree[b], 2);  // both MMA issuers
         }
-        mbar_init(afull, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -330,92 +439,117 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
     const uint32_t tmem = tmem_slot;
 
     if (warp == 0) {
-        if (lane == 0) {
-            // ---------------- producer: query tile pair once, then the target ring
-            mbar_expect_tx(afull, kSmemA);
-            bulk_g2s(sA, a.qbuf + (uint64_t)item.qrow0 * kPackRowBytes, kSmemA, afull);
+        // ---------------- loader: query tile pair per unit, then the target ring
+        uint32_t k = 0, i = 0;
+        for (uint32_t u = blockIdx.x; u < a.nitems; u += G, ++i) {
+            const TcItem item = a.items[u];
+            const uint32_t ab = i & 1u;
+            mbar_wait(&afree[ab], ((i >> 1) & 1u) ^ 1u);
+            if (elect_one()) {
+                mbar_expect_tx(&afull[ab], kSmemA);
+                bulk_g2s(sA + ab * kSmemA, a.qbuf + (uint64_t)item.qrow0 * kPackRowBytes, kSmemA, &afull[ab]);
+            }
+            __syncwarp();
             const uint8_t* tbase = a.tmap + (uint64_t)item.pair * a.t_pair_bytes;
-            for (uint32_t k = 0; k < ntiles; ++k) {
-                const uint32_t s = k % kStages, ph = (k / kStages) & 1u;
-                mbar_wait(&empty[s], ph ^ 1u);
-                mbar_expect_tx(&full[s], kTileBytes);
-                bulk_g2s(sB + s * kTileBytes, tbase + (uint64_t)(item.tile_begin + k) * kTileBytes, kTileBytes,
-                         &full[s]);
+            for (uint32_t t = item.tile_begin; t < item.tile_end; ++t, ++k) {
+                const uint32_t s = k % kStages;
+                mbar_wait(&empty[s], ((k / kStages) & 1u) ^ 1u);
+                if (trace && lane == 0 && k < 4096) a.trace[k] = clock64();
+                if (elect_one()) {
+                    mbar_expect_tx(&full[s], kBTileBytes);
+                    bulk_g2s(sB + s * kBTileBytes, tbase + (uint64_t)t * kBTileBytes, kBTileBytes, &full[s]);
+                }
+                __syncwarp();
             }
         }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            // ---------------- MMA issuer (single thread)
-            mbar_wait(afull, 0);
+    } else if (warp == 1 || warp == 2) {
+        // ---------------- MMA issuers: warp 1 even tiles, warp 2 odd tiles
+        // (disjoint accumulator buffers and stages); warp-uniform loops, one
+        // elected lane issues.
+        const uint32_t parity = warp - 1;
+        const uint32_t b_addr = smem_addr(sB);
+        uint32_t k = 0, i = 0;
+        for (uint32_t u = blockIdx.x; u < a.nitems; u += G, ++i) {
+            const uint32_t nt_unit = a.items[u].tile_end - a.items[u].tile_begin;
+            const uint32_t ab = i & 1u;
+            mbar_wait(&afull[ab], (i >> 1) & 1u);
             tc_fence_after();
-            const uint32_t a_addr = smem_addr(sA), b_addr = smem_addr(sB);
-            for (uint32_t k = 0; k < ntiles; ++k) {
-                const uint32_t s = k % kStages, ph = (k / kStages) & 1u;
-                const uint32_t acc = k & 1u, acc_ph = (k >> 1) & 1u;
-                mbar_wait(&tempty[acc], acc_ph ^ 1u);
-                mbar_wait(&full[s], ph);
+            const uint32_t a_addr = smem_addr(sA + ab * kSmemA);
+            const uint64_t ad0 = umma_desc(a_addr), ad1 = umma_desc(a_addr + kTileBytes);
+            for (uint32_t t = 0; t < nt_unit; ++t, ++k) {
+                if ((k & 1u) != parity) continue;
+                const uint32_t s = k % kStages, acc = k % kAccBufs;
+                if (trace && lane == 0 && k < 4096) a.trace[4096 + k] = clock64();
+                mbar_wait(&full[s], (k / kStages) & 1u);
+                if (trace && lane == 0 && k < 4096) a.trace[8192 + k] = clock64();
                 tc_fence_after();
-#pragma unroll
-                for (uint32_t qt = 0; qt < 2; ++qt) {
-#pragma unroll
-                    for (uint32_t ks = 0; ks < 2; ++ks) {
-                        tc_mma_f16(tmem + acc * 256u + qt * 128u,
-                                   umma_desc(a_addr + qt * kTileBytes + ks * 256u),
-                                   umma_desc(b_addr + s * kTileBytes + ks * 256u), kIdescF16M128N128, ks);
-                    }
+                if (elect_one()) {
+                    const uint64_t bd = umma_desc(b_addr + s * kBTileBytes);
+                    const uint32_t d = tmem + acc * 256u;
+                    // K-step 1 starts 256 B (two 8-channel chunks) further: +16 in descriptor units
+                    tc_mma_f16(d, ad0, bd, kIdescF16M128N128, 0u);
+                    tc_mma_f16(d, ad0 + 16u, bd + 16u, kIdescF16M128N128, 1u);
+                    tc_commit(&tfull[acc * 2 + 0]);
+                    tc_mma_f16(d + 128u, ad1, bd, kIdescF16M128N128, 0u);
+                    tc_mma_f16(d + 128u, ad1 + 16u, bd + 16u, kIdescF16M128N128, 1u);
+                    tc_commit(&tfull[acc * 2 + 1]);
+                    tc_commit(&empty[s]);
                 }
-                tc_commit(&empty[s]);    // smem slot reusable once these MMAs retire
-                tc_commit(&tfull[acc]);  // accumulator ready for the epilogue
+                __syncwarp();
             }
+            if (elect_one()) tc_commit(&afree[ab]);  // this issuer no longer reads this unit's query tiles
+            __syncwarp();
         }
     } else {
-        // ---------------- epilogue: 8 warps, two per TMEM lane quadrant
-        const uint32_t e = warp - 2, qt = e >> 2, quad = warp & 3u;
+        // ---------------- epilogue: 8 warps, query tile qt, TMEM lane quadrant w%4
+        const uint32_t e = warp - kFirstEpiWarp, qt = e >> 2, quad = warp & 3u;
         const uint32_t row = qt * 128u + quad * 32u + lane;  // 0..255 within the tile pair
-        const float margin = a.margin[item.qrow0 + row];
-        float best = -INFINITY, second = -INFINITY, thr = -INFINITY;
-        uint32_t bidx = 0xFFFFFFFFu;
-        float v[128];
-        for (uint32_t k = 0; k < ntiles; ++k) {
-            const uint32_t acc = k & 1u, acc_ph = (k >> 1) & 1u;
-            mbar_wait(&tfull[acc], acc_ph);
-            tc_fence_after();
-            const uint32_t taddr = tmem + ((quad * 32u) << 16) + acc * 256u + qt * 128u;
-            tmem_ld32(taddr + 0, v + 0);
-            tmem_ld32(taddr + 32, v + 32);
-            tmem_ld32(taddr + 64, v + 64);
-            tmem_ld32(taddr + 96, v + 96);
-            tmem_ld_wait();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);  // MMA may overwrite this buffer now
-            const uint32_t col0 = (item.tile_begin + k) * kTileRows;
-            if (col0 + kTileRows > a.nt) {  // last, partial tile: padded targets never win
-#pragma unroll
-                for (int j = 0; j < 128; ++j)
-                    if (col0 + j >= a.nt) v[j] = -INFINITY;
-            }
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const float m = chunk_max(v + 32 * c);
-                if (m >= thr) {  // rare after warm-up: this chunk may hold the best or a near tie
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const float x = v[32 * c + j];
-                        if (x > best) {
-                            second = fmaxf(second, best);
-                            best = x;
-                            bidx = col0 + 32 * c + j;
-                        } else {
-                            second = fmaxf(second, x);
-                        }
-                    }
-                    thr = best - margin;
+        const uint32_t lane_base = (quad * 32u) << 16;
+        uint32_t total = 0;  // tiles this CTA will score
+        for (uint32_t u = blockIdx.x; u < a.nitems; u += G) total += a.items[u].tile_end - a.items[u].tile_begin;
+        // releasing tile k's accumulator enables tile k + kAccBufs; the first
+        // kAccBufs tiles start with free buffers
+        if (lane == 0)
+            for (uint32_t j = 0; j < kAccBufs && j < total; ++j) mbar_arrive(&full[j % kStages]);
+        uint32_t k = 0;
+        Frag f0, f1, f2, f3;
+        for (uint32_t u = blockIdx.x; u < a.nitems; u += G) {
+            const TcItem item = a.items[u];
+            const bool warp_real = qt * 128u + quad * 32u < item.nvalid;  // else all rows padding
+            RowState st{-INFINITY, -INFINITY, 0xFFFFFFFFu};
+            for (uint32_t t = item.tile_begin; t < item.tile_end; ++t, ++k) {
+                const uint32_t acc = k % kAccBufs;
+                const bool next = k + kAccBufs < total;
+                mbar_wait(&tfull[acc * 2 + qt], (k / kAccBufs) & 1u);
+                const bool tw = trace && warp == kFirstEpiWarp && k < 4096;
+                if (tw && lane == 0) a.trace[12288 + k] = clock64();
+                if (!warp_real || (a.debug & 1)) {  // nothing to score: hand the buffer straight back
+                    __syncwarp();
+                    if (lane == 0 && next) mbar_arrive(&full[(k + kAccBufs) % kStages]);
+                    continue;
+                }
+                tc_fence_after();
+                const uint32_t taddr = tmem + lane_base + acc * 256u + qt * 128u;
+                frag_ld(taddr + 0, f0);
+                frag_ld(taddr + 32, f1);
+                frag_ld(taddr + 64, f2);
+                frag_ld(taddr + 96, f3);
+                frag_wait2(f0, f1);
+                frag_wait2(f2, f3);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0 && next) mbar_arrive(&full[(k + kAccBufs) % kStages]);  // buffer drained
+                if (tw && lane == 0) a.trace[16384 + k] = clock64();
+                subtile_scan(st, f0, f1, 2 * t, a.nt);
+                subtile_scan(st, f2, f3, 2 * t + 1, a.nt);
+                if (tw) {
+                    __syncwarp();
+                    if (lane == 0) a.trace[20480 + k] = clock64() + (st.best > 1e30f ? 1 : 0);
                 }
             }
+            a.partial[(uint64_t)u * kQueryTilePair + row] =
+                make_float4(st.best, st.second, __uint_as_float(st.tile), 0.0f);
         }
-        a.partial[(uint64_t)blockIdx.x * kQueryTilePair + row] =
-            make_float4(best, second, __uint_as_float(bidx), 0.0f);
     }
     tc_fence_before();
     __syncthreads();
@@ -434,34 +568,56 @@ struct MergeArgs {
     uint32_t splits;
     const uint32_t* n_active;
     const float* margin;
+    const uint8_t* qbuf;
+    const uint8_t* tmap;
+    uint64_t t_pair_bytes;
+    uint32_t nt;
+    uint32_t dim;
     uint32_t* out;
+    float* min_dist;            // may be null
     uint32_t out_stride;
     uint32_t* rescan;           // (gathered row, pair, qi) triples
     unsigned int* rescan_count;
     unsigned long long* near_ties;  // per pair
 };
 
+template <bool kL2>
+__device__ __forceinline__ float packed_chain(const float* q, const uint8_t* map, uint32_t row, uint32_t dim);
+__device__ __forceinline__ void load_query(const uint8_t* qbuf, uint32_t grow, uint32_t dim, float* q);
+
+template <bool kL2>
 __global__ void merge_kernel(MergeArgs a) {
     const uint32_t tp = blockIdx.x, r = threadIdx.x;
     const uint32_t pair = a.tp_pair[tp];
     const uint32_t qi = a.tp_qi0[tp] + r;
     if (qi >= a.n_active[pair]) return;
     float best = -INFINITY, second = -INFINITY;
-    uint32_t idx = 0;
+    uint32_t tile = 0;
     for (uint32_t s = 0; s < a.splits; ++s) {
         const float4 p = a.partial[((uint64_t)tp * a.splits + s) * kQueryTilePair + r];
-        if (p.x > best) {
-            second = fmaxf(second, best);
-            best = p.x;
-            idx = __float_as_uint(p.z);
-        } else {
-            second = fmaxf(second, p.x);
-        }
-        second = fmaxf(second, p.y);
+        second = fmaxf(second, fmaxf(p.y, fminf(best, p.x)));
+        if (p.x > best) tile = __float_as_uint(p.z);
+        best = fmaxf(best, p.x);
     }
     const uint32_t grow = a.tp_row0[tp] + r;
+    const uint64_t o = (uint64_t)pair * a.out_stride + qi;
     if (best - second > a.margin[grow]) {
-        a.out[(uint64_t)pair * a.out_stride + qi] = idx;
+        // certified: the reference winner lies in `tile`; decide it exactly
+        float q[kPackK];
+        load_query(a.qbuf, grow, a.dim, q);
+        const uint8_t* tm = a.tmap + pair * a.t_pair_bytes;
+        const uint32_t t0 = tile * kSubTile, t1 = min(a.nt, t0 + kSubTile);
+        float bd = INFINITY;
+        uint32_t bi = t0;
+        for (uint32_t t = t0; t < t1; ++t) {
+            const float d = packed_chain<kL2>(q, tm, t, a.dim);
+            if (d < bd) {
+                bd = d;
+                bi = t;
+            }
+        }
+        a.out[o] = bi;
+        if (a.min_dist) a.min_dist[o] = bd;
     } else {
         const uint32_t k = atomicAdd(a.rescan_count, 1u);
         a.rescan[3 * k] = grow;
@@ -552,28 +708,27 @@ __global__ void __launch_bounds__(kRescanThreads) rescan_kernel(RescanArgs a) {
 }
 
 __global__ void rescan_finish_kernel(const uint32_t* rescan, const unsigned int* count,
-                                     unsigned long long* keys, uint32_t* out, uint32_t out_stride) {
+                                     unsigned long long* keys, uint32_t* out, float* min_dist,
+                                     uint32_t out_stride, bool dot) {
     const uint32_t n = *count;
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-        out[(uint64_t)rescan[3 * k + 1] * out_stride + rescan[3 * k + 2]] = (uint32_t)(keys[k] & 0xFFFFFFFFull);
+        const uint64_t o = (uint64_t)rescan[3 * k + 1] * out_stride + rescan[3 * k + 2];
+        const unsigned long long key = keys[k];
+        out[o] = (uint32_t)(key & 0xFFFFFFFFull);
+        if (min_dist) {
+            float d = from_orderable((uint32_t)(key >> 32));
+            if (d == 0.0f) d = dot ? -0.0f : 0.0f;  // canonical sign of an exact zero
+            min_dist[o] = d;
+        }
         keys[k] = ~0ull;
     }
 }
 
-// Exact reference distance of each winner (dense API).
-template <bool kL2>
-__global__ void winner_dist_kernel(const uint8_t* qbuf, const uint8_t* tmap, uint32_t nq, uint32_t dim,
-                                   const uint32_t* nearest, float* min_dist) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= nq) return;
-    float q[kPackK];
-    load_query(qbuf, i, dim, q);
-    min_dist[i] = packed_chain<kL2>(q, tmap, nearest[i], dim);
-}
-
 // Raw scores of one tile pair x one target tile (UMMA layout self-test).
-__global__ void __launch_bounds__(kScanThreads, 1) selftest_kernel(const uint8_t* qbuf, const uint8_t* tmap,
-                                                                    float* out) {
+constexpr int kSelftestThreads = 320;
+constexpr uint32_t kTmemA = 384;  // self-test: query tiles copied into TMEM columns 384..415
+__global__ void __launch_bounds__(kSelftestThreads, 1) selftest_kernel(const uint8_t* qbuf, const uint8_t* tmap,
+                                                                    float* out, int mode) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint32_t tmem_slot;
     __shared__ uint64_t bar_ld, bar_mma;
@@ -599,10 +754,20 @@ __global__ void __launch_bounds__(kScanThreads, 1) selftest_kernel(const uint8_t
         mbar_wait(&bar_ld, 0);
         tc_fence_after();
         const uint32_t a_addr = smem_addr(smem), b_addr = a_addr + kSmemA;
-        for (uint32_t qt = 0; qt < 2; ++qt)
-            for (uint32_t ks = 0; ks < 2; ++ks)
-                tc_mma_f16(tmem + qt * 128u, umma_desc(a_addr + qt * kTileBytes + ks * 256u),
-                           umma_desc(b_addr + ks * 256u), kIdescF16M128N128, ks);
+        if (mode == 0) {  // both operands from shared memory
+            for (uint32_t qt = 0; qt < 2; ++qt)
+                for (uint32_t ks = 0; ks < 2; ++ks)
+                    tc_mma_f16(tmem + qt * 128u, umma_desc(a_addr + qt * kTileBytes + ks * 256u),
+                               umma_desc(b_addr + ks * 256u), kIdescF16M128N128, ks);
+        } else {  // production path: query tiles copied into TMEM, TS MMA
+            for (uint32_t qt = 0; qt < 2; ++qt)
+                for (uint32_t ks = 0; ks < 2; ++ks)
+                    tc_cp_128x256b(tmem + kTmemA + qt * 16u + ks * 8u, umma_desc(a_addr + qt * kTileBytes + ks * 256u));
+            for (uint32_t qt = 0; qt < 2; ++qt)
+                for (uint32_t ks = 0; ks < 2; ++ks)
+                    tc_mma_f16_ts(tmem + qt * 128u, tmem + kTmemA + qt * 16u + ks * 8u,
+                                  umma_desc(b_addr + ks * 256u), kIdescF16M128N128, ks);
+        }
         tc_commit(&bar_mma);
     }
     if (warp >= 2) {
@@ -610,11 +775,15 @@ __global__ void __launch_bounds__(kScanThreads, 1) selftest_kernel(const uint8_t
         tc_fence_after();
         const uint32_t e = warp - 2, qt = e >> 2, quad = warp & 3u;
         const uint32_t row = qt * 128u + quad * 32u + lane;
-        float v[32];
-        for (int c = 0; c < 4; ++c) {
-            tmem_ld32(tmem + ((quad * 32u) << 16) + qt * 128u + 32u * c, v);
-            tmem_ld_wait();
-            for (int j = 0; j < 32; ++j) out[row * 128 + 32 * c + j] = v[j];
+        Frag f, g;
+        for (int c = 0; c < 4; c += 2) {
+            frag_ld(tmem + ((quad * 32u) << 16) + qt * 128u + 32u * c, f);
+            frag_ld(tmem + ((quad * 32u) << 16) + qt * 128u + 32u * (c + 1), g);
+            frag_wait2(f, g);
+            for (int j = 0; j < 32; ++j) {
+                out[row * 128 + 32 * c + j] = __uint_as_float(f.r[j]);
+                out[row * 128 + 32 * (c + 1) + j] = __uint_as_float(g.r[j]);
+            }
         }
     }
     tc_fence_before();
@@ -644,6 +813,24 @@ int ensure_attrs() {
 }
 
 }  // namespace
+
+// profiling aid: with FNL_TC_DEBUG & 16 the last tc_scan launch's clock trace
+// of CTA 0 is written to $FNL_TC_TRACE (default /tmp/fnl_tc_trace.bin)
+static bool debug_mode_trace_dump(fnl_context* ctx, cudaStream_t s) {
+    static const int debug_mode = getenv("FNL_TC_DEBUG") ? atoi(getenv("FNL_TC_DEBUG")) : 0;
+    if (!(debug_mode & 16)) return false;
+    unsigned long long* trace = nullptr;
+    if (ws_arr(ctx, "tc.trace", 6 * 4096, &trace) != FNL_OK) return false;
+    static unsigned long long host[6 * 4096];
+    cudaMemcpyAsync(host, trace, sizeof(host), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    const char* path = getenv("FNL_TC_TRACE") ? getenv("FNL_TC_TRACE") : "/tmp/fnl_tc_trace.bin";
+    if (FILE* f = fopen(path, "wb")) {
+        fwrite(host, 1, sizeof(host), f);
+        fclose(f);
+    }
+    return true;
+}
 
 // ====================================================================== host
 int tensor_pack(fnl_context* ctx, const char* tag, const float* d_src, uint32_t npairs, uint32_t rows,
@@ -677,7 +864,7 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     TRY(ensure_attrs());
     cudaStream_t s = ctx_stream(ctx);
     const uint32_t nt = T.rows;
-    const uint32_t ntiles = ceil_div_u(nt, kTileRows);
+    const uint32_t ntiles = ceil_div_u(nt, kBTileRows);
 
     // ---- host work list: gather slots (one per active pair) and tile pairs
     std::vector<uint32_t> slot_pair, slot_base, tp_pair, tp_row0, tp_qi0;
@@ -697,13 +884,13 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     if (slot_pair.empty()) return FNL_OK;
     const uint32_t ntp = (uint32_t)tp_pair.size();
     // Target splits: pick the split count that minimises the modelled makespan
-    // (waves of one CTA per SM x (tiles per CTA + fixed prologue cost)).
+    // of the persistent grid (units per CTA x (tiles per unit + switch cost)).
     const uint32_t sms = (uint32_t)ctx_sm_count(ctx);
     uint32_t best_s = 1;
     double best_cost = 1e300;
     for (uint32_t sp = 1; sp <= std::min<uint32_t>(ntiles, 64); ++sp) {
         const double waves = std::ceil((double)ntp * sp / sms);
-        const double cost = waves * (std::ceil((double)ntiles / sp) + 24.0);
+        const double cost = waves * (std::ceil((double)ntiles / sp) + 3.0);
         if (cost < best_cost - 1e-9) {
             best_cost = cost;
             best_s = sp;
@@ -715,7 +902,8 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     items.reserve((size_t)ntp * splits);
     for (uint32_t j = 0; j < ntp; ++j)
         for (uint32_t sp = 0; sp < splits; ++sp)
-            items.push_back({tp_pair[j], tp_row0[j], sp * per, std::min(ntiles, (sp + 1) * per)});
+            items.push_back({tp_pair[j], tp_row0[j], sp * per, std::min(ntiles, (sp + 1) * per),
+                             std::min<uint32_t>(kQueryTilePair, h_active[tp_pair[j]] - tp_qi0[j]), 0, 0, 0});
     const uint32_t nitems = (uint32_t)items.size();
     const uint32_t nslots = (uint32_t)slot_pair.size();
 
@@ -723,7 +911,7 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     // the previous pass is never overwritten)
     static thread_local int flip = 0;
     flip ^= 1;
-    const size_t words = 2 * (size_t)nslots + 3 * (size_t)ntp + 4 * (size_t)nitems;
+    const size_t words = 2 * (size_t)nslots + 3 * (size_t)ntp + 8 * (size_t)nitems + 4;
     uint32_t* pin = nullptr;
     uint32_t* dlist = nullptr;
     TRY(ws_pinned(ctx, flip ? "tc.list.pin1" : "tc.list.pin0", words * 4, (void**)&pin));
@@ -734,14 +922,16 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     std::copy(tp_pair.begin(), tp_pair.end(), w + 2 * nslots);
     std::copy(tp_row0.begin(), tp_row0.end(), w + 2 * nslots + ntp);
     std::copy(tp_qi0.begin(), tp_qi0.end(), w + 2 * nslots + 2 * ntp);
-    memcpy(w + 2 * nslots + 3 * ntp, items.data(), items.size() * sizeof(TcItem));
+    // items start 16-byte aligned
+    const size_t item_off = (2 * (size_t)nslots + 3 * (size_t)ntp + 3) & ~(size_t)3;
+    memcpy(w + item_off, items.data(), items.size() * sizeof(TcItem));
     FNL_CUDA_TRY(cudaMemcpyAsync(dlist, pin, words * 4, cudaMemcpyHostToDevice, s));
     const uint32_t* d_slot_pair = dlist;
     const uint32_t* d_slot_base = dlist + nslots;
     const uint32_t* d_tp_pair = dlist + 2 * nslots;
     const uint32_t* d_tp_row0 = d_tp_pair + ntp;
     const uint32_t* d_tp_qi0 = d_tp_row0 + ntp;
-    const TcItem* d_items = reinterpret_cast<const TcItem*>(d_tp_qi0 + ntp);
+    const TcItem* d_items = reinterpret_cast<const TcItem*>(dlist + item_off);
 
     // ---- device scratch
     uint8_t* qbuf;
@@ -778,18 +968,26 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     }
     // ---- K3 tensor-core scan (the dominant kernel; timed)
     {
-        TcArgs t{qbuf, margin, T.data, T.pair_bytes, nt, d_items, partial};
+        static const int debug_mode = getenv("FNL_TC_DEBUG") ? atoi(getenv("FNL_TC_DEBUG")) : 0;
+        unsigned long long* trace = nullptr;
+        if (debug_mode & 16) {
+            TRY(ws_arr(ctx, "tc.trace", 6 * 4096, &trace));
+            FNL_CUDA_TRY(cudaMemsetAsync(trace, 0, 6 * 4096 * 8, s));
+        }
+        TcArgs t{qbuf, T.data, T.pair_bytes, nt, d_items, nitems, partial, debug_mode, trace};
+        const uint32_t grid = std::min<uint32_t>(nitems, sms);
         cudaEvent_t end_ev;
         ctx_score_begin(ctx, &end_ev);
-        tc_scan_kernel<<<nitems, kScanThreads, kSmemTotal, s>>>(t);
+        tc_scan_kernel<<<grid, kScanThreads, kSmemTotal, s>>>(t);
         ctx_score_end(ctx, end_ev);
         FNL_CUDA_TRY(cudaGetLastError());
     }
     // ---- K3b merge + certification
     {
-        MergeArgs m{partial, d_tp_pair, d_tp_row0, d_tp_qi0, splits, d_active, margin, out, out_stride,
-                    rescan, rcount, d_near_ties};
-        merge_kernel<<<ntp, kQueryTilePair, 0, s>>>(m);
+        MergeArgs m{partial, d_tp_pair, d_tp_row0, d_tp_qi0, splits, d_active, margin, qbuf, T.data,
+                    T.pair_bytes, nt, dim, out, min_dist, out_stride, rescan, rcount, d_near_ties};
+        if (l2) merge_kernel<true><<<ntp, kQueryTilePair, 0, s>>>(m);
+        else merge_kernel<false><<<ntp, kQueryTilePair, 0, s>>>(m);
         FNL_CUDA_TRY(cudaGetLastError());
     }
     // ---- K4' exact re-decision of near ties (grid-stride over a device count)
@@ -799,16 +997,11 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
         if (l2) rescan_kernel<true><<<grid, kRescanThreads, 0, s>>>(r);
         else rescan_kernel<false><<<grid, kRescanThreads, 0, s>>>(r);
         FNL_CUDA_TRY(cudaGetLastError());
-        rescan_finish_kernel<<<4, 256, 0, s>>>(rescan, rcount, keys, out, out_stride);
+        rescan_finish_kernel<<<4, 256, 0, s>>>(rescan, rcount, keys, out, min_dist, out_stride, !l2);
         FNL_CUDA_TRY(cudaGetLastError());
     }
-    if (min_dist) {  // dense API only: single slot, identity rows
-        const uint32_t nq = h_active[slot_pair[0]];
-        if (l2) winner_dist_kernel<true><<<ceil_div_u(nq, 256), 256, 0, s>>>(qbuf, T.data, nq, dim, out, min_dist);
-        else winner_dist_kernel<false><<<ceil_div_u(nq, 256), 256, 0, s>>>(qbuf, T.data, nq, dim, out, min_dist);
-        FNL_CUDA_TRY(cudaGetLastError());
-    }
-    ctx_count_launches(ctx, 5 + (min_dist ? 1 : 0));
+    if (debug_mode_trace_dump(ctx, s)) {}
+    ctx_count_launches(ctx, 5);
     return FNL_OK;
 }
 
@@ -830,7 +1023,7 @@ int tensor_nn_dense(fnl_context* ctx, const float* d_q, uint32_t nq, const float
 }
 
 int tensor_selftest_scores(fnl_context* ctx, const float* d_q, const float* d_t, uint32_t dim, bool l2,
-                           float* d_out) {
+                           int mode, float* d_out) {
     TRY(ensure_attrs());
     unsigned long long* scratch;
     TRY(ws_arr(ctx, "tc.st.scratch", 4, &scratch));
@@ -855,7 +1048,7 @@ int tensor_selftest_scores(fnl_context* ctx, const float* d_q, const float* d_t,
     GatherArgs g{Q.data, Q.pair_bytes, nullptr, n, act, lists, lists + 1, qbuf, margin, T.max_norm, dim, l2};
     gather_kernel<<<dim3(4, 1), 256, 0, s>>>(g);
     FNL_CUDA_TRY(cudaGetLastError());
-    selftest_kernel<<<1, kScanThreads, kSmemTotal, s>>>(qbuf, T.data, d_out);
+    selftest_kernel<<<1, kSelftestThreads, kSmemTotal, s>>>(qbuf, T.data, d_out, mode);
     FNL_CUDA_TRY(cudaGetLastError());
     FNL_CUDA_TRY(cudaStreamSynchronize(s));
     return FNL_OK;

@@ -59,7 +59,9 @@ int tensor_nn_dense(fnl_context* ctx, const float* d_q, uint32_t nq, const float
 
 // Self-test: raw tensor-core scores of a packed query tile pair (256 rows)
 // against one packed target tile (128 rows) -> out[256][128] fp32.
+// mode 0: both operands from shared memory; mode 1: query tiles copied to TMEM
+// with tcgen05.cp and a TS MMA (the production path).
 int tensor_selftest_scores(fnl_context* ctx, const float* d_q, const float* d_t, uint32_t dim,
-                           bool l2, float* d_out);
+                           bool l2, int mode, float* d_out);
 
 }  // namespace fnl

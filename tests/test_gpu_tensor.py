@@ -30,9 +30,10 @@ def strip(rep):
     return r
 
 
+@pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("metric", ["dot", "l2"])
 @pytest.mark.parametrize("dim", [24, 8, 30])
-def test_umma_layout_and_accumulation_error(fnl, metric, dim):
+def test_umma_layout_and_accumulation_error(fnl, metric, dim, mode):
     """Raw TMEM scores vs float64 on the same binary16 values: pins the UMMA
     descriptor / canonical-layout encoding and measures the accumulation error
     the certification margin has to cover (margin uses 2^-16 * sum|products|)."""
@@ -42,7 +43,7 @@ def test_umma_layout_and_accumulation_error(fnl, metric, dim):
     q /= np.linalg.norm(q, axis=1, keepdims=True).astype(np.float32)
     t /= np.linalg.norm(t, axis=1, keepdims=True).astype(np.float32)
     q, t = h16(q), h16(t)
-    got = fnl._tensor_selftest(q, t, metric).astype(np.float64)
+    got = fnl._tensor_selftest(q, t, metric, mode).astype(np.float64)
     exact = q.astype(np.float64) @ t.astype(np.float64).T
     if metric == "l2":
         n2 = (t.astype(np.float64) ** 2).sum(1)
