@@ -16,6 +16,8 @@ import os as _os
 _here = _os.path.dirname(_os.path.abspath(__file__))
 try:
     from ._fastnn import (  # noqa: F401
+        _parse_report,
+        _render_report,
         _tensor_selftest,
         abi_version,
         block_distances,

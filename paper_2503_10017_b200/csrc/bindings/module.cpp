@@ -413,6 +413,34 @@ PYBIND11_MODULE(_fastnn, m) {
           },
           py::arg("queries"), py::arg("targets"), py::arg("metric") = "dot", py::arg("mode") = 1);
 
+    // host-side report rendering, exposed for the golden-format tests
+    m.def("_render_report",
+          [](py::dict d, const std::string& format) {
+              fastnn::RunReport r;
+              auto get = [&](const char* k, auto& v) {
+                  if (d.contains(k)) v = d[k].cast<std::decay_t<decltype(v)>>();
+              };
+              get("backend", r.backend); get("metric", r.metric); get("precision", r.precision);
+              get("height1", r.height1); get("width1", r.width1); get("height2", r.height2); get("width2", r.width2);
+              get("dim", r.dim); get("k", r.k); get("grid_stride", r.grid_stride); get("max_iters", r.max_iters);
+              get("convergence_fraction", r.convergence_fraction); get("block_size", r.block_size); get("seed", r.seed);
+              get("subsample_us", r.subsample_us); get("forward_nn_us", r.forward_nn_us);
+              get("reverse_nn_us", r.reverse_nn_us); get("harvest_us", r.harvest_us);
+              get("a_block_fetches", r.a_block_fetches); get("b_block_fetches", r.b_block_fetches);
+              get("iterations", r.iterations); get("samples", r.samples); get("converged", r.converged);
+              get("converged_fraction", r.converged_fraction); get("half_saturated", r.half_saturated);
+              get("half_saturation_events", r.half_saturation_events);
+              if (d.contains("hybrid_full_argmin_agreement") && !d["hybrid_full_argmin_agreement"].is_none())
+                  r.hybrid_full_argmin_agreement = d["hybrid_full_argmin_agreement"].cast<double>();
+              get("matches_emitted", r.matches_emitted); get("duplicates_dropped", r.duplicates_dropped);
+              get("active_history", r.active_history);
+              return fastnn::render_report(r, format == "csv" ? fastnn::ReportFormat::Csv : fastnn::ReportFormat::Json);
+          },
+          py::arg("report"), py::arg("format") = "json");
+    m.def("_parse_report", [](const std::string& text) {
+        return fastnn::render_report(fastnn::parse_report_json(text), fastnn::ReportFormat::Json);
+    });
+
     m.def("device_count", [] {
         int n = 0;
         fnl_device_count(&n);
