@@ -150,15 +150,24 @@ __global__ void pack_kernel(PackArgs a) {
     float v[8];
     uint32_t sat = 0;
     float ss = 0.0f;
+    const bool vec = (a.dim & 7u) == 0 && chunk * 8 < a.dim;  // whole 8-channel chunk, 32 B aligned
+    if (real && vec) {
+        const float4 lo = __ldg(reinterpret_cast<const float4*>(src + chunk * 8));
+        const float4 hi = __ldg(reinterpret_cast<const float4*>(src + chunk * 8 + 4));
+        v[0] = lo.x; v[1] = lo.y; v[2] = lo.z; v[3] = lo.w;
+        v[4] = hi.x; v[5] = hi.y; v[6] = hi.z; v[7] = hi.w;
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t c = chunk * 8 + i;
+            v[i] = (real && c < a.dim) ? src[c] : 0.0f;
+        }
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        const uint32_t c = chunk * 8 + i;
-        float x = 0.0f;
-        if (real && c < a.dim) {
-            x = src[c];
-            if (!isfinite(x)) atomicMin(a.bad + pair, (unsigned long long)row * a.dim + c);
-            x = half_round_sat(x, sat);
-        }
+        float x = v[i];
+        if (!isfinite(x)) atomicMin(a.bad + pair, (unsigned long long)row * a.dim + chunk * 8 + i);
+        x = half_round_sat(x, sat);
         v[i] = x;
         ss = __fmaf_rn(x, x, ss);
     }
@@ -185,8 +194,11 @@ __global__ void pack_kernel(PackArgs a) {
     *reinterpret_cast<uint4*>(a.dst + pair * a.pair_bytes + packed_offset(row, chunk)) = out;
     const uint32_t wsat = warp_sum(sat);
     if ((threadIdx.x & 31) == 0 && wsat) atomicAdd(a.sat + pair, (unsigned long long)wsat);
-    if (real && chunk == 0)
-        atomicMax(reinterpret_cast<unsigned int*>(a.max_norm) + pair, __float_as_uint(sqrtf(ss)));
+    // one atomic per warp (8 rows): non-negative floats order like their bits
+    uint32_t nb = real ? __float_as_uint(sqrtf(ss)) : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nb = max(nb, __shfl_xor_sync(0xFFFFFFFFu, nb, o));
+    if ((threadIdx.x & 31) == 0 && nb) atomicMax(reinterpret_cast<unsigned int*>(a.max_norm) + pair, nb);
 }
 
 // ---------------------------------------------------------------- K2 gather
@@ -581,11 +593,12 @@ struct MergeArgs {
     unsigned long long* near_ties;  // per pair
 };
 
-template <bool kL2>
-__device__ __forceinline__ float packed_chain(const float* q, const uint8_t* map, uint32_t row, uint32_t dim);
-__device__ __forceinline__ void load_query(const uint8_t* qbuf, uint32_t grow, uint32_t dim, float* q);
+template <bool kL2, int DIM>
+__device__ __forceinline__ float packed_chain(const float (&q)[kPackK], const uint8_t* map, uint32_t row,
+                                              uint32_t dim);
+__device__ __forceinline__ void load_query(const uint8_t* qbuf, uint32_t grow, float (&q)[kPackK]);
 
-template <bool kL2>
+template <bool kL2, int DIM>
 __global__ void merge_kernel(MergeArgs a) {
     const uint32_t tp = blockIdx.x, r = threadIdx.x;
     const uint32_t pair = a.tp_pair[tp];
@@ -604,13 +617,13 @@ __global__ void merge_kernel(MergeArgs a) {
     if (best - second > a.margin[grow]) {
         // certified: the reference winner lies in `tile`; decide it exactly
         float q[kPackK];
-        load_query(a.qbuf, grow, a.dim, q);
+        load_query(a.qbuf, grow, q);
         const uint8_t* tm = a.tmap + pair * a.t_pair_bytes;
         const uint32_t t0 = tile * kSubTile, t1 = min(a.nt, t0 + kSubTile);
         float bd = INFINITY;
         uint32_t bi = t0;
         for (uint32_t t = t0; t < t1; ++t) {
-            const float d = packed_chain<kL2>(q, tm, t, a.dim);
+            const float d = packed_chain<kL2, DIM>(q, tm, t, a.dim);
             if (d < bd) {
                 bd = d;
                 bi = t;
@@ -629,21 +642,28 @@ __global__ void merge_kernel(MergeArgs a) {
 
 // ---------------------------------------------------------------- K4' rescan
 // Reference FMA chain on binary16 values (packed layout), channels < dim only.
-template <bool kL2>
-__device__ __forceinline__ float packed_chain(const float* q, const uint8_t* map, uint32_t row, uint32_t dim) {
+// Reference FMA chain over channels < dim of binary16 values (packed layout).
+// DIM > 0: dim is the compile-time constant DIM (query fully in registers);
+// DIM == 0: runtime dim <= kPackK (all loops unrolled to kPackK, predicated).
+template <bool kL2, int DIM>
+__device__ __forceinline__ float packed_chain(const float (&q)[kPackK], const uint8_t* map, uint32_t row,
+                                              uint32_t dim) {
     float acc = 0.0f;
-    for (uint32_t c0 = 0; c0 < dim; c0 += 8) {
-        const uint4 raw = *reinterpret_cast<const uint4*>(map + packed_offset(row, c0 >> 3));
-        const __half* h = reinterpret_cast<const __half*>(&raw);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            if (c0 + k < dim) {
-                const float t = __half2float(h[k]);
-                if constexpr (kL2) {
-                    const float d = __fsub_rn(q[c0 + k], t);
-                    acc = __fmaf_rn(d, d, acc);
-                } else {
-                    acc = __fmaf_rn(q[c0 + k], t, acc);
+    for (uint32_t c0 = 0; c0 < kPackK; c0 += 8) {
+        if (DIM > 0 ? c0 < (uint32_t)DIM : c0 < dim) {
+            const uint4 raw = *reinterpret_cast<const uint4*>(map + packed_offset(row, c0 >> 3));
+            const __half* h = reinterpret_cast<const __half*>(&raw);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                if (DIM > 0 ? c0 + k < (uint32_t)DIM : c0 + k < dim) {
+                    const float t = __half2float(h[k]);
+                    if constexpr (kL2) {
+                        const float d = __fsub_rn(q[c0 + k], t);
+                        acc = __fmaf_rn(d, d, acc);
+                    } else {
+                        acc = __fmaf_rn(q[c0 + k], t, acc);
+                    }
                 }
             }
         }
@@ -651,8 +671,9 @@ __device__ __forceinline__ float packed_chain(const float* q, const uint8_t* map
     return kL2 ? acc : -acc;
 }
 
-__device__ __forceinline__ void load_query(const uint8_t* qbuf, uint32_t grow, uint32_t dim, float* q) {
-    for (uint32_t c0 = 0; c0 < dim; c0 += 8) {
+__device__ __forceinline__ void load_query(const uint8_t* qbuf, uint32_t grow, float (&q)[kPackK]) {
+#pragma unroll
+    for (uint32_t c0 = 0; c0 < kPackK; c0 += 8) {
         const uint4 raw = *reinterpret_cast<const uint4*>(qbuf + packed_offset(grow, c0 >> 3));
         const __half* h = reinterpret_cast<const __half*>(&raw);
 #pragma unroll
@@ -679,7 +700,7 @@ struct RescanArgs {
 
 constexpr int kRescanThreads = 256;
 
-template <bool kL2>
+template <bool kL2, int DIM>
 __global__ void __launch_bounds__(kRescanThreads) rescan_kernel(RescanArgs a) {
     const uint32_t count = *a.rescan_count;
     const uint32_t nchunks = (a.nt + a.chunk - 1) / a.chunk;
@@ -688,12 +709,12 @@ __global__ void __launch_bounds__(kRescanThreads) rescan_kernel(RescanArgs a) {
     for (uint32_t unit = blockIdx.x; unit < count * nchunks; unit += gridDim.x) {
         const uint32_t k = unit / nchunks, ch = unit % nchunks;
         const uint32_t grow = a.rescan[3 * k], pair = a.rescan[3 * k + 1];
-        load_query(a.qbuf, grow, a.dim, q);
+        load_query(a.qbuf, grow, q);
         const uint8_t* tm = a.tmap + pair * a.t_pair_bytes;
         const uint32_t t0 = ch * a.chunk, t1 = min(a.nt, t0 + a.chunk);
         unsigned long long key = ~0ull;
         for (uint32_t t = t0 + threadIdx.x; t < t1; t += kRescanThreads)
-            key = umin64(key, (unsigned long long)pack_key(packed_chain<kL2>(q, tm, t, a.dim), t));
+            key = umin64(key, (unsigned long long)pack_key(packed_chain<kL2, DIM>(q, tm, t, a.dim), t));
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) key = umin64(key, __shfl_xor_sync(0xFFFFFFFFu, key, o));
         if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = key;
@@ -986,16 +1007,26 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     {
         MergeArgs m{partial, d_tp_pair, d_tp_row0, d_tp_qi0, splits, d_active, margin, qbuf, T.data,
                     T.pair_bytes, nt, dim, out, min_dist, out_stride, rescan, rcount, d_near_ties};
-        if (l2) merge_kernel<true><<<ntp, kQueryTilePair, 0, s>>>(m);
-        else merge_kernel<false><<<ntp, kQueryTilePair, 0, s>>>(m);
+        if (dim == 24) {
+            if (l2) merge_kernel<true, 24><<<ntp, kQueryTilePair, 0, s>>>(m);
+            else merge_kernel<false, 24><<<ntp, kQueryTilePair, 0, s>>>(m);
+        } else {
+            if (l2) merge_kernel<true, 0><<<ntp, kQueryTilePair, 0, s>>>(m);
+            else merge_kernel<false, 0><<<ntp, kQueryTilePair, 0, s>>>(m);
+        }
         FNL_CUDA_TRY(cudaGetLastError());
     }
     // ---- K4' exact re-decision of near ties (grid-stride over a device count)
     {
         RescanArgs r{rescan, rcount, qbuf, T.data, T.pair_bytes, nt, dim, 4096u, keys, l2};
         const uint32_t grid = 2 * (uint32_t)ctx_sm_count(ctx);
-        if (l2) rescan_kernel<true><<<grid, kRescanThreads, 0, s>>>(r);
-        else rescan_kernel<false><<<grid, kRescanThreads, 0, s>>>(r);
+        if (dim == 24) {
+            if (l2) rescan_kernel<true, 24><<<grid, kRescanThreads, 0, s>>>(r);
+            else rescan_kernel<false, 24><<<grid, kRescanThreads, 0, s>>>(r);
+        } else {
+            if (l2) rescan_kernel<true, 0><<<grid, kRescanThreads, 0, s>>>(r);
+            else rescan_kernel<false, 0><<<grid, kRescanThreads, 0, s>>>(r);
+        }
         FNL_CUDA_TRY(cudaGetLastError());
         rescan_finish_kernel<<<4, 256, 0, s>>>(rescan, rcount, keys, out, min_dist, out_stride, !l2);
         FNL_CUDA_TRY(cudaGetLastError());
