@@ -63,36 +63,64 @@ def pair_maps(k):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled during the timed region.
 
-    def __init__(self, index):
+    The sampler starts before the region (nvidia-smi needs ~0.1-0.3 s to come
+    up), a reader thread timestamps every line, and summary() keeps only the
+    samples taken between mark_start() and mark_end()."""
+
+    def __init__(self, index, period_ms=25):
         self.index = index
+        self.period_ms = period_ms
         self.proc = None
+        self.lines = []
+        self.t0 = self.t1 = None
 
     def __enter__(self):
+        import threading
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
+            return self
+        self.first = threading.Event()
+
+        def reader():
+            for line in self.proc.stdout:
+                self.lines.append((time.time(), line))
+                self.first.set()
+        self.thread = threading.Thread(target=reader, daemon=True)
+        self.thread.start()
+        self.first.wait(timeout=3.0)
         return self
 
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+
     def __exit__(self, *exc):
-        self.out = ""
         if self.proc:
             self.proc.terminate()
             try:
-                self.out, _ = self.proc.communicate(timeout=5)
+                self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+            self.thread.join(timeout=2)
 
     def summary(self):
         rows = []
-        for line in (self.out or "").splitlines():
+        for ts, line in self.lines:
+            if self.t0 is not None and ts < self.t0:
+                continue
+            if self.t1 is not None and ts > self.t1 + 0.05:
+                continue
             parts = [p.strip() for p in line.split(",")]
             if len(parts) >= 7:
                 try:
@@ -103,8 +131,7 @@ class ClockSampler:
             return None
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v.lower() == "active"})
-        loaded = [r[0] for r in rows if r[0] > 300] or [r[0] for r in rows]
-        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(r[1] for r in rows),
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
                 "reasons": reasons, "samples": len(rows)}
 
 
@@ -241,6 +268,7 @@ def main_b200(args):
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        clk.mark_start()
         ev0.record(stream)
         for _ in range(args.steps):
             stats = step_device()
@@ -248,10 +276,32 @@ def main_b200(args):
             near_ties += sum(s["near_tie_rows"] for s in stats)
         ev1.record(stream)
         torch.cuda.synchronize()
+        clk.mark_end()
     barrier()
     elapsed_ms = ev0.elapsed_time(ev1)
     timing = fnl.kernel_timing(reset=True)
     matches_last = int(out_counts.sum().item())
+
+    # ---- per-kernel-class breakdown: one extra step with events around every
+    # launch (outside the timed region; events add small gaps)
+    fnl.kernel_profile(enable=1, reset=True)
+    t_prof0 = torch.cuda.Event(enable_timing=True)
+    t_prof1 = torch.cuda.Event(enable_timing=True)
+    t_prof0.record(stream)
+    step_device()
+    t_prof1.record(stream)
+    torch.cuda.synchronize()
+    prof = fnl.kernel_profile(enable=0, reset=True)
+    fnl.kernel_timing(reset=True)
+    prof_step_ms = t_prof0.elapsed_time(t_prof1)
+    # algorithmic HBM bytes of K1: fp32 rows in, binary16 UMMA rows out, both maps
+    pack_bytes = 2 * B * NT * (D * 4 + 64)
+    breakdown = {k: {"ms": round(v["ms"], 4), "launches": int(v["launches"])}
+                 for k, v in prof.items() if v["launches"]}
+    breakdown["step_ms"] = round(prof_step_ms, 4)
+    breakdown["unattributed_ms"] = round(prof_step_ms - sum(v["ms"] for v in prof.values()), 4)
+    if prof["pack"]["ms"] > 0:
+        breakdown["pack"]["hbm_gbs"] = round(pack_bytes / (prof["pack"]["ms"] / 1e3) / 1e9, 1)
 
     # ---- e2e through the public host-buffer batch API
     n1, n2 = h1.numpy(), h2.numpy()
@@ -318,7 +368,8 @@ def main_b200(args):
                              "per GPU per step > 126 MB L2 (no L2 flush needed)",
                    "query_rows_per_step": tot_rows / args.steps,
                    "near_tie_rows_per_step": near_ties / args.steps if world == 1 else None,
-                   "matches_per_step_rank0": matches_last},
+                   "matches_per_step_rank0": matches_last,
+                   "kernel_breakdown_rank0": breakdown},
         "e2e": {"value": e2e_value, "unit": "pairs/s",
                 "h2d_bytes_per_step": int(2 * B * H * W * D * 4),
                 "d2h_bytes_per_step": int(B * samples * 3 * 4 + B * 4)},
@@ -339,7 +390,7 @@ def main_b200(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--pairs", type=int, default=128, help="pairs per GPU per step")
     ap.add_argument("--backend", default="tensor")

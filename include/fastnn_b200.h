@@ -173,6 +173,25 @@ int fnl_tensor_selftest(fnl_context* ctx, const float* h_queries, const float* h
 int fnl_kernel_timing(fnl_context* ctx, int reset, double* score_ms, uint64_t* score_launches,
                       uint64_t* total_launches);
 
+/* Per-kernel-class device time (CUDA events around every launch of the class,
+ * on the context stream) since the last reset.  enable = 1 turns the
+ * non-score classes on, 0 off, -1 leaves the setting; class_ms and
+ * class_launches (may be null) receive FNL_KCLASS_COUNT entries.  The score
+ * class is always timed (same numbers as fnl_kernel_timing). */
+enum {
+    FNL_KCLASS_SCORE = 0,   /* K3 tcgen05 score + running argmax / K4 exact scan  */
+    FNL_KCLASS_PACK = 1,    /* K1 fp32 -> binary16 pack (tensor) / prepare (exact) */
+    FNL_KCLASS_GATHER = 2,  /* K2 query gather + certification margin              */
+    FNL_KCLASS_MERGE = 3,   /* K3b split merge + certification + sub-tile resolve  */
+    FNL_KCLASS_RESCAN = 4,  /* K4' exact re-decision of uncertified rows           */
+    FNL_KCLASS_HARVEST = 5, /* K5 harvest / compaction / convergence, K6 init      */
+    FNL_KCLASS_ATTN = 6,    /* K7 FlashMatch attention                             */
+    FNL_KCLASS_OTHER = 7,
+    FNL_KCLASS_COUNT = 8
+};
+int fnl_kernel_profile(fnl_context* ctx, int enable, int reset, double* class_ms,
+                       uint64_t* class_launches);
+
 #ifdef __cplusplus
 }
 #endif

@@ -26,6 +26,7 @@ try:
         gen_matched_pair,
         gen_random,
         grid_subsample,
+        kernel_profile,
         kernel_timing,
         mutual_nn_exact,
         nn_bruteforce,
@@ -68,6 +69,7 @@ __all__ = [
     "reciprocal_match_batch",
     "reciprocal_match_device",
     "kernel_timing",
+    "kernel_profile",
     "device_count",
     "set_device",
     "abi_version",

@@ -400,6 +400,26 @@ PYBIND11_MODULE(_fastnn, m) {
           py::arg("reset") = false,
           "device time and launch count of the dominant scoring kernel since the last reset");
 
+    m.def("kernel_profile",
+          [](int enable, bool reset) {
+              double ms[FNL_KCLASS_COUNT] = {};
+              std::uint64_t n[FNL_KCLASS_COUNT] = {};
+              fastnn::b200::check(fnl_kernel_profile(fastnn::b200::context(), enable, reset ? 1 : 0, ms, n));
+              static const char* names[FNL_KCLASS_COUNT] = {"score", "pack", "gather", "merge",
+                                                            "rescan", "harvest", "attention", "other"};
+              py::dict d;
+              for (int c = 0; c < FNL_KCLASS_COUNT; ++c) {
+                  py::dict e;
+                  e["ms"] = ms[c];
+                  e["launches"] = n[c];
+                  d[names[c]] = e;
+              }
+              return d;
+          },
+          py::arg("enable") = -1, py::arg("reset") = false,
+          "per-kernel-class device time (CUDA events) since the last reset; enable=1/0 turns the "
+          "breakdown of the non-score classes on/off");
+
     m.def("_tensor_selftest",
           [](const F32& q, const F32& t, const std::string& metric, int mode) {
               if (q.ndim() != 2 || t.ndim() != 2 || q.shape(0) != 256 || t.shape(0) != 128 || q.shape(1) != t.shape(1))

@@ -53,9 +53,17 @@ struct fnl_context {
     std::map<std::string, Buf> pinned;
     // instrumentation of the dominant scoring kernel
     bool timing = true;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used, ev_free;
+    bool profile_all = false;  // per-kernel-class breakdown (fnl_kernel_profile)
+    struct Mark {
+        int cls;
+        cudaEvent_t a, b;
+    };
+    std::vector<Mark> ev_used;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_free;
     double score_ms = 0.0;
     uint64_t score_launches = 0, total_launches = 0;
+    double class_ms[FNL_KCLASS_COUNT] = {};
+    uint64_t class_launches[FNL_KCLASS_COUNT] = {};
 };
 
 namespace {
@@ -101,10 +109,12 @@ int dev_arr(fnl_context* ctx, const char* name, size_t count, T** out) {
 
 uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
-// Score-kernel timing: events bracket every dominant-kernel launch.
-void timing_begin(fnl_context* ctx, cudaEvent_t* a, cudaEvent_t* b) {
+// Kernel timing: events bracket every dominant-kernel launch (class
+// FNL_KCLASS_SCORE) and, when profiling is on, every other kernel class.
+void timing_begin(fnl_context* ctx, cudaEvent_t* a, cudaEvent_t* b, int cls = FNL_KCLASS_SCORE) {
     *a = *b = nullptr;
     if (!ctx->timing) return;
+    if (cls != FNL_KCLASS_SCORE && !ctx->profile_all) return;
     std::pair<cudaEvent_t, cudaEvent_t> ev;
     if (!ctx->ev_free.empty()) {
         ev = ctx->ev_free.back();
@@ -114,20 +124,24 @@ void timing_begin(fnl_context* ctx, cudaEvent_t* a, cudaEvent_t* b) {
         cudaEventCreate(&ev.second);
     }
     cudaEventRecord(ev.first, ctx->stream);
-    ctx->ev_used.push_back(ev);
+    ctx->ev_used.push_back({cls, ev.first, ev.second});
     *a = ev.first;
     *b = ev.second;
 }
-void timing_end(fnl_context* ctx, cudaEvent_t b) {
-    ctx->score_launches++;
+void timing_end(fnl_context* ctx, cudaEvent_t b, int cls = FNL_KCLASS_SCORE) {
+    if (cls == FNL_KCLASS_SCORE) ctx->score_launches++;
+    ctx->class_launches[cls]++;
     if (b) cudaEventRecord(b, ctx->stream);
 }
 void timing_harvest(fnl_context* ctx) {
     // caller has synchronised the stream
-    for (auto& ev : ctx->ev_used) {
+    for (auto& m : ctx->ev_used) {
         float ms = 0.0f;
-        if (cudaEventElapsedTime(&ms, ev.first, ev.second) == cudaSuccess) ctx->score_ms += ms;
-        ctx->ev_free.push_back(ev);
+        if (cudaEventElapsedTime(&ms, m.a, m.b) == cudaSuccess) {
+            if (m.cls == FNL_KCLASS_SCORE) ctx->score_ms += ms;
+            ctx->class_ms[m.cls] += ms;
+        }
+        ctx->ev_free.push_back({m.a, m.b});
     }
     ctx->ev_used.clear();
 }
@@ -221,6 +235,7 @@ int prepare_maps(fnl_context* ctx, const char* tag, const float* d_src, uint32_t
         a.row_sat = out->row_sat;
         out->data = r;
     }
+    fnl::ProfScope prof(ctx, FNL_KCLASS_PACK);
     if (nmaps == 1) {
         FNL_CUDA_TRY(fnl::launch_prepare(a, ctx->stream));
     } else {
@@ -247,7 +262,10 @@ int exact_nn(fnl_context* ctx, const fnl::ScanArgs& sa, uint32_t max_q, uint32_t
     timing_begin(ctx, &e0, &e1);
     FNL_CUDA_TRY(fnl::launch_exact_scan(sa, max_q, npairs, l2, hybrid, ctx->stream));
     timing_end(ctx, e1);
-    FNL_CUDA_TRY(fnl::launch_finalize(fa, max_q, npairs, ctx->stream));
+    {
+        fnl::ProfScope prof(ctx, FNL_KCLASS_OTHER);
+        FNL_CUDA_TRY(fnl::launch_finalize(fa, max_q, npairs, ctx->stream));
+    }
     ctx->total_launches += 2;
     return FNL_OK;
 }
@@ -280,6 +298,11 @@ void ctx_score_begin(fnl_context* ctx, cudaEvent_t* end_event) {
     timing_begin(ctx, &a, end_event);
 }
 void ctx_score_end(fnl_context* ctx, cudaEvent_t end_event) { timing_end(ctx, end_event); }
+void ctx_prof_begin(fnl_context* ctx, int cls, cudaEvent_t* end_event) {
+    cudaEvent_t a;
+    timing_begin(ctx, &a, end_event, cls);
+}
+void ctx_prof_end(fnl_context* ctx, int cls, cudaEvent_t end_event) { timing_end(ctx, end_event, cls); }
 void ctx_count_launches(fnl_context* ctx, int n) { ctx->total_launches += n; }
 }  // namespace fnl
 
@@ -335,7 +358,7 @@ extern "C" int fnl_context_destroy(fnl_context* ctx) {
     cudaStreamSynchronize(ctx->stream);
     for (auto& kv : ctx->dev) cudaFree(kv.second.p);
     for (auto& kv : ctx->pinned) cudaFreeHost(kv.second.p);
-    for (auto& ev : ctx->ev_used) { cudaEventDestroy(ev.first); cudaEventDestroy(ev.second); }
+    for (auto& m : ctx->ev_used) { cudaEventDestroy(m.a); cudaEventDestroy(m.b); }
     for (auto& ev : ctx->ev_free) { cudaEventDestroy(ev.first); cudaEventDestroy(ev.second); }
     cudaStreamDestroy(ctx->own_stream);
     cudaStreamDestroy(ctx->copy_stream);
@@ -369,6 +392,23 @@ extern "C" int fnl_kernel_timing(fnl_context* ctx, int reset, double* score_ms,
         ctx->score_launches = 0;
         ctx->total_launches = 0;
     }
+    return FNL_OK;
+}
+
+extern "C" int fnl_kernel_profile(fnl_context* ctx, int enable, int reset, double* class_ms,
+                                  uint64_t* class_launches) {
+    TRY(check_device(ctx));
+    FNL_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    timing_harvest(ctx);
+    for (int c = 0; c < FNL_KCLASS_COUNT; ++c) {
+        if (class_ms) class_ms[c] = ctx->class_ms[c];
+        if (class_launches) class_launches[c] = ctx->class_launches[c];
+        if (reset) {
+            ctx->class_ms[c] = 0.0;
+            ctx->class_launches[c] = 0;
+        }
+    }
+    if (enable >= 0) ctx->profile_all = enable != 0;
     return FNL_OK;
 }
 
@@ -626,7 +666,10 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
     }
     PhaseTimer timer{ctx};
     timer.begin(kPhaseSubsample);
-    FNL_CUDA_TRY(fnl::launch_match_init(m, s));
+    {
+        fnl::ProfScope prof(ctx, FNL_KCLASS_HARVEST);
+        FNL_CUDA_TRY(fnl::launch_match_init(m, s));
+    }
     timer.end();
 
     // ---- NN pass helper: queries = rows of qmap at ids, targets = tmap
@@ -681,7 +724,10 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
         TRY(nn_pass(P2, p2, m.active_v, P1, p1, m.back));
         timer.end();
         timer.begin(kPhaseHarvest);
-        FNL_CUDA_TRY(fnl::launch_harvest(m, t, s));
+        {
+            fnl::ProfScope prof(ctx, FNL_KCLASS_HARVEST);
+            FNL_CUDA_TRY(fnl::launch_harvest(m, t, s));
+        }
         timer.end();
         ctx->total_launches += 1;
         unsigned int ndone = 0;

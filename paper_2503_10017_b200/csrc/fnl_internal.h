@@ -33,6 +33,16 @@ int ws_arr(fnl_context* ctx, const char* name, size_t count, T** out) {
 void ctx_score_begin(fnl_context* ctx, cudaEvent_t* end_event);
 void ctx_score_end(fnl_context* ctx, cudaEvent_t end_event);
 void ctx_count_launches(fnl_context* ctx, int n);
+// brackets one launch of kernel class cls (FNL_KCLASS_*); no-op unless profiling
+void ctx_prof_begin(fnl_context* ctx, int cls, cudaEvent_t* end_event);
+void ctx_prof_end(fnl_context* ctx, int cls, cudaEvent_t end_event);
+struct ProfScope {
+    fnl_context* ctx;
+    int cls;
+    cudaEvent_t end = nullptr;
+    ProfScope(fnl_context* c, int k) : ctx(c), cls(k) { ctx_prof_begin(ctx, cls, &end); }
+    ~ProfScope() { ctx_prof_end(ctx, cls, end); }
+};
 
 // ---------------------------------------------------------------- K1 prepare
 // Validates finiteness (first offending flat index into *bad_index, which the

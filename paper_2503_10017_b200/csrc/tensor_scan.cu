@@ -126,7 +126,12 @@ __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
 }
 
 // ---------------------------------------------------------------- K1 pack
-// 4 threads per row (one 8-channel chunk each), 8 rows per warp = one group.
+// HBM-bound stream: 4 lanes per row (one 8-channel chunk each), so a warp
+// covers one 8-row group = 768 B of fp32 in and 512 B of binary16 out, both
+// fully coalesced.  Blocks are persistent per pair (grid-stride over the
+// pair's row groups, two groups in flight per warp), and the per-pair max
+// norm / saturation count are reduced in the block, so a map costs a handful
+// of atomics instead of one per warp.
 struct PackArgs {
     const float* src;
     uint8_t* dst;
@@ -140,29 +145,31 @@ struct PackArgs {
     unsigned long long* sat;         // per pair saturation count
 };
 
-__global__ void pack_kernel(PackArgs a) {
-    const uint32_t pair = blockIdx.y;
-    const uint32_t gthread = blockIdx.x * blockDim.x + threadIdx.x;
-    const uint32_t row = gthread >> 2, chunk = gthread & 3u;
-    if (row >= a.rows_pad) return;  // whole groups of 4 lanes exit together
+constexpr int kPackThreads = 256;
+
+__device__ __forceinline__ void pack_load(const PackArgs& a, const float* src, uint32_t row, uint32_t chunk,
+                                          float (&v)[8]) {
     const bool real = row < a.rows;
-    const float* src = a.src + ((uint64_t)pair * a.rows + row) * a.dim;
-    float v[8];
-    uint32_t sat = 0;
-    float ss = 0.0f;
     const bool vec = (a.dim & 7u) == 0 && chunk * 8 < a.dim;  // whole 8-channel chunk, 32 B aligned
     if (real && vec) {
-        const float4 lo = __ldg(reinterpret_cast<const float4*>(src + chunk * 8));
-        const float4 hi = __ldg(reinterpret_cast<const float4*>(src + chunk * 8 + 4));
+        const float4 lo = __ldcs(reinterpret_cast<const float4*>(src + (uint64_t)row * a.dim + chunk * 8));
+        const float4 hi = __ldcs(reinterpret_cast<const float4*>(src + (uint64_t)row * a.dim + chunk * 8 + 4));
         v[0] = lo.x; v[1] = lo.y; v[2] = lo.z; v[3] = lo.w;
         v[4] = hi.x; v[5] = hi.y; v[6] = hi.z; v[7] = hi.w;
     } else {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const uint32_t c = chunk * 8 + i;
-            v[i] = (real && c < a.dim) ? src[c] : 0.0f;
+            v[i] = (real && c < a.dim) ? src[(uint64_t)row * a.dim + c] : 0.0f;
         }
     }
+}
+
+// rounds one row chunk, writes it, returns the row's norm (0 for padding rows)
+__device__ __forceinline__ float pack_store(const PackArgs& a, uint8_t* dst, uint32_t pair, uint32_t row,
+                                            uint32_t chunk, float (&v)[8], uint32_t& sat) {
+    const bool real = row < a.rows;
+    float ss = 0.0f;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         float x = v[i];
@@ -191,14 +198,55 @@ __global__ void pack_kernel(PackArgs a) {
     out.y = pack_half2(v[2], v[3]);
     out.z = pack_half2(v[4], v[5]);
     out.w = pack_half2(v[6], v[7]);
-    *reinterpret_cast<uint4*>(a.dst + pair * a.pair_bytes + packed_offset(row, chunk)) = out;
-    const uint32_t wsat = warp_sum(sat);
-    if ((threadIdx.x & 31) == 0 && wsat) atomicAdd(a.sat + pair, (unsigned long long)wsat);
-    // one atomic per warp (8 rows): non-negative floats order like their bits
-    uint32_t nb = real ? __float_as_uint(sqrtf(ss)) : 0u;
+    *reinterpret_cast<uint4*>(dst + packed_offset(row, chunk)) = out;
+    return real ? sqrtf(ss) : 0.0f;
+}
+
+__global__ void __launch_bounds__(kPackThreads) pack_kernel(PackArgs a) {
+    const uint32_t pair = blockIdx.y;
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint32_t chunk = lane & 3u, sub = lane >> 2;
+    const float* src = a.src + (uint64_t)pair * a.rows * a.dim;
+    uint8_t* dst = a.dst + pair * a.pair_bytes;
+    const uint32_t groups = a.rows_pad >> 3;
+    const uint32_t gstride = gridDim.x * (kPackThreads / 32);
+    uint32_t sat = 0;
+    float nmax = 0.0f;
+    uint32_t g = blockIdx.x * (kPackThreads / 32) + warp;
+    for (; g + gstride < groups; g += 2 * gstride) {  // two row groups in flight
+        float v0[8], v1[8];
+        pack_load(a, src, g * 8 + sub, chunk, v0);
+        pack_load(a, src, (g + gstride) * 8 + sub, chunk, v1);
+        nmax = fmaxf(nmax, pack_store(a, dst, pair, g * 8 + sub, chunk, v0, sat));
+        nmax = fmaxf(nmax, pack_store(a, dst, pair, (g + gstride) * 8 + sub, chunk, v1, sat));
+    }
+    if (g < groups) {
+        float v0[8];
+        pack_load(a, src, g * 8 + sub, chunk, v0);
+        nmax = fmaxf(nmax, pack_store(a, dst, pair, g * 8 + sub, chunk, v0, sat));
+    }
+    // block reduction: one atomic per block per counter
+    __shared__ uint32_t red_sat[kPackThreads / 32];
+    __shared__ float red_max[kPackThreads / 32];
+    sat = warp_sum(sat);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) nb = max(nb, __shfl_xor_sync(0xFFFFFFFFu, nb, o));
-    if ((threadIdx.x & 31) == 0 && nb) atomicMax(reinterpret_cast<unsigned int*>(a.max_norm) + pair, nb);
+    for (int o = 16; o > 0; o >>= 1) nmax = fmaxf(nmax, __shfl_xor_sync(0xFFFFFFFFu, nmax, o));
+    if (lane == 0) {
+        red_sat[warp] = sat;
+        red_max[warp] = nmax;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t ts = 0;
+        float tm = 0.0f;
+        for (int w = 0; w < kPackThreads / 32; ++w) {
+            ts += red_sat[w];
+            tm = fmaxf(tm, red_max[w]);
+        }
+        if (ts) atomicAdd(a.sat + pair, (unsigned long long)ts);
+        // non-negative floats order like their bits
+        if (tm > 0.0f) atomicMax(reinterpret_cast<unsigned int*>(a.max_norm) + pair, __float_as_uint(tm));
+    }
 }
 
 // ---------------------------------------------------------------- K2 gather
@@ -286,7 +334,7 @@ struct TcArgs {
     uint32_t nt;
     const TcItem* items;
     uint32_t nitems;
-    float4* partial;  // [item][2 sets][256] = (best, second, idx bits, 0)
+    float4* partial;  // [item][256][2] = (b1, b2, b3, t1 bits), (t2 bits, 0, 0, 0)
     int debug;        // profiling only: 1 = epilogue releases buffers unread, 16 = clock trace of CTA 0
     unsigned long long* trace;  // [4][4096] clock64 stamps (debug & 16)
 };
@@ -331,16 +379,15 @@ __device__ __forceinline__ bool elect_one() {
 }
 
 // Per query row and 64-target sub-tile: m = max of the 64 fp32 scores
-// (3-input-max tree, ~0.5 ALU op per score, no data-dependent branch), then
-//   best' = max(best, m), second' = max(second, min(best, m)),
-//   tile'  = m > best ? this sub-tile : tile.
-// `best` is the largest sub-tile maximum, `tile` the first sub-tile reaching
-// it, `second` the largest maximum of every other sub-tile.  The merge kernel
-// certifies best - second > margin (no score outside the winning sub-tile can
-// be the reference winner) and resolves that sub-tile with the exact chain.
+// (3-input-max tree, ~0.5 ALU op per score, no data-dependent branch), then a
+// branch-free insert of (m, sub-tile) into the row's top-3 of sub-tile maxima:
+// b1 >= b2 >= b3 with the sub-tiles t1, t2 of the first two.  The merge kernel
+// certifies b1 - b2 > margin (the reference winner lies in t1) or else
+// b1 - b3 > margin (it lies in t1 or t2) and resolves those sub-tiles with the
+// exact chain; only rows with three sub-tiles inside the margin are re-scanned.
 struct RowState {
-    float best, second;
-    uint32_t tile;
+    float b1, b2, b3;
+    uint32_t t1, t2;
 };
 
 __device__ __forceinline__ float tile_max64(const float* v) {
@@ -356,9 +403,12 @@ __device__ __forceinline__ float tile_max64(const float* v) {
 }
 
 __device__ __forceinline__ void tile_update(RowState& st, float m, uint32_t tile) {
-    st.second = fmaxf(st.second, fminf(st.best, m));
-    st.tile = m > st.best ? tile : st.tile;
-    st.best = fmaxf(st.best, m);
+    const bool gt1 = m > st.b1, gt2 = m > st.b2;
+    st.b3 = fmaxf(st.b3, fminf(st.b2, m));
+    st.t2 = gt1 ? st.t1 : (gt2 ? tile : st.t2);
+    st.b2 = fmaxf(st.b2, fminf(st.b1, m));
+    st.t1 = gt1 ? tile : st.t1;
+    st.b1 = fmaxf(st.b1, m);
 }
 
 // tcgen05.ld of 32 columns whose destination registers are tied to the
@@ -528,7 +578,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
         for (uint32_t u = blockIdx.x; u < a.nitems; u += G) {
             const TcItem item = a.items[u];
             const bool warp_real = qt * 128u + quad * 32u < item.nvalid;  // else all rows padding
-            RowState st{-INFINITY, -INFINITY, 0xFFFFFFFFu};
+            RowState st{-INFINITY, -INFINITY, -INFINITY, 0xFFFFFFFFu, 0xFFFFFFFFu};
             for (uint32_t t = item.tile_begin; t < item.tile_end; ++t, ++k) {
                 const uint32_t acc = k % kAccBufs;
                 const bool next = k + kAccBufs < total;
@@ -556,11 +606,12 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
                 subtile_scan(st, f2, f3, 2 * t + 1, a.nt);
                 if (tw) {
                     __syncwarp();
-                    if (lane == 0) a.trace[20480 + k] = clock64() + (st.best > 1e30f ? 1 : 0);
+                    if (lane == 0) a.trace[20480 + k] = clock64() + (st.b1 > 1e30f ? 1 : 0);
                 }
             }
-            a.partial[(uint64_t)u * kQueryTilePair + row] =
-                make_float4(st.best, st.second, __uint_as_float(st.tile), 0.0f);
+            float4* po = a.partial + ((uint64_t)u * kQueryTilePair + row) * 2;
+            po[0] = make_float4(st.b1, st.b2, st.b3, __uint_as_float(st.t1));
+            po[1] = make_float4(__uint_as_float(st.t2), 0.0f, 0.0f, 0.0f);
         }
     }
     tc_fence_before();
@@ -604,39 +655,63 @@ __global__ void merge_kernel(MergeArgs a) {
     const uint32_t pair = a.tp_pair[tp];
     const uint32_t qi = a.tp_qi0[tp] + r;
     if (qi >= a.n_active[pair]) return;
-    float best = -INFINITY, second = -INFINITY;
-    uint32_t tile = 0;
+    // global top-3 of sub-tile maxima over the target splits: each split's
+    // (b1, t1), (b2, t2) are candidates, its b3 bounds every other sub-tile
+    float B1 = -INFINITY, B2 = -INFINITY, B3 = -INFINITY;
+    uint32_t T1 = 0, T2 = 0xFFFFFFFFu;
+    auto insert = [&](float v, uint32_t t) {
+        if (v > B1) {
+            B3 = fmaxf(B3, B2);
+            B2 = B1;
+            T2 = T1;
+            B1 = v;
+            T1 = t;
+        } else if (v > B2) {
+            B3 = fmaxf(B3, B2);
+            B2 = v;
+            T2 = t;
+        } else {
+            B3 = fmaxf(B3, v);
+        }
+    };
     for (uint32_t s = 0; s < a.splits; ++s) {
-        const float4 p = a.partial[((uint64_t)tp * a.splits + s) * kQueryTilePair + r];
-        second = fmaxf(second, fmaxf(p.y, fminf(best, p.x)));
-        if (p.x > best) tile = __float_as_uint(p.z);
-        best = fmaxf(best, p.x);
+        const float4* pp = a.partial + (((uint64_t)tp * a.splits + s) * kQueryTilePair + r) * 2;
+        const float4 p = pp[0];
+        const float4 p2 = pp[1];
+        insert(p.x, __float_as_uint(p.w));
+        insert(p.y, __float_as_uint(p2.x));
+        B3 = fmaxf(B3, p.z);
     }
     const uint32_t grow = a.tp_row0[tp] + r;
     const uint64_t o = (uint64_t)pair * a.out_stride + qi;
-    if (best - second > a.margin[grow]) {
-        // certified: the reference winner lies in `tile`; decide it exactly
+    const float margin = a.margin[grow];
+    const bool top1 = B1 - B2 > margin;
+    if (!top1) atomicAdd(a.near_ties + pair, 1ull);  // top-2 gap inside the error bound
+    if (top1 || B1 - B3 > margin) {
+        // certified: the reference winner lies in T1 (or T1 / T2); decide exactly,
+        // lowest index on exact ties via the packed (dist, index) key
         float q[kPackK];
         load_query(a.qbuf, grow, q);
         const uint8_t* tm = a.tmap + pair * a.t_pair_bytes;
-        const uint32_t t0 = tile * kSubTile, t1 = min(a.nt, t0 + kSubTile);
-        float bd = INFINITY;
-        uint32_t bi = t0;
-        for (uint32_t t = t0; t < t1; ++t) {
-            const float d = packed_chain<kL2, DIM>(q, tm, t, a.dim);
-            if (d < bd) {
-                bd = d;
-                bi = t;
+        unsigned long long key = ~0ull;
+        for (int c = 0; c < (top1 ? 1 : 2); ++c) {
+            const uint32_t t0 = (c ? T2 : T1) * kSubTile, t1 = min(a.nt, t0 + kSubTile);
+            for (uint32_t t = t0; t < t1; ++t) {
+                const unsigned long long k = pack_key(packed_chain<kL2, DIM>(q, tm, t, a.dim), t);
+                key = k < key ? k : key;
             }
         }
-        a.out[o] = bi;
-        if (a.min_dist) a.min_dist[o] = bd;
+        a.out[o] = (uint32_t)(key & 0xFFFFFFFFull);
+        if (a.min_dist) {
+            float d = from_orderable((uint32_t)(key >> 32));
+            if (d == 0.0f) d = kL2 ? 0.0f : -0.0f;  // canonical sign of an exact zero
+            a.min_dist[o] = d;
+        }
     } else {
         const uint32_t k = atomicAdd(a.rescan_count, 1u);
         a.rescan[3 * k] = grow;
         a.rescan[3 * k + 1] = pair;
         a.rescan[3 * k + 2] = qi;
-        atomicAdd(a.near_ties + pair, 1ull);
     }
 }
 
@@ -871,9 +946,12 @@ int tensor_pack(fnl_context* ctx, const char* tag, const float* d_src, uint32_t 
     out->rows = rows;
     out->npairs = npairs;
     PackArgs a{d_src, out->data, pair_bytes, rows, rows_pad, dim, l2, out->max_norm, d_bad, d_sat};
-    const uint32_t threads = rows_pad * 4;
-    dim3 grid(ceil_div_u(threads, 256), npairs);
-    pack_kernel<<<grid, 256, 0, s>>>(a);
+    // ~8 resident blocks per SM over the whole batch, at least one per pair
+    const uint32_t groups = rows_pad / 8, warps = kPackThreads / 32;
+    const uint32_t want = std::max<uint32_t>(1, ceil_div_u(8u * (uint32_t)ctx_sm_count(ctx), npairs));
+    dim3 grid(std::min(want, ceil_div_u(groups, warps)), npairs);
+    ProfScope prof(ctx, FNL_KCLASS_PACK);
+    pack_kernel<<<grid, kPackThreads, 0, s>>>(a);
     FNL_CUDA_TRY(cudaGetLastError());
     ctx_count_launches(ctx, 1);
     return FNL_OK;
@@ -964,7 +1042,7 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     uint32_t* d_active;
     TRY(ws_arr(ctx, "tc.qbuf", (size_t)rows_total * kPackRowBytes, &qbuf));
     TRY(ws_arr(ctx, "tc.margin", rows_total, &margin));
-    TRY(ws_arr(ctx, "tc.partial", (size_t)nitems * kQueryTilePair, &partial));
+    TRY(ws_arr(ctx, "tc.partial", (size_t)nitems * kQueryTilePair * 2, &partial));
     TRY(ws_arr(ctx, "tc.rescan", (size_t)3 * rows_total, &rescan));
     TRY(ws_arr(ctx, "tc.rcount", 1, &rcount));
     TRY(ws_arr(ctx, "tc.keys", rows_total, &keys));
@@ -984,6 +1062,7 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
         uint32_t max_rows = 0;
         for (uint32_t p : slot_pair) max_rows = std::max(max_rows, ceil_div_u(h_active[p], kQueryTilePair) * kQueryTilePair);
         dim3 grid(ceil_div_u(max_rows * 4, 256), nslots);
+        ProfScope prof(ctx, FNL_KCLASS_GATHER);
         gather_kernel<<<grid, 256, 0, s>>>(g);
         FNL_CUDA_TRY(cudaGetLastError());
     }
@@ -1007,6 +1086,7 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     {
         MergeArgs m{partial, d_tp_pair, d_tp_row0, d_tp_qi0, splits, d_active, margin, qbuf, T.data,
                     T.pair_bytes, nt, dim, out, min_dist, out_stride, rescan, rcount, d_near_ties};
+        ProfScope prof(ctx, FNL_KCLASS_MERGE);
         if (dim == 24) {
             if (l2) merge_kernel<true, 24><<<ntp, kQueryTilePair, 0, s>>>(m);
             else merge_kernel<false, 24><<<ntp, kQueryTilePair, 0, s>>>(m);
@@ -1020,6 +1100,7 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     {
         RescanArgs r{rescan, rcount, qbuf, T.data, T.pair_bytes, nt, dim, 4096u, keys, l2};
         const uint32_t grid = 2 * (uint32_t)ctx_sm_count(ctx);
+        ProfScope prof(ctx, FNL_KCLASS_RESCAN);
         if (dim == 24) {
             if (l2) rescan_kernel<true, 24><<<grid, kRescanThreads, 0, s>>>(r);
             else rescan_kernel<false, 24><<<grid, kRescanThreads, 0, s>>>(r);
