@@ -202,50 +202,60 @@ __device__ __forceinline__ float pack_store(const PackArgs& a, uint8_t* dst, uin
     return real ? sqrtf(ss) : 0.0f;
 }
 
-__global__ void __launch_bounds__(kPackThreads) pack_kernel(PackArgs a) {
-    const uint32_t pair = blockIdx.y;
-    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    const uint32_t chunk = lane & 3u, sub = lane >> 2;
-    const float* src = a.src + (uint64_t)pair * a.rows * a.dim;
-    uint8_t* dst = a.dst + pair * a.pair_bytes;
-    const uint32_t groups = a.rows_pad >> 3;
-    const uint32_t gstride = gridDim.x * (kPackThreads / 32);
-    uint32_t sat = 0;
-    float nmax = 0.0f;
-    uint32_t g = blockIdx.x * (kPackThreads / 32) + warp;
-    for (; g + gstride < groups; g += 2 * gstride) {  // two row groups in flight
-        float v0[8], v1[8];
-        pack_load(a, src, g * 8 + sub, chunk, v0);
-        pack_load(a, src, (g + gstride) * 8 + sub, chunk, v1);
-        nmax = fmaxf(nmax, pack_store(a, dst, pair, g * 8 + sub, chunk, v0, sat));
-        nmax = fmaxf(nmax, pack_store(a, dst, pair, (g + gstride) * 8 + sub, chunk, v1, sat));
-    }
-    if (g < groups) {
-        float v0[8];
-        pack_load(a, src, g * 8 + sub, chunk, v0);
-        nmax = fmaxf(nmax, pack_store(a, dst, pair, g * 8 + sub, chunk, v0, sat));
-    }
-    // block reduction: one atomic per block per counter
-    __shared__ uint32_t red_sat[kPackThreads / 32];
-    __shared__ float red_max[kPackThreads / 32];
+__device__ __forceinline__ void pack_flush(const PackArgs& a, uint32_t pair, uint32_t& sat, float& nmax) {
     sat = warp_sum(sat);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) nmax = fmaxf(nmax, __shfl_xor_sync(0xFFFFFFFFu, nmax, o));
-    if (lane == 0) {
-        red_sat[warp] = sat;
-        red_max[warp] = nmax;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t ts = 0;
-        float tm = 0.0f;
-        for (int w = 0; w < kPackThreads / 32; ++w) {
-            ts += red_sat[w];
-            tm = fmaxf(tm, red_max[w]);
-        }
-        if (ts) atomicAdd(a.sat + pair, (unsigned long long)ts);
+    if ((threadIdx.x & 31u) == 0) {
+        if (sat) atomicAdd(a.sat + pair, (unsigned long long)sat);
         // non-negative floats order like their bits
-        if (tm > 0.0f) atomicMax(reinterpret_cast<unsigned int*>(a.max_norm) + pair, __float_as_uint(tm));
+        if (nmax > 0.0f) atomicMax(reinterpret_cast<unsigned int*>(a.max_norm) + pair, __float_as_uint(nmax));
+    }
+    sat = 0;
+    nmax = 0.0f;
+}
+
+// Flat over (pair, 8-row group): warp w owns a contiguous range of groups of
+// the whole batch (exactly one wave of warps, no tail), two groups in flight;
+// counters are flushed once per pair the warp touches.
+__global__ void __launch_bounds__(kPackThreads) pack_kernel(PackArgs a, uint32_t npairs) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t chunk = lane & 3u, sub = lane >> 2;
+    const uint32_t groups = a.rows_pad >> 3;
+    const uint64_t total = (uint64_t)npairs * groups;
+    const uint64_t nwarps = (uint64_t)gridDim.x * (kPackThreads / 32);
+    const uint64_t w = (uint64_t)blockIdx.x * (kPackThreads / 32) + (threadIdx.x >> 5);
+    uint64_t g = total * w / nwarps;
+    const uint64_t end = total * (w + 1) / nwarps;
+    if (g >= end) return;
+    uint32_t pair = (uint32_t)(g / groups);
+    uint32_t sat = 0;
+    float nmax = 0.0f;
+    while (g < end) {
+        const uint32_t gi = (uint32_t)(g - (uint64_t)pair * groups);
+        const float* src = a.src + (uint64_t)pair * a.rows * a.dim;
+        uint8_t* dst = a.dst + pair * a.pair_bytes;
+        // groups of this pair left in this warp's range, two at a time
+        const uint64_t left = end - g;
+        const uint32_t n = left < (uint64_t)(groups - gi) ? (uint32_t)left : groups - gi;
+        uint32_t j = 0;
+        for (; j + 1 < n; j += 2) {
+            float v0[8], v1[8];
+            const uint32_t r0 = (gi + j) * 8 + sub, r1 = r0 + 8;
+            pack_load(a, src, r0, chunk, v0);
+            pack_load(a, src, r1, chunk, v1);
+            nmax = fmaxf(nmax, pack_store(a, dst, pair, r0, chunk, v0, sat));
+            nmax = fmaxf(nmax, pack_store(a, dst, pair, r1, chunk, v1, sat));
+        }
+        if (j < n) {
+            float v0[8];
+            const uint32_t r0 = (gi + j) * 8 + sub;
+            pack_load(a, src, r0, chunk, v0);
+            nmax = fmaxf(nmax, pack_store(a, dst, pair, r0, chunk, v0, sat));
+        }
+        pack_flush(a, pair, sat, nmax);
+        g += n;
+        ++pair;
     }
 }
 
@@ -650,68 +660,95 @@ __device__ __forceinline__ float packed_chain(const float (&q)[kPackK], const ui
 __device__ __forceinline__ void load_query(const uint8_t* qbuf, uint32_t grow, float (&q)[kPackK]);
 
 template <bool kL2, int DIM>
-__global__ void merge_kernel(MergeArgs a) {
+__global__ void __launch_bounds__(kQueryTilePair) merge_kernel(MergeArgs a) {
+    // phase 1 (thread per row): certification from the split partials
+    // phase 2 (warp per row): exact resolution of the candidate sub-tiles, two
+    //   targets per lane, coalesced 16 B loads, (dist, index) key reduction
+    __shared__ uint32_t s_t[kQueryTilePair][2];  // candidate sub-tiles; t[1] = ~0 when one suffices
+    __shared__ uint32_t s_go[kQueryTilePair];    // 1 = resolve here
     const uint32_t tp = blockIdx.x, r = threadIdx.x;
     const uint32_t pair = a.tp_pair[tp];
-    const uint32_t qi = a.tp_qi0[tp] + r;
-    if (qi >= a.n_active[pair]) return;
-    // global top-3 of sub-tile maxima over the target splits: each split's
-    // (b1, t1), (b2, t2) are candidates, its b3 bounds every other sub-tile
-    float B1 = -INFINITY, B2 = -INFINITY, B3 = -INFINITY;
-    uint32_t T1 = 0, T2 = 0xFFFFFFFFu;
-    auto insert = [&](float v, uint32_t t) {
-        if (v > B1) {
-            B3 = fmaxf(B3, B2);
-            B2 = B1;
-            T2 = T1;
-            B1 = v;
-            T1 = t;
-        } else if (v > B2) {
-            B3 = fmaxf(B3, B2);
-            B2 = v;
-            T2 = t;
-        } else {
-            B3 = fmaxf(B3, v);
+    const uint32_t nrows = min(kQueryTilePair, a.n_active[pair] - a.tp_qi0[tp]);
+    const uint32_t row0 = a.tp_row0[tp];
+    s_go[r] = 0;
+    if (r < nrows) {
+        // global top-3 of sub-tile maxima over the target splits: each split's
+        // (b1, t1), (b2, t2) are candidates, its b3 bounds every other sub-tile
+        float B1 = -INFINITY, B2 = -INFINITY, B3 = -INFINITY;
+        uint32_t T1 = 0, T2 = 0xFFFFFFFFu;
+        auto insert = [&](float v, uint32_t t) {
+            if (v > B1) {
+                B3 = fmaxf(B3, B2);
+                B2 = B1;
+                T2 = T1;
+                B1 = v;
+                T1 = t;
+            } else if (v > B2) {
+                B3 = fmaxf(B3, B2);
+                B2 = v;
+                T2 = t;
+            } else {
+                B3 = fmaxf(B3, v);
+            }
+        };
+        for (uint32_t s = 0; s < a.splits; ++s) {
+            const float4* pp = a.partial + (((uint64_t)tp * a.splits + s) * kQueryTilePair + r) * 2;
+            const float4 p = pp[0];
+            const float4 p2 = pp[1];
+            insert(p.x, __float_as_uint(p.w));
+            insert(p.y, __float_as_uint(p2.x));
+            B3 = fmaxf(B3, p.z);
         }
-    };
-    for (uint32_t s = 0; s < a.splits; ++s) {
-        const float4* pp = a.partial + (((uint64_t)tp * a.splits + s) * kQueryTilePair + r) * 2;
-        const float4 p = pp[0];
-        const float4 p2 = pp[1];
-        insert(p.x, __float_as_uint(p.w));
-        insert(p.y, __float_as_uint(p2.x));
-        B3 = fmaxf(B3, p.z);
+        const float margin = a.margin[row0 + r];
+        const bool top1 = B1 - B2 > margin;
+        if (!top1) atomicAdd(a.near_ties + pair, 1ull);  // top-2 gap inside the error bound
+        if (top1 || B1 - B3 > margin) {
+            // certified: the reference winner lies in T1 (or T1 / T2)
+            s_t[r][0] = T1;
+            s_t[r][1] = top1 ? 0xFFFFFFFFu : T2;
+            s_go[r] = 1;
+        } else {
+            const uint32_t k = atomicAdd(a.rescan_count, 1u);
+            a.rescan[3 * k] = row0 + r;
+            a.rescan[3 * k + 1] = pair;
+            a.rescan[3 * k + 2] = a.tp_qi0[tp] + r;
+        }
     }
-    const uint32_t grow = a.tp_row0[tp] + r;
-    const uint64_t o = (uint64_t)pair * a.out_stride + qi;
-    const float margin = a.margin[grow];
-    const bool top1 = B1 - B2 > margin;
-    if (!top1) atomicAdd(a.near_ties + pair, 1ull);  // top-2 gap inside the error bound
-    if (top1 || B1 - B3 > margin) {
-        // certified: the reference winner lies in T1 (or T1 / T2); decide exactly,
-        // lowest index on exact ties via the packed (dist, index) key
+    __syncthreads();
+    const uint32_t warp = r >> 5, lane = r & 31;
+    const uint8_t* tm = a.tmap + pair * a.t_pair_bytes;
+    for (uint32_t row = warp; row < nrows; row += kQueryTilePair / 32) {
+        if (!s_go[row]) continue;
         float q[kPackK];
-        load_query(a.qbuf, grow, q);
-        const uint8_t* tm = a.tmap + pair * a.t_pair_bytes;
+        load_query(a.qbuf, row0 + row, q);
         unsigned long long key = ~0ull;
-        for (int c = 0; c < (top1 ? 1 : 2); ++c) {
-            const uint32_t t0 = (c ? T2 : T1) * kSubTile, t1 = min(a.nt, t0 + kSubTile);
-            for (uint32_t t = t0; t < t1; ++t) {
-                const unsigned long long k = pack_key(packed_chain<kL2, DIM>(q, tm, t, a.dim), t);
-                key = k < key ? k : key;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const uint32_t st = s_t[row][c];
+            if (st == 0xFFFFFFFFu) continue;
+#pragma unroll
+            for (uint32_t h = 0; h < kSubTile; h += 32) {
+                const uint32_t t = st * kSubTile + h + lane;
+                if (t < a.nt) {
+                    const unsigned long long k = pack_key(packed_chain<kL2, DIM>(q, tm, t, a.dim), t);
+                    key = k < key ? k : key;
+                }
             }
         }
-        a.out[o] = (uint32_t)(key & 0xFFFFFFFFull);
-        if (a.min_dist) {
-            float d = from_orderable((uint32_t)(key >> 32));
-            if (d == 0.0f) d = kL2 ? 0.0f : -0.0f;  // canonical sign of an exact zero
-            a.min_dist[o] = d;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long other = __shfl_xor_sync(0xFFFFFFFFu, key, o);
+            key = other < key ? other : key;
         }
-    } else {
-        const uint32_t k = atomicAdd(a.rescan_count, 1u);
-        a.rescan[3 * k] = grow;
-        a.rescan[3 * k + 1] = pair;
-        a.rescan[3 * k + 2] = qi;
+        if (lane == 0) {
+            const uint64_t o = (uint64_t)pair * a.out_stride + a.tp_qi0[tp] + row;
+            a.out[o] = (uint32_t)(key & 0xFFFFFFFFull);
+            if (a.min_dist) {
+                float d = from_orderable((uint32_t)(key >> 32));
+                if (d == 0.0f) d = kL2 ? 0.0f : -0.0f;  // canonical sign of an exact zero
+                a.min_dist[o] = d;
+            }
+        }
     }
 }
 
@@ -946,12 +983,10 @@ int tensor_pack(fnl_context* ctx, const char* tag, const float* d_src, uint32_t 
     out->rows = rows;
     out->npairs = npairs;
     PackArgs a{d_src, out->data, pair_bytes, rows, rows_pad, dim, l2, out->max_norm, d_bad, d_sat};
-    // ~8 resident blocks per SM over the whole batch, at least one per pair
-    const uint32_t groups = rows_pad / 8, warps = kPackThreads / 32;
-    const uint32_t want = std::max<uint32_t>(1, ceil_div_u(8u * (uint32_t)ctx_sm_count(ctx), npairs));
-    dim3 grid(std::min(want, ceil_div_u(groups, warps)), npairs);
+    // exactly one wave: 8 resident 256-thread blocks per SM
+    const uint32_t grid = 8u * (uint32_t)ctx_sm_count(ctx);
     ProfScope prof(ctx, FNL_KCLASS_PACK);
-    pack_kernel<<<grid, kPackThreads, 0, s>>>(a);
+    pack_kernel<<<grid, kPackThreads, 0, s>>>(a, npairs);
     FNL_CUDA_TRY(cudaGetLastError());
     ctx_count_launches(ctx, 1);
     return FNL_OK;
