@@ -157,6 +157,28 @@ int fnl_mutual_nn(fnl_context* ctx, const float* h_d1, uint32_t h1, uint32_t w1,
                   const float* h_d2, uint32_t h2, uint32_t w2, uint32_t dim, int metric,
                   uint32_t* h_pairs, uint32_t* n_pairs);
 
+/* ---- K7 FlashMatch attention (no reference code) --------------
+ * O = softmax(Q K^T * scale) V per (batch, head), non-causal, binary16 Q/K/V/O
+ * (device pointers, 16 B aligned), fp32 scores / softmax statistics /
+ * accumulation on the tcgen05 tensor cores.  head_dim must be 64.  Strides are
+ * in elements (multiples of 8) for [batch][head][token]; head_dim is
+ * contiguous, so e.g. a fused QKV projection [B][N][3][H][64] is read in place
+ * (q/k/v = base + {0,1,2}*H*64, strides {N*3*H*64, 64, 3*H*64}).  Runs on the
+ * context stream; asynchronous. */
+typedef struct fnl_attention_desc {
+    const void* q;
+    const void* k;
+    const void* v;
+    void* o;
+    uint32_t batch, heads, nq, nkv, head_dim;
+    float scale;              /* softmax scale, usually 1/sqrt(head_dim) */
+    uint64_t q_stride[3];     /* batch, head, token */
+    uint64_t k_stride[3];
+    uint64_t v_stride[3];
+    uint64_t o_stride[3];
+} fnl_attention_desc;
+int fnl_flashmatch_fwd(fnl_context* ctx, const fnl_attention_desc* desc);
+
 /* ---- diagnostics -------------------------------------------------------------
  * Raw tensor-core scores (fp32 TMEM accumulators) of 256 query rows against 128
  * target rows after the binary16 pack: h_scores[256][128].  dot: q.t;

@@ -47,6 +47,8 @@ except ImportError as e:  # fail loudly: the product has no Python fallback
         f"paper_2503_10017_b200: compiled extension missing or broken ({e}); "
         "run `python -c 'import __graft_entry__ as g; g.build()'` (or `make`) first") from e
 
+from .flashmatch import flashmatch  # noqa: E402,F401  (K7 attention, torch tensors)
+
 LIBRARY_PATH = _os.path.join(_here, "libfastnn_b200.so")
 
 __all__ = [
@@ -70,6 +72,7 @@ __all__ = [
     "reciprocal_match_device",
     "kernel_timing",
     "kernel_profile",
+    "flashmatch",
     "device_count",
     "set_device",
     "abi_version",

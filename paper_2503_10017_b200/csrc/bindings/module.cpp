@@ -2,6 +2,7 @@
 // bindings/module.cpp:64-260): the same 14 functions, argument names, defaults,
 // dtypes, return shapes and dict keys, plus batch / device-resident entry points
 // and instrumentation.  GPU work runs with the GIL released.
+#include <array>
 #include <pybind11/numpy.h>
 #include <pybind11/pybind11.h>
 #include <pybind11/stl.h>
@@ -419,6 +420,39 @@ PYBIND11_MODULE(_fastnn, m) {
           py::arg("enable") = -1, py::arg("reset") = false,
           "per-kernel-class device time (CUDA events) since the last reset; enable=1/0 turns the "
           "breakdown of the non-score classes on/off");
+
+    m.def("_flashmatch_fwd",
+          [](std::uintptr_t q, std::uintptr_t k, std::uintptr_t v, std::uintptr_t o, std::uint32_t batch,
+             std::uint32_t heads, std::uint32_t nq, std::uint32_t nkv, std::uint32_t head_dim, float scale,
+             std::array<std::uint64_t, 3> qs, std::array<std::uint64_t, 3> ks, std::array<std::uint64_t, 3> vs,
+             std::array<std::uint64_t, 3> os, std::uintptr_t stream) {
+              fnl_context* ctx = fastnn::b200::context();
+              fastnn::b200::check(fnl_context_set_stream(ctx, reinterpret_cast<void*>(stream)));
+              fnl_attention_desc d{};
+              d.q = reinterpret_cast<const void*>(q);
+              d.k = reinterpret_cast<const void*>(k);
+              d.v = reinterpret_cast<const void*>(v);
+              d.o = reinterpret_cast<void*>(o);
+              d.batch = batch;
+              d.heads = heads;
+              d.nq = nq;
+              d.nkv = nkv;
+              d.head_dim = head_dim;
+              d.scale = scale;
+              for (int i = 0; i < 3; ++i) {
+                  d.q_stride[i] = qs[i];
+                  d.k_stride[i] = ks[i];
+                  d.v_stride[i] = vs[i];
+                  d.o_stride[i] = os[i];
+              }
+              const int st = fnl_flashmatch_fwd(ctx, &d);
+              fnl_context_set_stream(ctx, nullptr);
+              fastnn::b200::check(st);
+          },
+          py::arg("q"), py::arg("k"), py::arg("v"), py::arg("o"), py::arg("batch"), py::arg("heads"),
+          py::arg("nq"), py::arg("nkv"), py::arg("head_dim"), py::arg("scale"), py::arg("q_strides"),
+          py::arg("k_strides"), py::arg("v_strides"), py::arg("o_strides"), py::arg("stream") = 0,
+          "K7 FlashMatch attention on raw device pointers (binary16, head_dim 64); see flashmatch.py");
 
     m.def("_tensor_selftest",
           [](const F32& q, const F32& t, const std::string& metric, int mode) {

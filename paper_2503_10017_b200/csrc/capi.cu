@@ -412,6 +412,12 @@ extern "C" int fnl_kernel_profile(fnl_context* ctx, int enable, int reset, doubl
     return FNL_OK;
 }
 
+extern "C" int fnl_flashmatch_fwd(fnl_context* ctx, const fnl_attention_desc* desc) {
+    TRY(check_device(ctx));
+    if (!desc) return fail(FNL_EINVAL, "fnl_flashmatch_fwd: null descriptor");
+    return fnl::flashmatch_forward(ctx, *desc);
+}
+
 // ============================================================== L1 block scorer
 extern "C" int fnl_block_distances(fnl_context* ctx, const float* h_q, uint32_t nq,
                                    const float* h_t, uint32_t nt, uint32_t dim, int metric,

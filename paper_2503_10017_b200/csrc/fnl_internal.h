@@ -44,6 +44,9 @@ struct ProfScope {
     ~ProfScope() { ctx_prof_end(ctx, cls, end); }
 };
 
+// ---------------------------------------------------------------- K7 FlashMatch
+int flashmatch_forward(fnl_context* ctx, const struct fnl_attention_desc& d);
+
 // ---------------------------------------------------------------- K1 prepare
 // Validates finiteness (first offending flat index into *bad_index, which the
 // caller initialises to UINT64_MAX), and for hybrid writes the binary16-rounded

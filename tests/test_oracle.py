@@ -111,3 +111,16 @@ def test_oracle_matches_compiled_reference(orc, ref):
             r2 = json.loads(r2)
             assert r1["active_history"] == r2["active_history"]
             assert (r1["a_block_fetches"], r1["b_block_fetches"]) == (r2["a_block_fetches"], r2["b_block_fetches"])
+
+
+def test_attention_oracle_pinned_by_loop():
+    """The vectorised FlashMatch oracle agrees with its two-pass loop form."""
+    import numpy as np
+    from oracle import attention
+    rng = np.random.default_rng(5)
+    q = rng.standard_normal((7, 64)).astype(np.float16)
+    k = rng.standard_normal((11, 64)).astype(np.float16)
+    v = rng.standard_normal((11, 64)).astype(np.float16)
+    a = attention.attention(q, k, v)
+    b = attention.attention_loop(q.tolist(), k.tolist(), v.tolist())
+    assert np.abs(a - b).max() < 1e-12
