@@ -178,6 +178,9 @@ typedef struct fnl_attention_desc {
     uint64_t o_stride[3];
 } fnl_attention_desc;
 int fnl_flashmatch_fwd(fnl_context* ctx, const fnl_attention_desc* desc);
+/* profiling aid: the 64 clock64 stamps of CTA 0 of the last traced launch
+ * (set FNL_FM_TRACE=1 before the first launch) */
+int fnl_flashmatch_trace(fnl_context* ctx, unsigned long long* stamps64);
 
 /* ---- diagnostics -------------------------------------------------------------
  * Raw tensor-core scores (fp32 TMEM accumulators) of 256 query rows against 128

@@ -454,6 +454,14 @@ PYBIND11_MODULE(_fastnn, m) {
           py::arg("k_strides"), py::arg("v_strides"), py::arg("o_strides"), py::arg("stream") = 0,
           "K7 FlashMatch attention on raw device pointers (binary16, head_dim 64); see flashmatch.py");
 
+    m.def("_flashmatch_trace", []() {
+        std::vector<unsigned long long> v(64);
+        fnl_context* ctx = fastnn::b200::context();
+        fastnn::b200::check(fnl_context_synchronize(ctx));
+        fastnn::b200::check(fnl_flashmatch_trace(ctx, v.data()));
+        return v;
+    });
+
     m.def("_tensor_selftest",
           [](const F32& q, const F32& t, const std::string& metric, int mode) {
               if (q.ndim() != 2 || t.ndim() != 2 || q.shape(0) != 256 || t.shape(0) != 128 || q.shape(1) != t.shape(1))

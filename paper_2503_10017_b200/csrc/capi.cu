@@ -418,6 +418,12 @@ extern "C" int fnl_flashmatch_fwd(fnl_context* ctx, const fnl_attention_desc* de
     return fnl::flashmatch_forward(ctx, *desc);
 }
 
+extern "C" int fnl_flashmatch_trace(fnl_context* ctx, unsigned long long* stamps64) {
+    TRY(check_device(ctx));
+    if (!stamps64) return fail(FNL_EINVAL, "fnl_flashmatch_trace: null output");
+    return fnl::flashmatch_trace(stamps64);
+}
+
 // ============================================================== L1 block scorer
 extern "C" int fnl_block_distances(fnl_context* ctx, const float* h_q, uint32_t nq,
                                    const float* h_t, uint32_t nt, uint32_t dim, int metric,

@@ -6,21 +6,31 @@
 //   binary16 Q/K/V/O, fp32 scores, fp32 softmax statistics, fp32 accumulation
 //   (HybridCast numerics).
 //
-// One CTA = 128 query rows of one (batch, head); 4 warps, thread r owns query
-// row r (= TMEM lane r).  Per 128-key block j:
+// One CTA = 128 query rows of one (batch, head); kColGroups threads per row
+// (warp w reads TMEM lane quadrant w%4, key columns of column group w/4).  Per
+// 128-key block j (software-pipelined: S_{j+1} is issued as soon as S_j is
+// drained and runs under softmax j; PV_j runs under softmax j+1 and its TMEM
+// buffer is drained one block late):
 //   S_j = Q K_j^T        tcgen05.mma kind::f16 M128 N128 K16 x4 (SS) -> TMEM cols [0,128)
-//   softmax              tcgen05.ld of the thread's 128 scores, online max /
+//   softmax              tcgen05.ld of the thread's scores, online max /
 //                        rescale / exp2 / row sum in registers, P_j (binary16)
 //                        st.shared in the UMMA K-major layout
-//   O_j = P_j V_j        tcgen05.mma M128 N64 K16 x8 (SS, V MN-major)  -> TMEM cols [128,192)
+//   O_j = P_j V_j        tcgen05.mma M128 N64 K16 x8 (SS, V MN-major)  -> TMEM cols 128 + 64 (j&1)
 //   o = o * alpha + O_j  (registers; the final 1/l and binary16 cast in the epilogue)
-// K/V blocks are double-buffered with cp.async (zero-filled past the ends), so
-// block j+1 lands while block j is scored; two CTAs share an SM (112 KB smem,
-// 256 TMEM columns each) so one CTA's softmax overlaps the other's MMAs.  The
-// N x N score matrix never leaves the SM.
+// K/V blocks are double-buffered with cp.async (zero-filled past the ends); two
+// CTAs share an SM (112 KB smem, 256 TMEM columns each).  The N x N score
+// matrix never leaves the SM.
+//
+// Measured (tools/fm_trace.py clock stamps): one block
+// costs ~5k SM cycles per CTA pair, of which ~2.2k are the MUFU ex2 phase
+// (16 ex2/clk/SM) and the rest barrier-separated latency phases -- the next
+// step is FA4-style warp specialisation (ping-pong softmax warpgroups) so the
+// latency phases hide under the other tile's exponentials.
 #include <cuda_fp16.h>
 #include <math.h>
 #include <stdint.h>
+
+#include <stdlib.h>
 
 #include <string>
 
@@ -33,14 +43,15 @@ namespace fnl {
 
 namespace {
 
-constexpr uint32_t kFmThreads = 128;
+constexpr uint32_t kColGroups = 1;   // threads per query row (each owns 128/kColGroups key columns)
+constexpr uint32_t kFmThreads = 128 * kColGroups;
 constexpr uint32_t kHd = 64;         // head_dim
 constexpr uint32_t kBlockQ = 128;    // query rows per CTA
 constexpr uint32_t kBlockK = 128;    // keys per block
 constexpr uint32_t kTileQK = kBlockQ * kHd * 2;   // 16 KB (Q, K blocks and V blocks alike)
 constexpr uint32_t kTileP = kBlockQ * kBlockK * 2;  // 32 KB
 constexpr uint32_t kSmemFm = kTileQK /*Q*/ + 2 * kTileQK /*K*/ + 2 * kTileQK /*V*/ + kTileP + 64;
-constexpr uint32_t kTmemCols = 256;  // S [0,128) + O [128,192)
+constexpr uint32_t kTmemCols = 256;  // S [0,128) + O_j double buffer [128,256)
 
 // UMMA shared-memory descriptor, no swizzle, version 1 (sm_100).
 __device__ __forceinline__ uint64_t fm_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -93,6 +104,15 @@ __device__ __forceinline__ float ex2(float x) {
     return y;
 }
 
+// profiling aid: per-phase clock64 stamps of CTA 0, thread 0 (FNL_FM_TRACE=1)
+__device__ unsigned long long g_fm_trace[64];
+#define FM_STAMP(i)                                                         \
+    do {                                                                    \
+        if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && \
+            threadIdx.x == 0 && (i) < 64)                                   \
+            g_fm_trace[(i)] = clock64();                                    \
+    } while (0)
+
 struct FmArgs {
     const __half* q;
     const __half* k;
@@ -105,6 +125,7 @@ struct FmArgs {
     uint64_t v_sb, v_sh, v_sn;
     uint64_t o_sb, o_sh, o_sn;
     float scale_log2;  // softmax scale * log2(e)
+    int trace;
 };
 
 // 128 rows x 64 hd of a [token][hd] operand into smem.  Warp lanes: row%8 and
@@ -114,8 +135,8 @@ template <bool kV>
 __device__ __forceinline__ void load_tile(uint32_t sbase, const __half* g, uint64_t sn, uint32_t nvalid) {
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
 #pragma unroll
-    for (uint32_t j = 0; j < 8; ++j) {
-        const uint32_t combo = warp * 8u + j;
+    for (uint32_t j = 0; j < 1024u / kFmThreads; ++j) {
+        const uint32_t combo = j * (kFmThreads / 32u) + warp;
         const uint32_t chunk = (lane >> 3) + 4u * (combo & 1u);
         const uint32_t row = (combo >> 1) * 8u + (lane & 7u);
         const bool valid = row < nvalid;
@@ -128,8 +149,14 @@ __global__ void __launch_bounds__(kFmThreads, 2) flashmatch_kernel(FmArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint32_t tmem_slot;
     __shared__ __align__(8) uint64_t bar_s, bar_o;
-    const uint32_t tid = threadIdx.x, warp = tid >> 5;
+    __shared__ float red[kColGroups][kBlockQ];  // per-row partials across the column groups
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
+    // warp w reads TMEM lane quadrant w%4 (rows 32*(w%4) + lane), key columns
+    // [32*cg, 32*cg + 32) of S and O columns [16*cg, 16*cg + 16)
+    const uint32_t quad = warp & 3u, cg = warp >> 2;
+    const uint32_t row = quad * 32u + lane;
     const uint32_t q0 = blockIdx.x * kBlockQ, h = blockIdx.y, b = blockIdx.z;
+    FM_STAMP(0);
     const uint32_t sQ = smem_addr(smem);
     const uint32_t sK = sQ + kTileQK, sV = sK + 2 * kTileQK, sP = sV + 2 * kTileQK;
     uint8_t* pP = smem + 5 * kTileQK;
@@ -149,38 +176,38 @@ __global__ void __launch_bounds__(kFmThreads, 2) flashmatch_kernel(FmArgs a) {
     const __half* gk = a.k + b * a.k_sb + h * a.k_sh;
     const __half* gv = a.v + b * a.v_sb + h * a.v_sh;
     const uint32_t nblk = (a.nkv + kBlockK - 1) / kBlockK;
-    // group 0: Q, K_0, V_0; group 1: K_1, V_1
+    auto load_k = [&](uint32_t blk) {
+        if (blk < nblk)
+            load_tile<false>(sK + (blk & 1u) * kTileQK, gk + (uint64_t)blk * kBlockK * a.k_sn, a.k_sn,
+                             a.nkv - blk * kBlockK);
+        cp_async_commit();
+    };
+    auto load_v = [&](uint32_t blk) {
+        if (blk < nblk)
+            load_tile<true>(sV + (blk & 1u) * kTileQK, gv + (uint64_t)blk * kBlockK * a.v_sn, a.v_sn,
+                            a.nkv - blk * kBlockK);
+        cp_async_commit();
+    };
+    // cp.async groups in commit order: {Q, K0, V0}, K1, {}, then per block j:
+    // K_{j+2} (top of j), V_{j+1} (middle of j).  Every wait below is
+    // wait_group 2: it retires exactly the group the next MMA needs.
     load_tile<false>(sQ, gq, a.q_sn, a.nq - q0);
     load_tile<false>(sK, gk, a.k_sn, a.nkv);
     load_tile<true>(sV, gv, a.v_sn, a.nkv);
     cp_async_commit();
-    if (nblk > 1) {
-        load_tile<false>(sK + kTileQK, gk + (uint64_t)kBlockK * a.k_sn, a.k_sn, a.nkv - kBlockK);
-        load_tile<true>(sV + kTileQK, gv + (uint64_t)kBlockK * a.v_sn, a.v_sn, a.nkv - kBlockK);
-    }
+    load_k(1);
     cp_async_commit();
 
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_slot;
-    const uint32_t lane_base = (warp * 32u) << 16;
+    const uint32_t lane_base = (quad * 32u) << 16;
 
-    float o[kHd];
-#pragma unroll
-    for (uint32_t i = 0; i < kHd; ++i) o[i] = 0.0f;
-    float m = -INFINITY, l = 0.0f;
-    const float sl2 = a.scale_log2;
-
-    for (uint32_t j = 0; j < nblk; ++j) {
-        const uint32_t buf = j & 1u;
-        cp_async_wait<1>();  // this thread's copies of block j (and Q) have landed
-        fence_async_smem();  // ... and are visible to the tensor core
-        __syncthreads();
+    auto issue_s = [&](uint32_t kb) {
         if (warp == 0) {
             tc_fence_after();
             if (elect_one()) {
-                const uint32_t kb = sK + buf * kTileQK;
 #pragma unroll
                 for (uint32_t ks = 0; ks < kHd / 16; ++ks)
                     tc_mma_f16(tmem, fm_desc(sQ + ks * 256u, 128u, 1024u), fm_desc(kb + ks * 256u, 128u, 1024u),
@@ -189,98 +216,168 @@ __global__ void __launch_bounds__(kFmThreads, 2) flashmatch_kernel(FmArgs a) {
             }
             __syncwarp();
         }
-        mbar_wait(&bar_s, j & 1u);
-        tc_fence_after();
+    };
+    FM_STAMP(1);
+    cp_async_wait<2>();
+    fence_async_smem();
+    __syncthreads();
+    FM_STAMP(2);
+    issue_s(sK);  // S_0
 
-        // ---- online softmax over this thread's 128 scores
-        Frag f0, f1, f2, f3;
-        frag_ld(tmem + lane_base + 0, f0);
-        frag_ld(tmem + lane_base + 32, f1);
-        frag_ld(tmem + lane_base + 64, f2);
-        frag_ld(tmem + lane_base + 96, f3);
-        frag_wait2(f0, f1);
-        frag_wait2(f2, f3);
-        float s[kBlockK];
+    constexpr uint32_t kSc = kBlockK / kColGroups;  // S columns per thread
+    constexpr uint32_t kOc = kHd / kColGroups;      // O columns per thread
+    float o[kOc];
 #pragma unroll
-        for (uint32_t i = 0; i < 32; ++i) {
-            s[i] = __uint_as_float(f0.r[i]);
-            s[32 + i] = __uint_as_float(f1.r[i]);
-            s[64 + i] = __uint_as_float(f2.r[i]);
-            s[96 + i] = __uint_as_float(f3.r[i]);
+    for (uint32_t i = 0; i < kOc; ++i) o[i] = 0.0f;
+    float m = -INFINITY, l = 0.0f, alpha_prev = 0.0f;
+    const float sl2 = a.scale_log2;
+
+    // o = o * alpha_{j-1} + O_{j-1}  (TMEM buffer (j-1)&1, this thread's 16 columns)
+    auto drain_o = [&](uint32_t jj, float alpha) {
+        const uint32_t ob = tmem + lane_base + 128u + 64u * (jj & 1u) + cg * kOc;
+#pragma unroll
+        for (uint32_t c = 0; c < kOc; c += 16) {
+            uint32_t r[16];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                  "=r"(r[15])
+                : "r"(ob + c));
+            asm volatile("tcgen05.wait::ld.sync.aligned;"
+                         : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]),
+                           "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]),
+                           "+r"(r[14]), "+r"(r[15])
+                         :
+                         : "memory");
+#pragma unroll
+            for (uint32_t i = 0; i < 16; ++i) o[c + i] = fmaf(o[c + i], alpha, __uint_as_float(r[i]));
+        }
+    };
+
+    for (uint32_t j = 0; j < nblk; ++j) {
+        mbar_wait(&bar_s, j & 1u);
+        FM_STAMP(3 + 6 * j);
+        tc_fence_after();
+        float s[kSc];
+#pragma unroll
+        for (uint32_t c = 0; c < kSc; c += 32) {
+            Frag f;
+            frag_ld(tmem + lane_base + cg * kSc + c, f);
+            asm volatile("tcgen05.wait::ld.sync.aligned;"
+                         : "+r"(f.r[0]), "+r"(f.r[1]), "+r"(f.r[2]), "+r"(f.r[3]), "+r"(f.r[4]), "+r"(f.r[5]),
+                           "+r"(f.r[6]), "+r"(f.r[7]), "+r"(f.r[8]), "+r"(f.r[9]), "+r"(f.r[10]), "+r"(f.r[11]),
+                           "+r"(f.r[12]), "+r"(f.r[13]), "+r"(f.r[14]), "+r"(f.r[15]), "+r"(f.r[16]), "+r"(f.r[17]),
+                           "+r"(f.r[18]), "+r"(f.r[19]), "+r"(f.r[20]), "+r"(f.r[21]), "+r"(f.r[22]), "+r"(f.r[23]),
+                           "+r"(f.r[24]), "+r"(f.r[25]), "+r"(f.r[26]), "+r"(f.r[27]), "+r"(f.r[28]), "+r"(f.r[29]),
+                           "+r"(f.r[30]), "+r"(f.r[31])
+                         :
+                         : "memory");
+#pragma unroll
+            for (uint32_t i = 0; i < 32; ++i) s[c + i] = __uint_as_float(f.r[i]);
         }
         const uint32_t kvalid = a.nkv - j * kBlockK;
         if (kvalid < kBlockK) {
 #pragma unroll
-            for (uint32_t i = 0; i < kBlockK; ++i)
-                if (i >= kvalid) s[i] = -INFINITY;
+            for (uint32_t i = 0; i < kSc; ++i)
+                if (cg * kSc + i >= kvalid) s[i] = -INFINITY;
         }
-        float mx = -INFINITY;
+        {   // partial row max: four independent 3-input chains
+            float r4[4] = {s[0], s[1], s[2], s[3]};
 #pragma unroll
-        for (uint32_t i = 0; i < kBlockK; i += 2) mx = max3(mx, s[i], s[i + 1]);
+            for (uint32_t i = 4; i < kSc; i += 8) {
+#pragma unroll
+                for (uint32_t u = 0; u < 4; ++u) r4[u] = max3(r4[u], s[i + 2 * u], s[i + 2 * u + 1]);
+            }
+            red[cg][row] = fmaxf(fmaxf(r4[0], r4[1]), fmaxf(r4[2], r4[3]));
+        }
+        load_k(j + 2);       // K buffer j&1 is free (S_j retired)
+        cp_async_wait<2>();  // K_{j+1} landed
+        fence_async_smem();
+        tc_fence_before();
+        FM_STAMP(4 + 6 * j);
+        __syncthreads();     // [A] S_j drained by every thread, partial maxima posted
+        FM_STAMP(5 + 6 * j);
+        if (j + 1 < nblk) issue_s(sK + ((j + 1) & 1u) * kTileQK);  // runs under this softmax
+        if ((a.trace & 2) && j + 1 < nblk && tid == 0) {  // profiling: S MMA latency in isolation
+            mbar_wait(&bar_s, (j + 1) & 1u);
+            FM_STAMP(40 + 2 * j);
+        }
+
+        float mx = red[0][row];
+#pragma unroll
+        for (uint32_t g = 1; g < kColGroups; ++g) mx = fmaxf(mx, red[g][row]);
         const float m_new = fmaxf(m, mx * sl2);
         const float alpha = ex2(m - m_new);
-        float sum = 0.0f;
+        // PV_{j-1} must have retired before P is overwritten
+        if (j > 0) {
+            mbar_wait(&bar_o, (j - 1) & 1u);
+            tc_fence_after();
+        }
+        FM_STAMP(6 + 6 * j);
+        float acc[kSc / 8];
 #pragma unroll
-        for (uint32_t c = 0; c < kBlockK / 8; ++c) {
+        for (uint32_t c = 0; c < kSc / 8; ++c) {
             float p[8];
 #pragma unroll
-            for (uint32_t i = 0; i < 8; ++i) {
-                p[i] = ex2(fmaf(s[c * 8 + i], sl2, -m_new));
-                sum += p[i];
-            }
+            for (uint32_t i = 0; i < 8; ++i) p[i] = ex2(fmaf(s[c * 8 + i], sl2, -m_new));
+            acc[c] = ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
             uint4 w;
             w.x = pack_half2_rn(p[0], p[1]);
             w.y = pack_half2_rn(p[2], p[3]);
             w.z = pack_half2_rn(p[4], p[5]);
             w.w = pack_half2_rn(p[6], p[7]);
-            *reinterpret_cast<uint4*>(pP + off_p(tid, c)) = w;
+            *reinterpret_cast<uint4*>(pP + off_p(row, cg * (kSc / 8) + c)) = w;
         }
-        l = l * alpha + sum;
+#pragma unroll
+        for (uint32_t w = kSc / 16; w > 0; w >>= 1)
+#pragma unroll
+            for (uint32_t c = 0; c < w; ++c) acc[c] += acc[c + w];
+        l = l * alpha + acc[0];  // this thread's partial row sum
         m = m_new;
-        tc_fence_before();
+        if (j > 0) drain_o(j - 1, alpha_prev);  // V buffer (j-1)&1 free too
+        alpha_prev = alpha;
+        load_v(j + 1);
+        FM_STAMP(7 + 6 * j);
+        cp_async_wait<2>();  // V_j landed
         fence_async_smem();
-        __syncthreads();  // P complete; every thread has drained S
+        tc_fence_before();
+        __syncthreads();     // [B] P_j complete, O_{j-1} drained, maxima read
+        FM_STAMP(8 + 6 * j);
         if (warp == 0) {
             tc_fence_after();
             if (elect_one()) {
-                const uint32_t vb = sV + buf * kTileQK;
+                const uint32_t vb = sV + (j & 1u) * kTileQK;
 #pragma unroll
                 for (uint32_t ks = 0; ks < kBlockK / 16; ++ks)
-                    tc_mma_f16(tmem + 128u, fm_desc(sP + ks * 256u, 128u, 2048u), fm_desc(vb + ks * 256u, 128u, 2048u),
-                               kIdescPV, ks > 0 ? 1u : 0u);
+                    tc_mma_f16(tmem + 128u + 64u * (j & 1u), fm_desc(sP + ks * 256u, 128u, 2048u),
+                               fm_desc(vb + ks * 256u, 128u, 2048u), kIdescPV, ks > 0 ? 1u : 0u);
                 tc_commit(&bar_o);
             }
             __syncwarp();
         }
-        mbar_wait(&bar_o, j & 1u);
-        tc_fence_after();
-        Frag g0, g1;
-        frag_ld(tmem + lane_base + 128u, g0);
-        frag_ld(tmem + lane_base + 160u, g1);
-        frag_wait2(g0, g1);
-#pragma unroll
-        for (uint32_t i = 0; i < 32; ++i) {
-            o[i] = fmaf(o[i], alpha, __uint_as_float(g0.r[i]));
-            o[32 + i] = fmaf(o[32 + i], alpha, __uint_as_float(g1.r[i]));
+        if ((a.trace & 2) && tid == 0) {  // profiling: PV MMA latency in isolation
+            mbar_wait(&bar_o, j & 1u);
+            FM_STAMP(41 + 2 * j);
         }
-        tc_fence_before();
-        // K/V buffer `buf` is free (its MMAs retired): prefetch block j+2 into it
-        if (j + 2 < nblk) {
-            load_tile<false>(sK + buf * kTileQK, gk + (uint64_t)(j + 2) * kBlockK * a.k_sn, a.k_sn,
-                             a.nkv - (j + 2) * kBlockK);
-            load_tile<true>(sV + buf * kTileQK, gv + (uint64_t)(j + 2) * kBlockK * a.v_sn, a.v_sn,
-                            a.nkv - (j + 2) * kBlockK);
-        }
-        cp_async_commit();
     }
+    mbar_wait(&bar_o, (nblk - 1) & 1u);
+    tc_fence_after();
+    drain_o(nblk - 1, alpha_prev);
 
-    // ---- epilogue: normalise, binary16, one 128 B row per thread
-    const uint32_t row = q0 + tid;
-    if (row < a.nq) {
-        const float inv = 1.0f / l;
-        __half* go = a.o + b * a.o_sb + h * a.o_sh + (uint64_t)row * a.o_sn;
+    FM_STAMP(62);
+    // ---- epilogue: full row sum, normalise, binary16; 32 B of the row per thread
+    red[cg][row] = l;
+    __syncthreads();
+    float lsum = red[0][row];
 #pragma unroll
-        for (uint32_t c = 0; c < kHd / 8; ++c) {
+    for (uint32_t g = 1; g < kColGroups; ++g) lsum += red[g][row];
+    const uint32_t grow = q0 + row;
+    if (grow < a.nq) {
+        const float inv = 1.0f / lsum;
+        __half* go = a.o + b * a.o_sb + h * a.o_sh + (uint64_t)grow * a.o_sn + cg * kOc;
+#pragma unroll
+        for (uint32_t c = 0; c < kOc / 8; ++c) {
             uint4 w;
             w.x = pack_half2_rn(o[c * 8 + 0] * inv, o[c * 8 + 1] * inv);
             w.y = pack_half2_rn(o[c * 8 + 2] * inv, o[c * 8 + 3] * inv);
@@ -289,6 +386,7 @@ __global__ void __launch_bounds__(kFmThreads, 2) flashmatch_kernel(FmArgs a) {
             *reinterpret_cast<uint4*>(go + c * 8) = w;
         }
     }
+    FM_STAMP(63);
     tc_fence_before();
     __syncthreads();
     if (warp == 0) {
@@ -332,12 +430,19 @@ int flashmatch_forward(fnl_context* ctx, const fnl_attention_desc& d) {
     a.v_sb = d.v_stride[0]; a.v_sh = d.v_stride[1]; a.v_sn = d.v_stride[2];
     a.o_sb = d.o_stride[0]; a.o_sh = d.o_stride[1]; a.o_sn = d.o_stride[2];
     a.scale_log2 = d.scale * 1.4426950408889634f;
+    static const int trace = getenv("FNL_FM_TRACE") ? atoi(getenv("FNL_FM_TRACE")) : 0;
+    a.trace = trace;
     dim3 grid((d.nq + kBlockQ - 1) / kBlockQ, d.heads, d.batch);
     cudaStream_t s = ctx_stream(ctx);
     ProfScope prof(ctx, FNL_KCLASS_ATTN);
     flashmatch_kernel<<<grid, kFmThreads, kSmemFm, s>>>(a);
     FNL_CUDA_TRY(cudaGetLastError());
     ctx_count_launches(ctx, 1);
+    return FNL_OK;
+}
+
+int flashmatch_trace(unsigned long long* host64) {
+    FNL_CUDA_TRY(cudaMemcpyFromSymbol(host64, g_fm_trace, sizeof(g_fm_trace)));
     return FNL_OK;
 }
 

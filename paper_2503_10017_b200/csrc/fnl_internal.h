@@ -46,6 +46,7 @@ struct ProfScope {
 
 // ---------------------------------------------------------------- K7 FlashMatch
 int flashmatch_forward(fnl_context* ctx, const struct fnl_attention_desc& d);
+int flashmatch_trace(unsigned long long* host64);  // profiling aid (FNL_FM_TRACE=1)
 
 // ---------------------------------------------------------------- K1 prepare
 // Validates finiteness (first offending flat index into *bad_index, which the

@@ -1,0 +1,10 @@
+import os, sys, torch
+sys.path.insert(0, '/root/repo')
+import paper_2503_10017_b200 as fnl
+from paper_2503_10017_b200 import _fastnn
+q = torch.randn((2,16,768,64), device='cuda').half(); k = torch.randn_like(q); v = torch.randn_like(q)
+for _ in range(3): fnl.flashmatch(q,k,v)
+torch.cuda.synchronize()
+t = _fastnn._flashmatch_trace()
+t0 = t[0]
+print([ (i, t[i]-t0) for i in range(64) if t[i] >= t0])
