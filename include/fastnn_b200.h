@@ -157,6 +157,35 @@ int fnl_mutual_nn(fnl_context* ctx, const float* h_d1, uint32_t h1, uint32_t w1,
                   const float* h_d2, uint32_t h2, uint32_t w2, uint32_t dim, int metric,
                   uint32_t* h_pairs, uint32_t* n_pairs);
 
+/* ---- target-sharded matching (config C5: one oversized pair over N GPUs) -----
+ * Every process holds both maps; for each NN pass, shard `rank` of `count`
+ * scans only its contiguous range of 128-target tiles of the target map (image
+ * B's pixels in the forward pass, image A's in the reverse pass) and writes
+ * each query's exact winner in that range as a signed 64-bit key
+ *   ((orderable(dist) << 32) | index) ^ 2^63     (INT64_MAX = no candidate)
+ * into the caller-owned device buffer d_keys[pair * samples + i].  The
+ * library then calls reduce(user, d_keys, n, stream): the caller must perform
+ * an in-place MIN all-reduce of d_keys[0, n) over the `count` processes,
+ * ordered on `stream` (e.g. torch.distributed.all_reduce(op=MIN) on NCCL).
+ * The reduced key is the global reference winner (lowest index on exact
+ * ties), so every process continues with identical state and the MatchSet is
+ * bit-identical to the unsharded run.  Tensor backend only.  Replaces nothing
+ * in the reference (it has no distributed code); the entry point mirrors
+ * fnl_reciprocal_match_batch_device. */
+typedef int (*fnl_key_reduce_fn)(void* user, int64_t* d_keys, uint64_t count, void* stream);
+typedef struct fnl_shard_spec {
+    uint32_t rank, count;
+    int64_t* d_keys;          /* device, >= npairs * samples entries */
+    uint64_t keys_capacity;
+    fnl_key_reduce_fn reduce; /* returns 0 on success */
+    void* user;
+} fnl_shard_spec;
+int fnl_reciprocal_match_sharded_device(fnl_context* ctx, uint32_t npairs, const float* d_d1,
+                                        const float* d_d2, uint32_t h, uint32_t w, uint32_t dim,
+                                        const fnl_match_config* cfg, int backend,
+                                        const fnl_shard_spec* shard, uint32_t* d_pairs,
+                                        uint32_t* d_n_pairs, fnl_run_stats* h_stats);
+
 /* ---- K7 FlashMatch attention (no reference code) --------------
  * O = softmax(Q K^T * scale) V per (batch, head), non-causal, binary16 Q/K/V/O
  * (device pointers, 16 B aligned), fp32 scores / softmax statistics /

@@ -113,6 +113,16 @@ void check_shape3(const F32& a, const char* who) {
 
 }  // namespace
 
+// `stream` arguments: None = the library's own stream; otherwise a CUDA
+// stream handle as torch reports it (torch.cuda.Stream.cuda_stream), where 0
+// is the legacy default stream (cudaStreamLegacy == (cudaStream_t)0x1), not
+// "no stream" -- so work is ordered with torch's current stream.
+static void* stream_handle(const py::object& s) {
+    if (s.is_none()) return nullptr;
+    const auto h = s.cast<std::uintptr_t>();
+    return h == 0 ? reinterpret_cast<void*>(std::uintptr_t(1)) : reinterpret_cast<void*>(h);
+}
+
 PYBIND11_MODULE(_fastnn, m) {
     m.doc() = "B200-native fast reciprocal nearest-neighbour matching (FastNN-Lite / HybridCast)";
 
@@ -360,7 +370,8 @@ PYBIND11_MODULE(_fastnn, m) {
              std::uint32_t d, std::uintptr_t out_pairs, std::uintptr_t out_counts,
              const std::string& backend, std::uint32_t k, std::uint32_t stride, std::uint32_t max_iters,
              double convergence, const std::string& metric, const std::string& precision,
-             std::uint32_t block_size, std::uintptr_t stream) {
+             std::uint32_t block_size, py::object stream) {
+              void* const sh = stream_handle(stream);  // with the GIL held
               const auto cfg = make_cfg(k, stride, max_iters, convergence, metric, precision, block_size);
               cfg.validate();
               const auto cc = c_cfg(cfg);
@@ -369,7 +380,7 @@ PYBIND11_MODULE(_fastnn, m) {
               {
                   py::gil_scoped_release nogil;
                   fnl_context* ctx = fastnn::b200::context();
-                  fastnn::b200::check(fnl_context_set_stream(ctx, reinterpret_cast<void*>(stream)));
+                  fastnn::b200::check(fnl_context_set_stream(ctx, sh));
                   const int rc = fnl_reciprocal_match_batch_device(
                       ctx, n, reinterpret_cast<const float*>(d1), reinterpret_cast<const float*>(d2), h, w, d,
                       &cc, be, reinterpret_cast<std::uint32_t*>(out_pairs),
@@ -385,7 +396,68 @@ PYBIND11_MODULE(_fastnn, m) {
           py::arg("dim"), py::arg("out_pairs"), py::arg("out_counts"), py::arg("backend") = "tensor",
           py::arg("k") = 0, py::arg("stride") = 8, py::arg("max_iters") = 10,
           py::arg("convergence") = 0.99, py::arg("metric") = "dot", py::arg("precision") = "full",
-          py::arg("block_size") = 4096, py::arg("stream") = 0);
+          py::arg("block_size") = 4096, py::arg("stream") = py::none());
+
+    // Target-sharded matcher (config C5).  `reduce(count)` must MIN-all-reduce
+    // the first `count` int64 entries of the caller's key buffer (`keys`, a
+    // device pointer with `keys_capacity` entries) across the shards, on the
+    // current stream -- e.g. torch.distributed.all_reduce(keys[:count], MIN).
+    m.def("reciprocal_match_sharded_device",
+          [](std::uintptr_t d1, std::uintptr_t d2, std::uint32_t n, std::uint32_t h, std::uint32_t w,
+             std::uint32_t d, std::uintptr_t out_pairs, std::uintptr_t out_counts, std::uintptr_t keys,
+             std::uint64_t keys_capacity, std::uint32_t rank, std::uint32_t count, py::function reduce,
+             const std::string& backend, std::uint32_t k, std::uint32_t stride, std::uint32_t max_iters,
+             double convergence, const std::string& metric, std::uint32_t block_size, py::object stream) {
+              void* const sh = stream_handle(stream);  // with the GIL held
+              const auto cfg = make_cfg(k, stride, max_iters, convergence, metric, "full", block_size);
+              cfg.validate();
+              const auto cc = c_cfg(cfg);
+              const int be = c_backend(fastnn::backend_from_string(backend));
+              std::vector<fnl_run_stats> st(n);
+              struct Ctx {
+                  py::function fn;
+                  std::string err;
+              } cb{reduce, {}};
+              fnl_shard_spec spec{};
+              spec.rank = rank;
+              spec.count = count;
+              spec.d_keys = reinterpret_cast<std::int64_t*>(keys);
+              spec.keys_capacity = keys_capacity;
+              spec.user = &cb;
+              spec.reduce = [](void* user, std::int64_t*, std::uint64_t cnt, void*) -> int {
+                  auto* c = static_cast<Ctx*>(user);
+                  py::gil_scoped_acquire gil;
+                  try {
+                      c->fn(cnt);
+                      return 0;
+                  } catch (const std::exception& e) {
+                      c->err = e.what();
+                      return 1;
+                  }
+              };
+              int rc;
+              {
+                  py::gil_scoped_release nogil;
+                  fnl_context* ctx = fastnn::b200::context();
+                  fastnn::b200::check(fnl_context_set_stream(ctx, sh));
+                  rc = fnl_reciprocal_match_sharded_device(
+                      ctx, n, reinterpret_cast<const float*>(d1), reinterpret_cast<const float*>(d2), h, w, d,
+                      &cc, be, &spec, reinterpret_cast<std::uint32_t*>(out_pairs),
+                      reinterpret_cast<std::uint32_t*>(out_counts), st.data());
+                  fnl_context_set_stream(ctx, nullptr);
+              }
+              if (rc != FNL_OK && !cb.err.empty()) throw std::runtime_error("shard reduce callback: " + cb.err);
+              fastnn::b200::check(rc);
+              py::list stats;
+              for (const auto& s : st) stats.append(stats_dict(s));
+              return stats;
+          },
+          py::arg("d1"), py::arg("d2"), py::arg("npairs"), py::arg("height"), py::arg("width"),
+          py::arg("dim"), py::arg("out_pairs"), py::arg("out_counts"), py::arg("keys"),
+          py::arg("keys_capacity"), py::arg("shard_rank"), py::arg("shard_count"), py::arg("reduce"),
+          py::arg("backend") = "tensor", py::arg("k") = 0, py::arg("stride") = 8, py::arg("max_iters") = 10,
+          py::arg("convergence") = 0.99, py::arg("metric") = "dot", py::arg("block_size") = 4096,
+          py::arg("stream") = py::none());
 
     m.def("kernel_timing",
           [](bool reset) {
@@ -425,9 +497,10 @@ PYBIND11_MODULE(_fastnn, m) {
           [](std::uintptr_t q, std::uintptr_t k, std::uintptr_t v, std::uintptr_t o, std::uint32_t batch,
              std::uint32_t heads, std::uint32_t nq, std::uint32_t nkv, std::uint32_t head_dim, float scale,
              std::array<std::uint64_t, 3> qs, std::array<std::uint64_t, 3> ks, std::array<std::uint64_t, 3> vs,
-             std::array<std::uint64_t, 3> os, std::uintptr_t stream) {
+             std::array<std::uint64_t, 3> os, py::object stream) {
               fnl_context* ctx = fastnn::b200::context();
-              fastnn::b200::check(fnl_context_set_stream(ctx, reinterpret_cast<void*>(stream)));
+              void* const sh = stream_handle(stream);
+              fastnn::b200::check(fnl_context_set_stream(ctx, sh));
               fnl_attention_desc d{};
               d.q = reinterpret_cast<const void*>(q);
               d.k = reinterpret_cast<const void*>(k);
@@ -451,7 +524,7 @@ PYBIND11_MODULE(_fastnn, m) {
           },
           py::arg("q"), py::arg("k"), py::arg("v"), py::arg("o"), py::arg("batch"), py::arg("heads"),
           py::arg("nq"), py::arg("nkv"), py::arg("head_dim"), py::arg("scale"), py::arg("q_strides"),
-          py::arg("k_strides"), py::arg("v_strides"), py::arg("o_strides"), py::arg("stream") = 0,
+          py::arg("k_strides"), py::arg("v_strides"), py::arg("o_strides"), py::arg("stream") = py::none(),
           "K7 FlashMatch attention on raw device pointers (binary16, head_dim 64); see flashmatch.py");
 
     m.def("_flashmatch_trace", []() {

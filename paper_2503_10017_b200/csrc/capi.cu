@@ -586,7 +586,8 @@ int check_cfg(const fnl_match_config* cfg) {
 int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1, uint32_t w1,
               const float* d_d2, uint32_t h2, uint32_t w2, uint32_t dim,
               const fnl_match_config* cfg, int backend, uint32_t* d_pairs_out,
-              uint32_t* d_npairs_out, fnl_run_stats* h_stats, bool validate) {
+              uint32_t* d_npairs_out, fnl_run_stats* h_stats, bool validate,
+              const fnl_shard_spec* shard = nullptr) {
     TRY(check_cfg(cfg));
     if (!valid_backend(backend)) return fail(FNL_EINVAL, "reciprocal_match: unknown backend");
     if (dim == 0 || h1 == 0 || w1 == 0 || h2 == 0 || w2 == 0)
@@ -640,6 +641,15 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
 
     // ---- K1: validate + (hybrid) round, or binary16 pack for the tensor path
     const bool tensor = backend == FNL_BACKEND_TENSOR;
+    const bool sharded = shard && shard->count > 1;
+    if (shard) {
+        if (!tensor) return fail(FNL_EINVAL, "sharded reciprocal_match: tensor backend only");
+        if (shard->count == 0 || shard->rank >= shard->count)
+            return fail(FNL_EINVAL, "sharded reciprocal_match: rank must be < count");
+        if (sharded && (!shard->d_keys || !shard->reduce || shard->keys_capacity < (uint64_t)npairs * cap))
+            return fail(FNL_EINVAL, "sharded reciprocal_match: key buffer (npairs * samples) and reduce callback "
+                                    "required");
+    }
     Prepared P1, P2;
     fnl::PackedMaps T1, T2;
     unsigned long long *near_ties = nullptr, *tsat = nullptr;
@@ -695,8 +705,23 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
             const fnl::PackedMaps& TQ = (qrows == p1 && ids == m.active_u) ? T1 : T2;
             const fnl::PackedMaps& TT = (qrows == p1 && ids == m.active_u) ? T2 : T1;
             ++call;
-            return fnl::tensor_nn_pass(ctx, npairs, TQ, ids, cap, h_active.data(), h_done.data(), TT, dim,
-                                       l2, out, cap, nullptr, near_ties);
+            if (!sharded)
+                return fnl::tensor_nn_pass(ctx, npairs, TQ, ids, cap, h_active.data(), h_done.data(), TT, dim,
+                                           l2, out, cap, nullptr, near_ties);
+            // target shard of this rank: contiguous 128-target tiles
+            const uint64_t tiles = ceil_div(nt, fnl::kTargetTileRows);
+            const uint32_t tb = (uint32_t)(tiles * shard->rank / shard->count);
+            const uint32_t te = (uint32_t)(tiles * (shard->rank + 1) / shard->count);
+            const uint64_t nkeys = (uint64_t)npairs * cap;
+            TRY(fnl::tensor_shard_reset(ctx, reinterpret_cast<long long*>(shard->d_keys), nkeys));
+            if (te > tb)
+                TRY(fnl::tensor_nn_pass(ctx, npairs, TQ, ids, cap, h_active.data(), h_done.data(), TT, dim, l2,
+                                        out, cap, nullptr, near_ties, tb, te,
+                                        reinterpret_cast<long long*>(shard->d_keys)));
+            if (shard->reduce(shard->user, shard->d_keys, nkeys, ctx->stream) != 0)
+                return fail(FNL_ERUNTIME, "sharded reciprocal_match: key reduction callback failed");
+            return fnl::tensor_shard_finalize(ctx, npairs, reinterpret_cast<const long long*>(shard->d_keys), cap,
+                                              m.n_active, m.done, out);
         }
         fnl::ScanArgs sa{};
         sa.qmap = Q.data;
@@ -871,6 +896,18 @@ extern "C" int fnl_reciprocal_match_batch_device(fnl_context* ctx, uint32_t npai
     if (npairs == 0) return FNL_OK;
     return run_match(ctx, npairs, d_d1, h, w, d_d2, h, w, dim, cfg, backend, d_pairs, d_n_pairs,
                      h_stats, false);
+}
+
+extern "C" int fnl_reciprocal_match_sharded_device(fnl_context* ctx, uint32_t npairs, const float* d_d1,
+                                                   const float* d_d2, uint32_t h, uint32_t w, uint32_t dim,
+                                                   const fnl_match_config* cfg, int backend,
+                                                   const fnl_shard_spec* shard, uint32_t* d_pairs,
+                                                   uint32_t* d_n_pairs, fnl_run_stats* h_stats) {
+    TRY(check_device(ctx));
+    if (!shard) return fail(FNL_EINVAL, "fnl_reciprocal_match_sharded_device: null shard spec");
+    if (npairs == 0) return FNL_OK;
+    return run_match(ctx, npairs, d_d1, h, w, d_d2, h, w, dim, cfg, backend, d_pairs, d_n_pairs, h_stats, false,
+                     shard);
 }
 
 extern "C" int fnl_reciprocal_match_batch(fnl_context* ctx, uint32_t npairs, const float* h_d1,

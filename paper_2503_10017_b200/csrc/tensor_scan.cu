@@ -555,6 +555,7 @@ struct MergeArgs {
     uint32_t* rescan;           // (gathered row, pair, qi) triples
     unsigned int* rescan_count;
     unsigned long long* near_ties;  // per pair
+    long long* shard_keys;      // sharded mode: signed winner keys instead of out/min_dist
 };
 
 template <bool kL2, int DIM>
@@ -645,6 +646,10 @@ __global__ void __launch_bounds__(kQueryTilePair) merge_kernel(MergeArgs a) {
         }
         if (lane == 0) {
             const uint64_t o = (uint64_t)pair * a.out_stride + a.tp_qi0[tp] + row;
+            if (a.shard_keys) {
+                a.shard_keys[o] = (long long)(key ^ 0x8000000000000000ull);
+                continue;
+            }
             a.out[o] = (uint32_t)(key & 0xFFFFFFFFull);
             if (a.min_dist) {
                 float d = from_orderable((uint32_t)(key >> 32));
@@ -706,7 +711,7 @@ struct RescanArgs {
     const uint8_t* qbuf;
     const uint8_t* tmap;
     uint64_t t_pair_bytes;
-    uint32_t nt;
+    uint32_t t_begin, nt;           // scanned target range [t_begin, nt)
     uint32_t dim;
     uint32_t chunk;                 // targets per work unit
     unsigned long long* keys;       // per rescan entry
@@ -718,7 +723,7 @@ constexpr int kRescanThreads = 256;
 template <bool kL2, int DIM>
 __global__ void __launch_bounds__(kRescanThreads) rescan_kernel(RescanArgs a) {
     const uint32_t count = *a.rescan_count;
-    const uint32_t nchunks = (a.nt + a.chunk - 1) / a.chunk;
+    const uint32_t nchunks = (a.nt - a.t_begin + a.chunk - 1) / a.chunk;
     __shared__ unsigned long long red[kRescanThreads / 32];
     float q[kPackK];
     for (uint32_t unit = blockIdx.x; unit < count * nchunks; unit += gridDim.x) {
@@ -726,7 +731,7 @@ __global__ void __launch_bounds__(kRescanThreads) rescan_kernel(RescanArgs a) {
         const uint32_t grow = a.rescan[3 * k], pair = a.rescan[3 * k + 1];
         load_query(a.qbuf, grow, q);
         const uint8_t* tm = a.tmap + pair * a.t_pair_bytes;
-        const uint32_t t0 = ch * a.chunk, t1 = min(a.nt, t0 + a.chunk);
+        const uint32_t t0 = a.t_begin + ch * a.chunk, t1 = min(a.nt, t0 + a.chunk);
         unsigned long long key = ~0ull;
         for (uint32_t t = t0 + threadIdx.x; t < t1; t += kRescanThreads)
             key = umin64(key, (unsigned long long)pack_key(packed_chain<kL2, DIM>(q, tm, t, a.dim), t));
@@ -745,11 +750,16 @@ __global__ void __launch_bounds__(kRescanThreads) rescan_kernel(RescanArgs a) {
 
 __global__ void rescan_finish_kernel(const uint32_t* rescan, const unsigned int* count,
                                      unsigned long long* keys, uint32_t* out, float* min_dist,
-                                     uint32_t out_stride, bool dot) {
+                                     uint32_t out_stride, bool dot, long long* shard_keys) {
     const uint32_t n = *count;
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
         const uint64_t o = (uint64_t)rescan[3 * k + 1] * out_stride + rescan[3 * k + 2];
         const unsigned long long key = keys[k];
+        if (shard_keys) {
+            shard_keys[o] = (long long)(key ^ 0x8000000000000000ull);
+            keys[k] = ~0ull;
+            continue;
+        }
         out[o] = (uint32_t)(key & 0xFFFFFFFFull);
         if (min_dist) {
             float d = from_orderable((uint32_t)(key >> 32));
@@ -758,6 +768,22 @@ __global__ void rescan_finish_kernel(const uint32_t* rescan, const unsigned int*
         }
         keys[k] = ~0ull;
     }
+}
+
+__global__ void shard_finalize_kernel(const long long* keys, uint32_t stride, const uint32_t* n_active,
+                                      const uint8_t* done, uint32_t* out) {
+    const uint32_t p = blockIdx.y;
+    if (done && done[p]) return;
+    const uint32_t n = n_active[p];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint64_t o = (uint64_t)p * stride + i;
+        out[o] = (uint32_t)(((unsigned long long)keys[o] ^ 0x8000000000000000ull) & 0xFFFFFFFFull);
+    }
+}
+
+__global__ void shard_reset_kernel(long long* keys, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        keys[i] = kShardKeyNone;
 }
 
 // Raw scores of one tile pair x one target tile (UMMA layout self-test).
@@ -897,11 +923,15 @@ int tensor_pack(fnl_context* ctx, const char* tag, const float* d_src, uint32_t 
 
 int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const uint32_t* ids, uint32_t cap,
                    const uint32_t* h_active, const uint8_t* h_done, const PackedMaps& T, uint32_t dim, bool l2,
-                   uint32_t* out, uint32_t out_stride, float* min_dist, unsigned long long* d_near_ties) {
+                   uint32_t* out, uint32_t out_stride, float* min_dist, unsigned long long* d_near_ties,
+                   uint32_t tile_begin, uint32_t tile_end, long long* shard_keys) {
     TRY(ensure_attrs());
     cudaStream_t s = ctx_stream(ctx);
     const uint32_t nt = T.rows;
-    const uint32_t ntiles = ceil_div_u(nt, kBTileRows);
+    const uint32_t all_tiles = ceil_div_u(nt, kBTileRows);
+    if (tile_end == 0 || tile_end > all_tiles) tile_end = all_tiles;
+    if (tile_begin >= tile_end) return fail(FNL_EINVAL, "tensor_nn_pass: empty target tile range");
+    const uint32_t ntiles = tile_end - tile_begin;  // tiles of this shard
 
     // ---- host work list: gather slots (one per active pair) and tile pairs
     std::vector<uint32_t> slot_pair, slot_base, tp_pair, tp_row0, tp_qi0;
@@ -939,7 +969,7 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     items.reserve((size_t)ntp * splits);
     for (uint32_t j = 0; j < ntp; ++j)
         for (uint32_t sp = 0; sp < splits; ++sp)
-            items.push_back({tp_pair[j], tp_row0[j], sp * per, std::min(ntiles, (sp + 1) * per),
+            items.push_back({tp_pair[j], tp_row0[j], tile_begin + sp * per, tile_begin + std::min(ntiles, (sp + 1) * per),
                              std::min<uint32_t>(kQueryTilePair, h_active[tp_pair[j]] - tp_qi0[j]), 0, 0, 0});
     const uint32_t nitems = (uint32_t)items.size();
     const uint32_t nslots = (uint32_t)slot_pair.size();
@@ -1023,7 +1053,7 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     // ---- K3b merge + certification
     {
         MergeArgs m{partial, d_tp_pair, d_tp_row0, d_tp_qi0, splits, d_active, margin, qbuf, T.data,
-                    T.pair_bytes, nt, dim, out, min_dist, out_stride, rescan, rcount, d_near_ties};
+                    T.pair_bytes, nt, dim, out, min_dist, out_stride, rescan, rcount, d_near_ties, shard_keys};
         ProfScope prof(ctx, FNL_KCLASS_MERGE);
         if (dim == 24) {
             if (l2) merge_kernel<true, 24><<<ntp, kQueryTilePair, 0, s>>>(m);
@@ -1036,7 +1066,8 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     }
     // ---- K4' exact re-decision of near ties (grid-stride over a device count)
     {
-        RescanArgs r{rescan, rcount, qbuf, T.data, T.pair_bytes, nt, dim, 4096u, keys, l2};
+        RescanArgs r{rescan, rcount, qbuf, T.data, T.pair_bytes, tile_begin * kBTileRows,
+                     std::min(nt, tile_end * kBTileRows), dim, 4096u, keys, l2};
         const uint32_t grid = 2 * (uint32_t)ctx_sm_count(ctx);
         ProfScope prof(ctx, FNL_KCLASS_RESCAN);
         if (dim == 24) {
@@ -1047,11 +1078,29 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
             else rescan_kernel<false, 0><<<grid, kRescanThreads, 0, s>>>(r);
         }
         FNL_CUDA_TRY(cudaGetLastError());
-        rescan_finish_kernel<<<4, 256, 0, s>>>(rescan, rcount, keys, out, min_dist, out_stride, !l2);
+        rescan_finish_kernel<<<4, 256, 0, s>>>(rescan, rcount, keys, out, min_dist, out_stride, !l2, shard_keys);
         FNL_CUDA_TRY(cudaGetLastError());
     }
     if (debug_mode_trace_dump(ctx, s)) {}
     ctx_count_launches(ctx, 5);
+    return FNL_OK;
+}
+
+int tensor_shard_finalize(fnl_context* ctx, uint32_t npairs, const long long* keys, uint32_t stride,
+                          const uint32_t* d_n_active, const uint8_t* d_done, uint32_t* out) {
+    cudaStream_t s = ctx_stream(ctx);
+    ProfScope prof(ctx, FNL_KCLASS_OTHER);
+    shard_finalize_kernel<<<dim3(ceil_div_u(stride, 256), npairs), 256, 0, s>>>(keys, stride, d_n_active, d_done, out);
+    FNL_CUDA_TRY(cudaGetLastError());
+    ctx_count_launches(ctx, 1);
+    return FNL_OK;
+}
+
+int tensor_shard_reset(fnl_context* ctx, long long* keys, uint64_t n) {
+    cudaStream_t s = ctx_stream(ctx);
+    shard_reset_kernel<<<(uint32_t)std::min<uint64_t>(1024, (n + 255) / 256), 256, 0, s>>>(keys, n);
+    FNL_CUDA_TRY(cudaGetLastError());
+    ctx_count_launches(ctx, 1);
     return FNL_OK;
 }
 

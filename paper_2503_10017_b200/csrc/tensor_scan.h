@@ -48,10 +48,27 @@ int tensor_pack(fnl_context* ctx, const char* tag, const float* d_src, uint32_t 
 // pairs with h_active[p] == 0 or h_done[p] are skipped.  Winner indices land in
 // out[p*out_stride + i]; if min_dist is non-null the exact reference distance of
 // the winner is written beside it.  d_near_ties[p] counts re-decided rows.
+//
+// Target sharding (config C5): only target tiles [tile_begin, tile_end) of T
+// (128 targets per tile; tile_end = 0 means all) are scanned, and with
+// shard_keys non-null the exact per-query winner of that range is written as a
+// signed 64-bit key  ((orderable(dist) << 32 | index) ^ 2^63)  into
+// shard_keys[p*out_stride + i] instead of out/min_dist, so a MIN all-reduce of
+// the keys over the shards (NCCL / gloo int64 MIN) yields the global winner
+// with the reference's lowest-index tie rule; tensor_shard_finalize decodes.
 int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const uint32_t* ids,
                    uint32_t cap, const uint32_t* h_active, const uint8_t* h_done,
                    const PackedMaps& T, uint32_t dim, bool l2, uint32_t* out, uint32_t out_stride,
-                   float* min_dist, unsigned long long* d_near_ties);
+                   float* min_dist, unsigned long long* d_near_ties, uint32_t tile_begin = 0,
+                   uint32_t tile_end = 0, long long* shard_keys = nullptr);
+
+// shard keys -> nearest indices for the active queries of every pair
+int tensor_shard_finalize(fnl_context* ctx, uint32_t npairs, const long long* keys, uint32_t stride,
+                          const uint32_t* d_n_active, const uint8_t* d_done, uint32_t* out);
+int tensor_shard_reset(fnl_context* ctx, long long* keys, uint64_t n);
+// value every shard key starts from (no candidate in this shard)
+constexpr long long kShardKeyNone = 0x7FFFFFFFFFFFFFFFll;
+constexpr uint32_t kTargetTileRows = 128;
 
 // Dense convenience (fnl_nn_query backend TENSOR): all rows of d_q against d_t.
 int tensor_nn_dense(fnl_context* ctx, const float* d_q, uint32_t nq, const float* d_t, uint32_t nt,

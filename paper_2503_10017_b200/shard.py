@@ -1,0 +1,80 @@
+"""Target-column sharding of one oversized pair over N GPUs (config C5).
+
+Every rank holds both descriptor maps.  In each NN pass rank r scans only its
+contiguous range of 128-target tiles of the target map and produces, per
+query, the exact winner of that range as a signed 64-bit key
+
+    key = ((orderable(dist) << 32) | index) ^ 2**63
+
+so that an int64 MIN all-reduce over the ranks (NCCL over NVLink, or gloo)
+selects the global reference winner -- smallest distance, lowest index on an
+exact tie (src/kernels.cpp:202-229, 287-300) -- and every rank continues the
+reciprocal loop (harvest, convergence: src/reciprocal.cpp:142-185) with
+identical state.  The MatchSet is therefore bit-identical to the unsharded
+run.  This is the only collective on the path: 8 B per active query per pass
+(221 KB for 27,648 queries).
+
+The device work is in libfastnn_b200.so (fnl_reciprocal_match_sharded_device);
+this module only supplies the key buffer and the all-reduce callback.
+"""
+import numpy as np
+
+TILE = 128                 # targets per K3 tile (kTargetTileRows)
+KEY_NONE = (1 << 63) - 1   # INT64_MAX: no candidate in this shard
+
+
+def shard_tiles(ntargets, rank, count):
+    """Target tile range [begin, end) of shard `rank` (same split as capi.cu)."""
+    tiles = (ntargets + TILE - 1) // TILE
+    return tiles * rank // count, tiles * (rank + 1) // count
+
+
+def orderable(dist):
+    """float32 -> u32 with the same total order as <, -0 == +0 (fnl_common.cuh)."""
+    b = np.asarray(dist, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    b = np.where(b == 0x80000000, 0, b)
+    return np.where(b & 0x80000000, (~b) & 0xFFFFFFFF, b | 0x80000000).astype(np.uint64)
+
+
+def encode_keys(dist, index):
+    """(dist, global index) -> signed shard keys (int64)."""
+    k = (orderable(dist) << np.uint64(32)) | np.asarray(index, dtype=np.uint64)
+    return (k ^ np.uint64(1 << 63)).view(np.int64)
+
+
+def decode_index(keys):
+    return (np.asarray(keys, dtype=np.int64).view(np.uint64) & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+
+
+def match_sharded(d1, d2, stride=8, metric="dot", group=None, backend="tensor", **kw):
+    """Reciprocal matching of one pair (or a stack) with the target columns
+    sharded over the ranks of `group` (torch.distributed; NCCL on GPUs).
+
+    d1, d2: float32 CUDA tensors [P, H, W, d] (or [H, W, d]) on this rank's
+    device, identical on every rank.  Returns (matches [P, samples, 3] int32
+    device tensor, counts [P] int32 device tensor, per-pair stats) -- equal on
+    every rank and to the unsharded result.
+    """
+    import torch
+    import torch.distributed as dist
+
+    from . import _fastnn
+
+    if d1.dim() == 3:
+        d1, d2 = d1.unsqueeze(0), d2.unsqueeze(0)
+    P, H, W, D = d1.shape
+    samples = ((H + stride - 1) // stride) * ((W + stride - 1) // stride)
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    keys = torch.empty((P * samples,), dtype=torch.int64, device=d1.device)
+    pairs = torch.empty((P, samples, 3), dtype=torch.int32, device=d1.device)
+    counts = torch.empty((P,), dtype=torch.int32, device=d1.device)
+
+    def reduce(count):
+        dist.all_reduce(keys[:count], op=dist.ReduceOp.MIN, group=group)
+
+    stream = torch.cuda.current_stream(d1.device).cuda_stream
+    stats = _fastnn.reciprocal_match_sharded_device(
+        d1.data_ptr(), d2.data_ptr(), P, H, W, D, pairs.data_ptr(), counts.data_ptr(), keys.data_ptr(),
+        keys.numel(), rank, world, reduce, backend=backend, stride=stride, metric=metric, stream=stream, **kw)
+    return pairs, counts, stats

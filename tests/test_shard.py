@@ -1,0 +1,84 @@
+"""Config C5 host logic on CPU: target-column sharding with an int64 MIN
+all-reduce over world_size 2 (gloo).  The keys carry (exact distance, global
+index); the test pins that MIN over shard keys is the reference's global NN
+(lowest index on exact ties) using the C oracle per shard."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_shard_tiles_cover_exactly():
+    from paper_2503_10017_b200.shard import shard_tiles
+    for nt in (1, 127, 128, 129, 196608, 1769472):
+        for world in (1, 2, 3, 8, 16):
+            ranges = [shard_tiles(nt, r, world) for r in range(world)]
+            assert ranges[0][0] == 0 and ranges[-1][1] == (nt + 127) // 128
+            assert all(ranges[i][1] == ranges[i + 1][0] for i in range(world - 1))
+
+
+def test_key_order_matches_reference_tie_rule():
+    from paper_2503_10017_b200.shard import decode_index, encode_keys
+    rng = np.random.default_rng(0)
+    d = rng.standard_normal(4000).astype(np.float32)
+    d[::7] = 0.0
+    d[1::7] = -0.0
+    d[2::11] = d[3::11][: len(d[2::11])]  # exact ties
+    idx = rng.permutation(4000).astype(np.uint32)
+    k = encode_keys(d, idx)
+    order = np.argsort(k, kind="stable")
+    # sorted by (dist, index) with -0 == +0
+    dd = np.where(d == 0, np.float32(0), d)
+    ref = np.lexsort((idx, dd))
+    assert np.array_equal(order, ref)
+    assert np.array_equal(decode_index(k), idx)
+
+
+def _worker(rank, world, port, q, t, metric, out):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle
+    from paper_2503_10017_b200.shard import encode_keys, shard_tiles
+    tb, te = shard_tiles(len(t), rank, world)
+    t0, t1 = tb * 128, min(len(t), te * 128)
+    if t1 > t0:
+        r = oracle.nn_scan(q, t[t0:t1], metric=metric)
+        keys = encode_keys(r["min_dist"], r["nearest"].astype(np.uint64) + t0)
+    else:
+        keys = np.full(len(q), (1 << 63) - 1, np.int64)
+    kt = torch.from_numpy(keys.copy())
+    dist.all_reduce(kt, op=dist.ReduceOp.MIN)
+    out[rank] = kt.numpy().copy()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,metric", [(2, "dot"), (2, "l2"), (3, "dot")])
+def test_sharded_min_reduce_equals_global_nn(world, metric):
+    import torch.multiprocessing as mp
+    from oracle import oracle
+    from paper_2503_10017_b200.shard import decode_index
+    rng = np.random.default_rng(1)
+    t = rng.standard_normal((700, 24)).astype(np.float32)
+    t[600] = t[100]                      # exact duplicate across the shard boundary:
+    q = rng.standard_normal((50, 24)).astype(np.float32)
+    q[7] = t[100]                        # the lower index (100) must win
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    mp.spawn(_worker, args=(world, port, q, t, metric, out), nprocs=world, join=True)
+    want = oracle.nn_scan(q, t, metric=metric)["nearest"]
+    for r in range(world):
+        assert np.array_equal(decode_index(out[r]), want)
+    assert decode_index(out[0])[7] == 100
