@@ -317,6 +317,18 @@ def main_b200(args):
     e2e_s = time.perf_counter() - t0
     barrier()
 
+    # ---- C5: one oversized 1536x1152 pair, target columns sharded over the ranks
+    c5 = None
+    if not args.no_c5:
+        c5 = bench_c5(fnl, world, rank, local)
+
+    # ---- C3: FlashMatch attention at the MASt3R ViT shapes (rank 0)
+    c3 = None
+    if rank == 0 and not args.no_c3:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import bench_flashmatch
+        c3 = bench_flashmatch.run(peaks()[0])
+
     # ---- max over ranks
     max_ms, max_e2e = allreduce([elapsed_ms, e2e_s], op=__import__("torch").distributed.ReduceOp.MAX) \
         if world > 1 else (elapsed_ms, e2e_s)
@@ -383,8 +395,45 @@ def main_b200(args):
                      "avg_launch_ms": tot_score_ms / max(1, tot_launch)},
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
+        "c5_sharded_pair": c5,
+        "c3_flashmatch": c3,
     }
     print(json.dumps(line), flush=True)
+
+
+C5_H, C5_W = 1536, 1152
+
+
+def bench_c5(fnl, world, rank, local, reps=3):
+    """Config C5: one 1536x1152 d=24 pair (1,769,472 px/image, 27,648 samples),
+    every NN pass scanning 1/world of the target columns per rank with one
+    int64 MIN all-reduce of the per-query (dist, index) keys (NCCL).  Device
+    time per pair, max over ranks."""
+    import torch
+    from paper_2503_10017_b200.shard import match_sharded
+    D1 = torch.from_numpy(fnl.gen_random(C5_H, C5_W, D, 2606)).cuda()
+    D2 = torch.from_numpy(fnl.gen_random(C5_H, C5_W, D, 2607)).cuda()
+    stream = torch.cuda.current_stream()
+    match_sharded(D1, D2, stride=STRIDE, metric=METRIC)  # warm-up (workspace, packing)
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        pairs, counts, stats = match_sharded(D1, D2, stride=STRIDE, metric=METRIC)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    ms = allreduce([ms], op=__import__("torch").distributed.ReduceOp.MAX)[0] if world > 1 else ms
+    rows = stats[0]["query_rows"]
+    flops = FLOP_PER_SCORE * C5_H * C5_W * rows
+    return {"workload": f"C5: one {C5_H}x{C5_W} d=24 pair (gen_random 2606/2607), stride 8 "
+                        f"({((C5_H + 7) // 8) * ((C5_W + 7) // 8)} samples), dot, tensor backend, target columns "
+                        f"sharded over {world} rank(s), int64 MIN all-reduce of (dist, index) keys per NN pass",
+            "shards": world, "ms_per_pair": round(ms, 3), "pairs_per_s": round(1000.0 / ms, 2),
+            "query_rows": int(rows), "iterations": int(stats[0]["iterations"]),
+            "matches": int(counts[0].item()),
+            "aggregate_tflops": round(flops / (ms / 1e3) / 1e12, 1)}
 
 
 def main():
@@ -398,6 +447,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c5", action="store_true", help="skip the sharded 1536x1152 pair (config C5)")
+    ap.add_argument("--no-c3", action="store_true", help="skip the FlashMatch attention section (config C3)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
