@@ -287,7 +287,7 @@ struct TcArgs {
     uint32_t nt;
     const TcItem* items;
     uint32_t nitems;
-    float4* partial;  // [item][256][2] = (b1, b2, b3, t1 bits), (t2 bits, 0, 0, 0)
+    float4* partial;  // [item][col half][256][2] = (b1, b2, b3, t1 bits), (t2 bits, 0, 0, 0)
     int debug;        // profiling only: 1 = epilogue releases buffers unread, 16 = clock trace of CTA 0
     unsigned long long* trace;  // [4][4096] clock64 stamps (debug & 16)
 };
@@ -312,9 +312,10 @@ constexpr uint32_t kBTileBytes = kBTileRows * kPackRowBytes;  // 8 KB
 constexpr int kStages = 8;
 constexpr int kAccBufs = 2;
 // warps: 0 loader, 1-2 MMA issuers (even / odd tiles), 3..10 epilogue (qt = (w-3)/4, quadrant = w%4)
-constexpr int kScanThreads = 352;
-constexpr int kEpiWarpsPerQt = 4;
+constexpr int kEpiColSplit = 2;  // epilogue warps per (query tile, lane quadrant): 64-target sub-tile each
+constexpr int kEpiWarpsPerQt = 4 * kEpiColSplit;
 constexpr int kFirstEpiWarp = 3;
+constexpr int kScanThreads = (kFirstEpiWarp + 2 * kEpiWarpsPerQt) * 32;
 constexpr uint32_t kSmemA = 2 * kTileBytes;                  // 16 KB: two query tiles
 constexpr uint32_t kSmemB = kStages * kBTileBytes;           // 64 KB ring
 constexpr uint32_t kSmemBars = (2 * kStages + 2 * kAccBufs + 2 + 2) * 8;
@@ -476,8 +477,12 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
             __syncwarp();
         }
     } else {
-        // ---------------- epilogue: 8 warps, query tile qt, TMEM lane quadrant w%4
-        const uint32_t e = warp - kFirstEpiWarp, qt = e >> 2, quad = warp & 3u;
+        // ---------------- epilogue: 2 x kEpiWarpsPerQt warps; warp = (query tile
+        // qt, column half ch, TMEM lane quadrant w%4).  Each warp owns one
+        // 64-target sub-tile of every 128-target tile, so four warps per SMSP
+        // overlap their TMEM-load / compare latencies.
+        const uint32_t e = warp - kFirstEpiWarp, grp = e >> 2, quad = warp & 3u;
+        const uint32_t qt = grp / kEpiColSplit, ch = grp % kEpiColSplit;
         const uint32_t row = qt * 128u + quad * 32u + lane;  // 0..255 within the tile pair
         const uint32_t lane_base = (quad * 32u) << 16;
         uint32_t total = 0;  // tiles this CTA will score
@@ -487,7 +492,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
         if (lane == 0)
             for (uint32_t j = 0; j < kAccBufs && j < total; ++j) mbar_arrive(&full[j % kStages]);
         uint32_t k = 0;
-        Frag f0, f1, f2, f3;
+        Frag f0, f1;
         for (uint32_t u = blockIdx.x; u < a.nitems; u += G) {
             const TcItem item = a.items[u];
             const bool warp_real = qt * 128u + quad * 32u < item.nvalid;  // else all rows padding
@@ -504,25 +509,21 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
                     continue;
                 }
                 tc_fence_after();
-                const uint32_t taddr = tmem + lane_base + acc * 256u + qt * 128u;
+                const uint32_t taddr = tmem + lane_base + acc * 256u + qt * 128u + ch * kSubTile;
                 frag_ld(taddr + 0, f0);
                 frag_ld(taddr + 32, f1);
-                frag_ld(taddr + 64, f2);
-                frag_ld(taddr + 96, f3);
                 frag_wait2(f0, f1);
-                frag_wait2(f2, f3);
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0 && next) mbar_arrive(&full[(k + kAccBufs) % kStages]);  // buffer drained
                 if (tw && lane == 0) a.trace[16384 + k] = clock64();
-                subtile_scan(st, f0, f1, 2 * t, a.nt);
-                subtile_scan(st, f2, f3, 2 * t + 1, a.nt);
+                subtile_scan(st, f0, f1, 2 * t + ch, a.nt);
                 if (tw) {
                     __syncwarp();
                     if (lane == 0) a.trace[20480 + k] = clock64() + (st.b1 > 1e30f ? 1 : 0);
                 }
             }
-            float4* po = a.partial + ((uint64_t)u * kQueryTilePair + row) * 2;
+            float4* po = a.partial + (((uint64_t)u * kEpiColSplit + ch) * kQueryTilePair + row) * 2;
             po[0] = make_float4(st.b1, st.b2, st.b3, __uint_as_float(st.t1));
             po[1] = make_float4(__uint_as_float(st.t2), 0.0f, 0.0f, 0.0f);
         }
@@ -595,8 +596,8 @@ __global__ void __launch_bounds__(kQueryTilePair) merge_kernel(MergeArgs a) {
                 B3 = fmaxf(B3, v);
             }
         };
-        for (uint32_t s = 0; s < a.splits; ++s) {
-            const float4* pp = a.partial + (((uint64_t)tp * a.splits + s) * kQueryTilePair + r) * 2;
+        for (uint32_t s = 0; s < a.splits * kEpiColSplit; ++s) {
+            const float4* pp = a.partial + (((uint64_t)tp * a.splits * kEpiColSplit + s) * kQueryTilePair + r) * 2;
             const float4 p = pp[0];
             const float4 p2 = pp[1];
             insert(p.x, __float_as_uint(p.w));
@@ -1010,7 +1011,7 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     uint32_t* d_active;
     TRY(ws_arr(ctx, "tc.qbuf", (size_t)rows_total * kPackRowBytes, &qbuf));
     TRY(ws_arr(ctx, "tc.margin", rows_total, &margin));
-    TRY(ws_arr(ctx, "tc.partial", (size_t)nitems * kQueryTilePair * 2, &partial));
+    TRY(ws_arr(ctx, "tc.partial", (size_t)nitems * kEpiColSplit * kQueryTilePair * 2, &partial));
     TRY(ws_arr(ctx, "tc.rescan", (size_t)3 * rows_total, &rescan));
     TRY(ws_arr(ctx, "tc.rcount", 1, &rcount));
     TRY(ws_arr(ctx, "tc.keys", rows_total, &keys));
