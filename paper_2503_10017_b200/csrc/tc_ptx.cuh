@@ -35,6 +35,34 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
             : "memory");
     } while (!done);
 }
+// try_wait with a long suspend-time hint: the warp sleeps in hardware until
+// the phase completes (or the hint expires) instead of re-polling, so helper
+// warps (loader / MMA issuer) do not steal issue slots from co-resident
+// epilogue warps on the same SM sub-partition
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    const uint32_t a = smem_addr(bar);
+    do {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(a), "r"(parity), "r"(1000000u)
+            : "memory");
+    } while (!done);
+}
+// spin on mbarrier.test_wait (never suspends the warp): lower wake-up latency
+// than try_wait when the phase completes within a few hundred cycles
+__device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    const uint32_t a = smem_addr(bar);
+    do {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+    } while (!done);
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
