@@ -363,7 +363,9 @@ def main_b200(args):
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                traffic = json.load(f).get("dram_bytes_per_launch")
+                pj = json.load(f)
+            # ncu figure of one captured launch, scaled per pair to this run's launches
+            traffic = pj["dram_bytes_per_launch"] / pj.get("pairs_in_launch", 1) * B
         except Exception:
             traffic = None
     line = {
