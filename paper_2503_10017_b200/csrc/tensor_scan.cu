@@ -58,6 +58,7 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
 }
 // kind::f16 instruction descriptor: A/B fp16, D fp32, both K-major, M=128, N=128.
 constexpr uint32_t kIdescF16M128N128 = (1u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+constexpr uint32_t kIdescF16M128N256 = (1u << 4) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
 
 __host__ __device__ __forceinline__ uint64_t packed_offset(uint32_t row, uint32_t chunk) {
     return (uint64_t)(row >> 3) * 512u + chunk * 128u + (row & 7u) * 16u;
@@ -292,33 +293,29 @@ struct TcArgs {
     unsigned long long* trace;  // [4][4096] clock64 stamps (debug & 16)
 };
 
-// K3 structure (measured on this B200: tools/ubench_mma.cu, ubench_epilogue.cu
-// and per-tile clock traces via FNL_TC_DEBUG=16):
-//  * tcgen05.mma M=128 N=128 K=16 runs at the full 64 cycles with both operands
-//    in shared memory when issued from a warp-uniform loop via elect.sync (a
-//    diverged single lane costs ~55% more).  An mbarrier try_wait costs
-//    ~60-110 cycles even when the phase is complete, so a target tile is 128
-//    targets (4 MMAs = 256 tensor cycles), each issuer waits on ONE barrier per
-//    tile, and two issuer warps alternate tiles so one's wait overlaps the
-//    other's MMAs.
-//  * TMEM (512 columns) holds two fp32 accumulator buffers of 2 query tiles x
-//    128 targets.  The B barrier of tile k completes only when its bytes
-//    landed AND all eight epilogue warps released tile k-2's accumulator.
-//  * The epilogue pulls a whole 128-column slice (4 tcgen05.ld), releases the
-//    buffer, then compares; the two query tiles commit separately so the two
-//    epilogue warps of each SM sub-partition start staggered.
-constexpr uint32_t kBTileRows = 128;
-constexpr uint32_t kBTileBytes = kBTileRows * kPackRowBytes;  // 8 KB
-constexpr int kStages = 8;
-constexpr int kAccBufs = 2;
-// warps: 0 loader, 1-2 MMA issuers (even / odd tiles), 3..10 epilogue (qt = (w-3)/4, quadrant = w%4)
-constexpr int kEpiColSplit = 2;  // epilogue warps per (query tile, lane quadrant): 64-target sub-tile each
-constexpr int kEpiWarpsPerQt = 4 * kEpiColSplit;
+// K3 structure (v8; measured on this B200 with the clock traces of
+// FNL_TC_DEBUG=16):
+//  * a target tile is 256 targets (16 KB, one cp.async.bulk); each query tile
+//    qt (128 rows) owns one TMEM accumulator buffer of 256 fp32 columns
+//    (columns 256*qt), filled by two tcgen05.mma M128 N256 K16 (the 24
+//    channels + norm terms padded to K=32) issued by its own issuer warp
+//    (warp 1 + qt), so each barrier has exactly one producer and one consumer
+//    chain and an issuer only ever waits on "B landed" + "my buffer drained";
+//  * all 16 epilogue warps drain every buffer: warp = (64-column quarter,
+//    TMEM lane quadrant w%4); two tcgen05.ld.x32, release, then compare, and
+//    the other query tile's buffer is refilled while they compare.
+constexpr uint32_t kBTileRows = kTargetTileRows;                // 256 targets per B tile
+constexpr uint32_t kBTileBytes = kBTileRows * kPackRowBytes;  // 16 KB
+constexpr int kStages = 4;
+// warps: 0 loader, 1-2 MMA issuers (query tile 0 / 1), 3..18 epilogue
+// (column quarter = (w-3)/4, TMEM lane quadrant = w%4)
+constexpr int kEpiColSplit = 4;  // 64-target sub-tiles per 256-target tile, one epilogue warp each
+constexpr int kEpiWarps = 4 * kEpiColSplit;
 constexpr int kFirstEpiWarp = 3;
-constexpr int kScanThreads = (kFirstEpiWarp + 2 * kEpiWarpsPerQt) * 32;
+constexpr int kScanThreads = (kFirstEpiWarp + kEpiWarps) * 32;
 constexpr uint32_t kSmemA = 2 * kTileBytes;                  // 16 KB: two query tiles
 constexpr uint32_t kSmemB = kStages * kBTileBytes;           // 64 KB ring
-constexpr uint32_t kSmemBars = (2 * kStages + 2 * kAccBufs + 2 + 2) * 8;
+constexpr uint32_t kSmemBars = (2 * kStages + 4 + 2 + 2) * 8;
 // A double buffered (next unit's queries load under the current unit); padded
 // past half the SM's shared memory so no second CTA co-resides and spins in
 // tcgen05.alloc for the 512 TMEM columns.
@@ -380,12 +377,13 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint32_t tmem_slot;
     uint8_t* sA = smem;                  // [2][16 KB]
-    uint8_t* sB = smem + 2 * kSmemA;     // [kStages][8 KB]
+    uint8_t* sB = smem + 2 * kSmemA;     // [kStages][16 KB]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kSmemA + kSmemB);
-    uint64_t* full = bars;                     // [kStages]  B landed + accumulator free
-    uint64_t* empty = bars + kStages;          // [kStages]  MMAs of the slot retired
-    uint64_t* tfull = bars + 2 * kStages;      // [kAccBufs][2 query tiles]
-    uint64_t* afull = tfull + 2 * kAccBufs;    // [2]
+    uint64_t* full = bars;                     // [kStages]  B tile landed
+    uint64_t* empty = bars + kStages;          // [kStages]  both query tiles' MMAs on the slot retired
+    uint64_t* tfull = bars + 2 * kStages;      // [2]  accumulator of query tile qt ready
+    uint64_t* accfree = tfull + 2;             // [2]  accumulator of query tile qt drained
+    uint64_t* afull = accfree + 2;             // [2]
     uint64_t* afree = afull + 2;               // [2]
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -394,13 +392,14 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], 1 + 2 * kEpiWarpsPerQt);
-            mbar_init(&empty[s], 1);
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 2);  // one commit per issuer
         }
-        for (int b = 0; b < 2 * kAccBufs; ++b) mbar_init(&tfull[b], 1);
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(&afull[b], 1);
-            mbar_init(&afree[b], 2);  // both MMA issuers
+        for (int q = 0; q < 2; ++q) {
+            mbar_init(&tfull[q], 1);
+            mbar_init(&accfree[q], kEpiWarps);
+            mbar_init(&afull[q], 1);
+            mbar_init(&afree[q], 2);  // both MMA issuers
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -439,93 +438,87 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
             }
         }
     } else if (warp == 1 || warp == 2) {
-        // ---------------- MMA issuers: warp 1 even tiles, warp 2 odd tiles
-        // (disjoint accumulator buffers and stages); warp-uniform loops, one
-        // elected lane issues.
-        const uint32_t parity = warp - 1;
+        // ---------------- MMA issuer of query tile qt = warp - 1: per target
+        // tile, wait "B landed" and "my accumulator drained", two MMAs
+        // (K-steps) M128 N256 into TMEM columns [256 qt, 256 qt + 256)
+        const uint32_t qt = warp - 1;
         const uint32_t b_addr = smem_addr(sB);
+        const uint32_t d = tmem + qt * 256u;
         uint32_t k = 0, i = 0;
         for (uint32_t u = blockIdx.x; u < a.nitems; u += G, ++i) {
             const uint32_t nt_unit = a.items[u].tile_end - a.items[u].tile_begin;
             const uint32_t ab = i & 1u;
             mbar_wait(&afull[ab], (i >> 1) & 1u);
             tc_fence_after();
-            const uint32_t a_addr = smem_addr(sA + ab * kSmemA);
-            const uint64_t ad0 = umma_desc(a_addr), ad1 = umma_desc(a_addr + kTileBytes);
+            const uint64_t ad = umma_desc(smem_addr(sA + ab * kSmemA + qt * kTileBytes));
             for (uint32_t t = 0; t < nt_unit; ++t, ++k) {
-                if ((k & 1u) != parity) continue;
-                const uint32_t s = k % kStages, acc = k % kAccBufs;
-                if (trace && lane == 0 && k < 4096) a.trace[4096 + k] = clock64();
+                const uint32_t s = k % kStages;
+                if (trace && qt == 0 && lane == 0 && k < 4096) a.trace[4096 + k] = clock64();
                 mbar_wait(&full[s], (k / kStages) & 1u);
-                if (trace && lane == 0 && k < 4096) a.trace[8192 + k] = clock64();
+                mbar_wait(&accfree[qt], (k & 1u) ^ 1u);
+                if (trace && qt == 0 && lane == 0 && k < 4096) a.trace[8192 + k] = clock64();
                 tc_fence_after();
                 if (elect_one()) {
                     const uint64_t bd = umma_desc(b_addr + s * kBTileBytes);
-                    const uint32_t d = tmem + acc * 256u;
                     // K-step 1 starts 256 B (two 8-channel chunks) further: +16 in descriptor units
-                    tc_mma_f16(d, ad0, bd, kIdescF16M128N128, 0u);
-                    tc_mma_f16(d, ad0 + 16u, bd + 16u, kIdescF16M128N128, 1u);
-                    tc_commit(&tfull[acc * 2 + 0]);
-                    tc_mma_f16(d + 128u, ad1, bd, kIdescF16M128N128, 0u);
-                    tc_mma_f16(d + 128u, ad1 + 16u, bd + 16u, kIdescF16M128N128, 1u);
-                    tc_commit(&tfull[acc * 2 + 1]);
+                    tc_mma_f16(d, ad, bd, kIdescF16M128N256, 0u);
+                    tc_mma_f16(d, ad + 16u, bd + 16u, kIdescF16M128N256, 1u);
+                    tc_commit(&tfull[qt]);
                     tc_commit(&empty[s]);
                 }
                 __syncwarp();
             }
-            if (elect_one()) tc_commit(&afree[ab]);  // this issuer no longer reads this unit's query tiles
+            if (elect_one()) tc_commit(&afree[ab]);  // this issuer no longer reads this unit's query tile
             __syncwarp();
         }
     } else {
-        // ---------------- epilogue: 2 x kEpiWarpsPerQt warps; warp = (query tile
-        // qt, column half ch, TMEM lane quadrant w%4).  Each warp owns one
-        // 64-target sub-tile of every 128-target tile, so four warps per SMSP
-        // overlap their TMEM-load / compare latencies.
-        const uint32_t e = warp - kFirstEpiWarp, grp = e >> 2, quad = warp & 3u;
-        const uint32_t qt = grp / kEpiColSplit, ch = grp % kEpiColSplit;
-        const uint32_t row = qt * 128u + quad * 32u + lane;  // 0..255 within the tile pair
+        // ---------------- epilogue: 16 warps = (64-column quarter ch, TMEM lane
+        // quadrant w%4); every warp drains both query tiles' buffers, keeping
+        // one running top-3 state per query tile
+        const uint32_t e = warp - kFirstEpiWarp, ch = e >> 2, quad = warp & 3u;
         const uint32_t lane_base = (quad * 32u) << 16;
-        uint32_t total = 0;  // tiles this CTA will score
-        for (uint32_t u = blockIdx.x; u < a.nitems; u += G) total += a.items[u].tile_end - a.items[u].tile_begin;
-        // releasing tile k's accumulator enables tile k + kAccBufs; the first
-        // kAccBufs tiles start with free buffers
-        if (lane == 0)
-            for (uint32_t j = 0; j < kAccBufs && j < total; ++j) mbar_arrive(&full[j % kStages]);
         uint32_t k = 0;
         Frag f0, f1;
         for (uint32_t u = blockIdx.x; u < a.nitems; u += G) {
             const TcItem item = a.items[u];
-            const bool warp_real = qt * 128u + quad * 32u < item.nvalid;  // else all rows padding
-            RowState st{-INFINITY, -INFINITY, -INFINITY, 0xFFFFFFFFu, 0xFFFFFFFFu};
+            RowState st[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) st[q] = RowState{-INFINITY, -INFINITY, -INFINITY, 0xFFFFFFFFu, 0xFFFFFFFFu};
             for (uint32_t t = item.tile_begin; t < item.tile_end; ++t, ++k) {
-                const uint32_t acc = k % kAccBufs;
-                const bool next = k + kAccBufs < total;
-                mbar_wait(&tfull[acc * 2 + qt], (k / kAccBufs) & 1u);
-                const bool tw = trace && warp == kFirstEpiWarp && k < 4096;
-                if (tw && lane == 0) a.trace[12288 + k] = clock64();
-                if (!warp_real || (a.debug & 1)) {  // nothing to score: hand the buffer straight back
+#pragma unroll
+                for (uint32_t qt = 0; qt < 2; ++qt) {
+                    const bool warp_real = qt * 128u + quad * 32u < item.nvalid;  // else all rows padding
+                    mbar_wait(&tfull[qt], k & 1u);
+                    const bool tw = trace && qt == 0 && warp == kFirstEpiWarp && k < 4096;
+                    if (tw && lane == 0) a.trace[12288 + k] = clock64();
+                    if (!warp_real || (a.debug & 1)) {  // nothing to score: hand the buffer straight back
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&accfree[qt]);
+                        continue;
+                    }
+                    tc_fence_after();
+                    const uint32_t taddr = tmem + lane_base + qt * 256u + ch * kSubTile;
+                    frag_ld(taddr + 0, f0);
+                    frag_ld(taddr + 32, f1);
+                    frag_wait2(f0, f1);
+                    tc_fence_before();
                     __syncwarp();
-                    if (lane == 0 && next) mbar_arrive(&full[(k + kAccBufs) % kStages]);
-                    continue;
-                }
-                tc_fence_after();
-                const uint32_t taddr = tmem + lane_base + acc * 256u + qt * 128u + ch * kSubTile;
-                frag_ld(taddr + 0, f0);
-                frag_ld(taddr + 32, f1);
-                frag_wait2(f0, f1);
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0 && next) mbar_arrive(&full[(k + kAccBufs) % kStages]);  // buffer drained
-                if (tw && lane == 0) a.trace[16384 + k] = clock64();
-                subtile_scan(st, f0, f1, 2 * t + ch, a.nt);
-                if (tw) {
-                    __syncwarp();
-                    if (lane == 0) a.trace[20480 + k] = clock64() + (st.b1 > 1e30f ? 1 : 0);
+                    if (lane == 0) mbar_arrive(&accfree[qt]);  // this warp's columns drained
+                    if (tw && lane == 0) a.trace[16384 + k] = clock64();
+                    subtile_scan(st[qt], f0, f1, t * kEpiColSplit + ch, a.nt);
+                    if (tw) {
+                        __syncwarp();
+                        if (lane == 0) a.trace[20480 + k] = clock64() + (st[qt].b1 > 1e30f ? 1 : 0);
+                    }
                 }
             }
-            float4* po = a.partial + (((uint64_t)u * kEpiColSplit + ch) * kQueryTilePair + row) * 2;
-            po[0] = make_float4(st.b1, st.b2, st.b3, __uint_as_float(st.t1));
-            po[1] = make_float4(__uint_as_float(st.t2), 0.0f, 0.0f, 0.0f);
+#pragma unroll
+            for (uint32_t qt = 0; qt < 2; ++qt) {
+                const uint32_t row = qt * 128u + quad * 32u + lane;  // 0..255 within the tile pair
+                float4* po = a.partial + (((uint64_t)u * kEpiColSplit + ch) * kQueryTilePair + row) * 2;
+                po[0] = make_float4(st[qt].b1, st[qt].b2, st[qt].b3, __uint_as_float(st[qt].t1));
+                po[1] = make_float4(__uint_as_float(st[qt].t2), 0.0f, 0.0f, 0.0f);
+            }
         }
     }
     tc_fence_before();
@@ -902,7 +895,8 @@ int tensor_pack(fnl_context* ctx, const char* tag, const float* d_src, uint32_t 
         return fail(FNL_EINVAL, "tensor backend: descriptor dim " + std::to_string(dim) + " exceeds " +
                                     std::to_string(l2 ? kPackK - 2 : kPackK) + " (" + (l2 ? "l2" : "dot") +
                                     " metric); use the exact backends");
-    const uint32_t rows_pad = ceil_div_u(rows, kTileRows) * kTileRows;
+    // padded to whole 256-target B tiles (also a whole number of 128-row operand tiles)
+    const uint32_t rows_pad = ceil_div_u(rows, kTargetTileRows) * kTargetTileRows;
     const uint64_t pair_bytes = (uint64_t)rows_pad * kPackRowBytes;
     std::string t(tag);
     TRY(ws_arr(ctx, (t + ".packed").c_str(), (size_t)npairs * pair_bytes, &out->data));

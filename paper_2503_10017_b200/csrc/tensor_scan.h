@@ -50,7 +50,7 @@ int tensor_pack(fnl_context* ctx, const char* tag, const float* d_src, uint32_t 
 // the winner is written beside it.  d_near_ties[p] counts re-decided rows.
 //
 // Target sharding (config C5): only target tiles [tile_begin, tile_end) of T
-// (128 targets per tile; tile_end = 0 means all) are scanned, and with
+// (kTargetTileRows = 256 targets per tile; tile_end = 0 means all) are scanned, and with
 // shard_keys non-null the exact per-query winner of that range is written as a
 // signed 64-bit key  ((orderable(dist) << 32 | index) ^ 2^63)  into
 // shard_keys[p*out_stride + i] instead of out/min_dist, so a MIN all-reduce of
@@ -68,7 +68,7 @@ int tensor_shard_finalize(fnl_context* ctx, uint32_t npairs, const long long* ke
 int tensor_shard_reset(fnl_context* ctx, long long* keys, uint64_t n);
 // value every shard key starts from (no candidate in this shard)
 constexpr long long kShardKeyNone = 0x7FFFFFFFFFFFFFFFll;
-constexpr uint32_t kTargetTileRows = 128;
+constexpr uint32_t kTargetTileRows = 256;  // targets per K3 B tile (shard granularity)
 
 // Dense convenience (fnl_nn_query backend TENSOR): all rows of d_q against d_t.
 int tensor_nn_dense(fnl_context* ctx, const float* d_q, uint32_t nq, const float* d_t, uint32_t nt,

@@ -1,7 +1,7 @@
 """Target-column sharding of one oversized pair over N GPUs (config C5).
 
 Every rank holds both descriptor maps.  In each NN pass rank r scans only its
-contiguous range of 128-target tiles of the target map and produces, per
+contiguous range of 256-target tiles of the target map and produces, per
 query, the exact winner of that range as a signed 64-bit key
 
     key = ((orderable(dist) << 32) | index) ^ 2**63
@@ -19,7 +19,7 @@ this module only supplies the key buffer and the all-reduce callback.
 """
 import numpy as np
 
-TILE = 128                 # targets per K3 tile (kTargetTileRows)
+TILE = 256                 # targets per K3 tile (kTargetTileRows)
 KEY_NONE = (1 << 63) - 1   # INT64_MAX: no candidate in this shard
 
 

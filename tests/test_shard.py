@@ -18,11 +18,11 @@ def _free_port():
 
 
 def test_shard_tiles_cover_exactly():
-    from paper_2503_10017_b200.shard import shard_tiles
+    from paper_2503_10017_b200.shard import TILE, shard_tiles
     for nt in (1, 127, 128, 129, 196608, 1769472):
         for world in (1, 2, 3, 8, 16):
             ranges = [shard_tiles(nt, r, world) for r in range(world)]
-            assert ranges[0][0] == 0 and ranges[-1][1] == (nt + 127) // 128
+            assert ranges[0][0] == 0 and ranges[-1][1] == (nt + TILE - 1) // TILE
             assert all(ranges[i][1] == ranges[i + 1][0] for i in range(world - 1))
 
 
@@ -50,9 +50,9 @@ def _worker(rank, world, port, q, t, metric, out):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from oracle import oracle
-    from paper_2503_10017_b200.shard import encode_keys, shard_tiles
+    from paper_2503_10017_b200.shard import TILE, encode_keys, shard_tiles
     tb, te = shard_tiles(len(t), rank, world)
-    t0, t1 = tb * 128, min(len(t), te * 128)
+    t0, t1 = tb * TILE, min(len(t), te * TILE)
     if t1 > t0:
         r = oracle.nn_scan(q, t[t0:t1], metric=metric)
         keys = encode_keys(r["min_dist"], r["nearest"].astype(np.uint64) + t0)
