@@ -395,6 +395,299 @@ __global__ void __launch_bounds__(kFmThreads, 2) flashmatch_kernel(FmArgs a) {
     }
 }
 
+// ---------------------------------------------------------------- v2 (product)
+// Two query tiles per CTA, warp-specialised (FA4-style ping-pong):
+//   warps 0-3  softmax warpgroup of query tile 0, warps 4-7 of tile 1
+//              (thread = query row = TMEM lane; tile t owns TMEM columns
+//              [256 t, 256 t + 256): S in the first 128, O_j double buffer)
+//   warp 8     MMA issuer for both tiles (S = Q K^T, O_j = P V)
+//   warp 9     loader: Q tiles, then a 3-stage K/V ring (cp.async, completion
+//              signalled with cp.async.mbarrier.arrive.noinc)
+// Hand-offs are mbarriers only (no CTA barrier in the loop):
+//   kv_full[st] / kv_empty[st]  loader <-> MMA warp
+//   s_full[t]   S_t(j) ready                   MMA -> softmax t
+//   p_full[t]   P_t(j) written, S_t(j) drained  softmax t -> MMA (4 warp arrivals)
+//   o_full[t][b] PV_t(j) retired, b = j&1      MMA -> softmax t
+// The MMA warp serves whichever tile published P first, and tile 1 starts
+// one softmax behind tile 0, so the two warpgroups take turns on the MUFU
+// (16 ex2/clk/SM, measured: tools/ubench_mufu.cu) while the other tile's S /
+// PV run on the tensor core.  The softmax streams its 128 scores through TMEM
+// twice in 32-column chunks (pass 1 row max; pass 2 exp2, row sum, binary16 P)
+// so S never occupies 128 registers.  160 + 64 KB smem, 512 TMEM columns,
+// one CTA per SM.
+constexpr uint32_t kFm2Threads = 320;
+constexpr uint32_t kKvStages = 3;  // K/V ring depth
+constexpr uint32_t kSmemFm2 = 2 * kTileQK + 2 * kKvStages * kTileQK + 2 * kTileP + 64;
+
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+    uint32_t done;
+    asm volatile(
+        "{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+    return done != 0;
+}
+
+// one 128 x 64 tile loaded by ONE warp (32 x 16 B per step, 32 steps)
+template <bool kV>
+__device__ __forceinline__ void load_tile_warp(uint32_t sbase, const __half* g, uint64_t sn, uint32_t nvalid) {
+    const uint32_t lane = threadIdx.x & 31u;
+#pragma unroll 8
+    for (uint32_t combo = 0; combo < 32u; ++combo) {
+        const uint32_t chunk = (lane >> 3) + 4u * (combo & 1u);
+        const uint32_t row = (combo >> 1) * 8u + (lane & 7u);
+        const bool valid = row < nvalid;
+        const __half* src = g + (valid ? (uint64_t)row * sn + chunk * 8u : 0);
+        cp_async16(sbase + (kV ? off_v(row, chunk) : off_qk(row, chunk)), src, valid);
+    }
+}
+
+__device__ __forceinline__ void frag_wait1(Frag& f) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(f.r[0]), "+r"(f.r[1]), "+r"(f.r[2]), "+r"(f.r[3]), "+r"(f.r[4]), "+r"(f.r[5]), "+r"(f.r[6]),
+                   "+r"(f.r[7]), "+r"(f.r[8]), "+r"(f.r[9]), "+r"(f.r[10]), "+r"(f.r[11]), "+r"(f.r[12]),
+                   "+r"(f.r[13]), "+r"(f.r[14]), "+r"(f.r[15]), "+r"(f.r[16]), "+r"(f.r[17]), "+r"(f.r[18]),
+                   "+r"(f.r[19]), "+r"(f.r[20]), "+r"(f.r[21]), "+r"(f.r[22]), "+r"(f.r[23]), "+r"(f.r[24]),
+                   "+r"(f.r[25]), "+r"(f.r[26]), "+r"(f.r[27]), "+r"(f.r[28]), "+r"(f.r[29]), "+r"(f.r[30]),
+                   "+r"(f.r[31])
+                 :
+                 : "memory");
+}
+
+__global__ void __launch_bounds__(kFm2Threads, 1) flashmatch2_kernel(FmArgs a) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint32_t tmem_slot;
+    __shared__ __align__(8) uint64_t s_full[2], p_full[2], o_full[2][2];
+    __shared__ __align__(8) uint64_t kv_full[kKvStages], kv_empty[kKvStages];
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
+    const uint32_t q0 = blockIdx.x * 2 * kBlockQ, h = blockIdx.y, b = blockIdx.z;
+    FM_STAMP(0);
+    // smem: Q[2] | K ring | V ring | P[2]
+    const uint32_t sQ = smem_addr(smem);
+    const uint32_t sK = sQ + 2 * kTileQK, sV = sK + kKvStages * kTileQK, sP = sV + kKvStages * kTileQK;
+    uint8_t* pP0 = smem + (2 + 2 * kKvStages) * kTileQK;
+    const uint32_t nblk = (a.nkv + kBlockK - 1) / kBlockK;
+
+    if (tid == 0) {
+        for (int t = 0; t < 2; ++t) {
+            mbar_init(&s_full[t], 1);
+            mbar_init(&p_full[t], 4);
+            mbar_init(&o_full[t][0], 1);
+            mbar_init(&o_full[t][1], 1);
+        }
+        for (uint32_t st = 0; st < kKvStages; ++st) {
+            mbar_init(&kv_full[st], 32);  // one cp.async.mbarrier.arrive.noinc per loader lane
+            mbar_init(&kv_empty[st], 1);  // one tcgen05.commit after the block's last PV
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_slot)),
+                     "r"(512u));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+
+    if (warp == 9) {
+        // ---------------- loader
+        const __half* gq = a.q + b * a.q_sb + h * a.q_sh + (uint64_t)q0 * a.q_sn;
+        const __half* gk = a.k + b * a.k_sb + h * a.k_sh;
+        const __half* gv = a.v + b * a.v_sb + h * a.v_sh;
+        const uint32_t qvalid = a.nq - q0;
+        load_tile_warp<false>(sQ, gq, a.q_sn, qvalid);
+        if (qvalid > kBlockQ)
+            load_tile_warp<false>(sQ + kTileQK, gq + (uint64_t)kBlockQ * a.q_sn, a.q_sn, qvalid - kBlockQ);
+        for (uint32_t blk = 0; blk < nblk; ++blk) {
+            const uint32_t st = blk % kKvStages;
+            mbar_wait(&kv_empty[st], ((blk / kKvStages) & 1u) ^ 1u);
+            load_tile_warp<false>(sK + st * kTileQK, gk + (uint64_t)blk * kBlockK * a.k_sn, a.k_sn,
+                                  a.nkv - blk * kBlockK);
+            load_tile_warp<true>(sV + st * kTileQK, gv + (uint64_t)blk * kBlockK * a.v_sn, a.v_sn,
+                                 a.nkv - blk * kBlockK);
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(&kv_full[st]))
+                         : "memory");
+        }
+    } else if (warp == 8) {
+        // ---------------- MMA warp
+        auto kv_ready = [&](uint32_t blk) {
+            mbar_wait(&kv_full[blk % kKvStages], (blk / kKvStages) & 1u);
+            fence_async_smem();
+        };
+        auto issue_s = [&](uint32_t t, uint32_t blk) {
+            tc_fence_after();
+            if (elect_one()) {
+                const uint32_t kb = sK + (blk % kKvStages) * kTileQK, qb = sQ + t * kTileQK;
+#pragma unroll
+                for (uint32_t ks = 0; ks < kHd / 16; ++ks)
+                    tc_mma_f16(tmem + t * 256u, fm_desc(qb + ks * 256u, 128u, 1024u),
+                               fm_desc(kb + ks * 256u, 128u, 1024u), kIdescS, ks > 0 ? 1u : 0u);
+                tc_commit(&s_full[t]);
+            }
+            __syncwarp();
+        };
+        kv_ready(0);  // also covers Q (issued before K0/V0 by the same lanes)
+        issue_s(0, 0);
+        FM_STAMP(1);
+        uint32_t jt[2] = {0, 0};  // next block whose PV each tile needs
+        bool started1 = false;
+        while (jt[0] < nblk || jt[1] < nblk) {
+#pragma unroll
+            for (uint32_t t = 0; t < 2; ++t) {
+                const uint32_t j = jt[t];
+                if (j >= nblk || (t == 1 && !started1)) continue;
+                if (!mbar_test(&p_full[t], j & 1u)) continue;
+                tc_fence_after();
+                // the second tile to finish block j is the last reader of K_j / V_j
+                const bool last_reader = jt[t ^ 1u] > j;
+                if (elect_one()) {
+                    const uint32_t vb = sV + (j % kKvStages) * kTileQK, pb = sP + t * kTileP;
+#pragma unroll
+                    for (uint32_t ks = 0; ks < kBlockK / 16; ++ks)
+                        tc_mma_f16(tmem + t * 256u + 128u + 64u * (j & 1u), fm_desc(pb + ks * 256u, 128u, 2048u),
+                                   fm_desc(vb + ks * 256u, 128u, 2048u), kIdescPV, ks > 0 ? 1u : 0u);
+                    tc_commit(&o_full[t][j & 1u]);
+                    if (last_reader) tc_commit(&kv_empty[j % kKvStages]);
+                }
+                __syncwarp();
+                if (j + 1 < nblk) {
+                    // the tile that reaches block j+1 first waits for its K/V
+                    if (jt[t ^ 1u] <= j + 1) kv_ready(j + 1);
+                    issue_s(t, j + 1);  // softmax t drained S_t(j) before p_full
+                }
+                jt[t] = j + 1;
+                if (t == 0 && !started1) {  // tile 1 starts one softmax behind tile 0
+                    issue_s(1, 0);
+                    started1 = true;
+                }
+                if (t == 0 && lane == 0 && a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 &&
+                    j < 16)
+                    g_fm_trace[40 + j] = clock64();
+            }
+        }
+    } else {
+        // ---------------- softmax warpgroup t
+        const uint32_t t = warp >> 2, row = tid & 127u;
+        const uint32_t lane_base = ((warp & 3u) * 32u) << 16;
+        const uint32_t tbase = tmem + t * 256u;
+        uint8_t* pP = pP0 + t * kTileP;
+        float o[kHd];
+#pragma unroll
+        for (uint32_t i = 0; i < kHd; ++i) o[i] = 0.0f;
+        float m = -INFINITY, l = 0.0f, alpha_prev = 0.0f;
+        const float sl2 = a.scale_log2;
+        auto drain_o = [&](uint32_t jj, float alpha) {
+            Frag g0, g1;
+            const uint32_t ob = tbase + lane_base + 128u + 64u * (jj & 1u);
+            frag_ld(ob, g0);
+            frag_ld(ob + 32u, g1);
+            frag_wait2(g0, g1);
+#pragma unroll
+            for (uint32_t i = 0; i < 32; ++i) {
+                o[i] = fmaf(o[i], alpha, __uint_as_float(g0.r[i]));
+                o[32 + i] = fmaf(o[32 + i], alpha, __uint_as_float(g1.r[i]));
+            }
+        };
+        for (uint32_t j = 0; j < nblk; ++j) {
+            mbar_wait(&s_full[t], j & 1u);
+            if (t == 0) FM_STAMP(3 + j);
+            tc_fence_after();
+            const uint32_t kvalid = a.nkv - j * kBlockK;
+            // pass 1: row max, streamed in 32-column chunks
+            float mx = -INFINITY;
+#pragma unroll
+            for (uint32_t c = 0; c < kBlockK / 32; ++c) {
+                Frag f;
+                frag_ld(tbase + lane_base + c * 32u, f);
+                frag_wait1(f);
+                if (kvalid < kBlockK) {
+#pragma unroll
+                    for (uint32_t i = 0; i < 32; ++i)
+                        if (c * 32u + i >= kvalid) f.r[i] = __float_as_uint(-INFINITY);
+                }
+                float r4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+                for (uint32_t i = 0; i < 32; i += 8)
+#pragma unroll
+                    for (uint32_t u = 0; u < 4; ++u)
+                        r4[u] = max3(r4[u], __uint_as_float(f.r[i + 2 * u]), __uint_as_float(f.r[i + 2 * u + 1]));
+                mx = max3(mx, fmaxf(r4[0], r4[1]), fmaxf(r4[2], r4[3]));
+            }
+            const float m_new = fmaxf(m, mx * sl2);
+            const float alpha = ex2(m - m_new);
+            if (t == 0 && j < 8) FM_STAMP(10 + j);
+            // P_{j-1} / O_{j-1}: PV_t(j-1) must have retired before P is overwritten
+            if (j > 0) {
+                mbar_wait(&o_full[t][(j - 1) & 1u], ((j - 1) >> 1) & 1u);
+                tc_fence_after();
+            }
+            if (t == 0 && j < 8) FM_STAMP(30 + j);
+            // pass 2: exp2, row sum, binary16 P in the UMMA K-major layout
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (uint32_t c = 0; c < kBlockK / 32; ++c) {
+                Frag f;
+                frag_ld(tbase + lane_base + c * 32u, f);
+                frag_wait1(f);
+                if (kvalid < kBlockK) {
+#pragma unroll
+                    for (uint32_t i = 0; i < 32; ++i)
+                        if (c * 32u + i >= kvalid) f.r[i] = __float_as_uint(-INFINITY);
+                }
+#pragma unroll
+                for (uint32_t q = 0; q < 4; ++q) {
+                    float p[8];
+#pragma unroll
+                    for (uint32_t i = 0; i < 8; ++i) p[i] = ex2(fmaf(__uint_as_float(f.r[q * 8 + i]), sl2, -m_new));
+                    acc[q] += ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
+                    uint4 w;
+                    w.x = pack_half2_rn(p[0], p[1]);
+                    w.y = pack_half2_rn(p[2], p[3]);
+                    w.z = pack_half2_rn(p[4], p[5]);
+                    w.w = pack_half2_rn(p[6], p[7]);
+                    *reinterpret_cast<uint4*>(pP + off_p(row, c * 4u + q)) = w;
+                }
+            }
+            tc_fence_before();
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_full[t]);  // P_t(j) written, S_t(j) drained
+            if (t == 0) FM_STAMP(20 + j);
+            if (j > 0) drain_o(j - 1, alpha_prev);
+            l = l * alpha + ((acc[0] + acc[1]) + (acc[2] + acc[3]));
+            m = m_new;
+            alpha_prev = alpha;
+        }
+        mbar_wait(&o_full[t][(nblk - 1) & 1u], ((nblk - 1) >> 1) & 1u);
+        tc_fence_after();
+        drain_o(nblk - 1, alpha_prev);
+        const uint32_t grow = q0 + t * kBlockQ + row;
+        if (grow < a.nq) {
+            const float inv = 1.0f / l;
+            __half* go = a.o + b * a.o_sb + h * a.o_sh + (uint64_t)grow * a.o_sn;
+#pragma unroll
+            for (uint32_t c = 0; c < kHd / 8; ++c) {
+                uint4 w;
+                w.x = pack_half2_rn(o[c * 8 + 0] * inv, o[c * 8 + 1] * inv);
+                w.y = pack_half2_rn(o[c * 8 + 2] * inv, o[c * 8 + 3] * inv);
+                w.z = pack_half2_rn(o[c * 8 + 4] * inv, o[c * 8 + 5] * inv);
+                w.w = pack_half2_rn(o[c * 8 + 6] * inv, o[c * 8 + 7] * inv);
+                *reinterpret_cast<uint4*>(go + c * 8) = w;
+            }
+        }
+    }
+    FM_STAMP(63);
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
+    }
+}
+
 bool fm_attr_done = false;
 
 }  // namespace
@@ -415,6 +708,7 @@ int flashmatch_forward(fnl_context* ctx, const fnl_attention_desc& d) {
     if (d.heads > 65535 || d.batch > 65535) return fail(FNL_EINVAL, "flashmatch: batch/heads exceed 65535");
     if (!fm_attr_done) {
         FNL_CUDA_TRY(cudaFuncSetAttribute(flashmatch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFm));
+        FNL_CUDA_TRY(cudaFuncSetAttribute(flashmatch2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFm2));
         fm_attr_done = true;
     }
     FmArgs a{};
@@ -435,7 +729,14 @@ int flashmatch_forward(fnl_context* ctx, const fnl_attention_desc& d) {
     dim3 grid((d.nq + kBlockQ - 1) / kBlockQ, d.heads, d.batch);
     cudaStream_t s = ctx_stream(ctx);
     ProfScope prof(ctx, FNL_KCLASS_ATTN);
-    flashmatch_kernel<<<grid, kFmThreads, kSmemFm, s>>>(a);
+    // v2 (warp-specialised, two query tiles per CTA) is the product kernel;
+    // FNL_FM_VERSION=1 selects the barrier-synchronous v1 for comparison
+    static const int ver = getenv("FNL_FM_VERSION") ? atoi(getenv("FNL_FM_VERSION")) : 2;
+    if (ver == 1)
+        flashmatch_kernel<<<grid, kFmThreads, kSmemFm, s>>>(a);
+    else
+        flashmatch2_kernel<<<dim3((d.nq + 2 * kBlockQ - 1) / (2 * kBlockQ), d.heads, d.batch), kFm2Threads,
+                             kSmemFm2, s>>>(a);
     FNL_CUDA_TRY(cudaGetLastError());
     ctx_count_launches(ctx, 1);
     return FNL_OK;
