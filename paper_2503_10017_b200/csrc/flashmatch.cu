@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(kFmThreads, 2) flashmatch_kernel(FmArgs a) {
 // twice in 32-column chunks (pass 1 row max; pass 2 exp2, row sum, binary16 P)
 // so S never occupies 128 registers.  160 + 64 KB smem, 512 TMEM columns,
 // one CTA per SM.
-constexpr uint32_t kFm2Threads = 320;
+constexpr uint32_t kFm2Threads = 576;  // 16 softmax warps + MMA warp + load warp
 constexpr uint32_t kKvStages = 3;  // K/V ring depth
 constexpr uint32_t kSmemFm2 = 2 * kTileQK + 2 * kKvStages * kTileQK + 2 * kTileP + 64;
 
@@ -456,6 +456,7 @@ __device__ __forceinline__ void frag_wait1(Frag& f) {
 }
 
 __global__ void __launch_bounds__(kFm2Threads, 1) flashmatch2_kernel(FmArgs a) {
+    __shared__ float red[2][2][2][kBlockQ];  // [tile][block parity][column half][row] partial maxima / sums
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint32_t tmem_slot;
     __shared__ __align__(8) uint64_t s_full[2], p_full[2], o_full[2][2];
@@ -472,7 +473,7 @@ __global__ void __launch_bounds__(kFm2Threads, 1) flashmatch2_kernel(FmArgs a) {
     if (tid == 0) {
         for (int t = 0; t < 2; ++t) {
             mbar_init(&s_full[t], 1);
-            mbar_init(&p_full[t], 4);
+            mbar_init(&p_full[t], 8);  // the tile's 8 softmax warps
             mbar_init(&o_full[t][0], 1);
             mbar_init(&o_full[t][1], 1);
         }
@@ -492,7 +493,7 @@ __global__ void __launch_bounds__(kFm2Threads, 1) flashmatch2_kernel(FmArgs a) {
     tc_fence_after();
     const uint32_t tmem = tmem_slot;
 
-    if (warp == 9) {
+    if (warp == 17) {
         // ---------------- loader
         const __half* gq = a.q + b * a.q_sb + h * a.q_sh + (uint64_t)q0 * a.q_sn;
         const __half* gk = a.k + b * a.k_sb + h * a.k_sh;
@@ -511,7 +512,7 @@ __global__ void __launch_bounds__(kFm2Threads, 1) flashmatch2_kernel(FmArgs a) {
             asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(&kv_full[st]))
                          : "memory");
         }
-    } else if (warp == 8) {
+    } else if (warp == 16) {
         // ---------------- MMA warp
         auto kv_ready = [&](uint32_t blk) {
             mbar_wait(&kv_full[blk % kKvStages], (blk / kKvStages) & 1u);
@@ -569,44 +570,44 @@ __global__ void __launch_bounds__(kFm2Threads, 1) flashmatch2_kernel(FmArgs a) {
             }
         }
     } else {
-        // ---------------- softmax warpgroup t
-        const uint32_t t = warp >> 2, row = tid & 127u;
+        // ---------------- softmax warpgroup t: warps 8t..8t+7; warp w reads TMEM
+        // lane quadrant w%4 and column half hf = (w/4)%2, i.e. two threads per
+        // query row, each owning 64 of the 128 key columns and 32 of the 64
+        // O columns; the row max / row sum halves meet in shared memory
+        const uint32_t t = warp >> 3, hf = (warp >> 2) & 1u, row = ((warp & 3u) << 5) | lane;
         const uint32_t lane_base = ((warp & 3u) * 32u) << 16;
         const uint32_t tbase = tmem + t * 256u;
         uint8_t* pP = pP0 + t * kTileP;
-        float o[kHd];
+        float o[kHd / 2];
 #pragma unroll
-        for (uint32_t i = 0; i < kHd; ++i) o[i] = 0.0f;
+        for (uint32_t i = 0; i < kHd / 2; ++i) o[i] = 0.0f;
         float m = -INFINITY, l = 0.0f, alpha_prev = 0.0f;
         const float sl2 = a.scale_log2;
+        auto tile_sync = [&]() { asm volatile("bar.sync %0, 256;" ::"r"(1u + t) : "memory"); };
         auto drain_o = [&](uint32_t jj, float alpha) {
-            Frag g0, g1;
-            const uint32_t ob = tbase + lane_base + 128u + 64u * (jj & 1u);
-            frag_ld(ob, g0);
-            frag_ld(ob + 32u, g1);
-            frag_wait2(g0, g1);
+            Frag g;
+            frag_ld(tbase + lane_base + 128u + 64u * (jj & 1u) + 32u * hf, g);
+            frag_wait1(g);
 #pragma unroll
-            for (uint32_t i = 0; i < 32; ++i) {
-                o[i] = fmaf(o[i], alpha, __uint_as_float(g0.r[i]));
-                o[32 + i] = fmaf(o[32 + i], alpha, __uint_as_float(g1.r[i]));
-            }
+            for (uint32_t i = 0; i < 32; ++i) o[i] = fmaf(o[i], alpha, __uint_as_float(g.r[i]));
         };
         for (uint32_t j = 0; j < nblk; ++j) {
             mbar_wait(&s_full[t], j & 1u);
             if (t == 0) FM_STAMP(3 + j);
             tc_fence_after();
             const uint32_t kvalid = a.nkv - j * kBlockK;
-            // pass 1: row max, streamed in 32-column chunks
+            // pass 1: partial row max over this thread's 64 columns
             float mx = -INFINITY;
 #pragma unroll
-            for (uint32_t c = 0; c < kBlockK / 32; ++c) {
+            for (uint32_t c = 0; c < 2; ++c) {
+                const uint32_t col0 = hf * 64u + c * 32u;
                 Frag f;
-                frag_ld(tbase + lane_base + c * 32u, f);
+                frag_ld(tbase + lane_base + col0, f);
                 frag_wait1(f);
                 if (kvalid < kBlockK) {
 #pragma unroll
                     for (uint32_t i = 0; i < 32; ++i)
-                        if (c * 32u + i >= kvalid) f.r[i] = __float_as_uint(-INFINITY);
+                        if (col0 + i >= kvalid) f.r[i] = __float_as_uint(-INFINITY);
                 }
                 float r4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
@@ -616,6 +617,9 @@ __global__ void __launch_bounds__(kFm2Threads, 1) flashmatch2_kernel(FmArgs a) {
                         r4[u] = max3(r4[u], __uint_as_float(f.r[i + 2 * u]), __uint_as_float(f.r[i + 2 * u + 1]));
                 mx = max3(mx, fmaxf(r4[0], r4[1]), fmaxf(r4[2], r4[3]));
             }
+            red[t][j & 1u][hf][row] = mx;
+            tile_sync();
+            mx = fmaxf(mx, red[t][j & 1u][hf ^ 1u][row]);
             const float m_new = fmaxf(m, mx * sl2);
             const float alpha = ex2(m - m_new);
             if (t == 0 && j < 8) FM_STAMP(10 + j);
@@ -624,18 +628,18 @@ __global__ void __launch_bounds__(kFm2Threads, 1) flashmatch2_kernel(FmArgs a) {
                 mbar_wait(&o_full[t][(j - 1) & 1u], ((j - 1) >> 1) & 1u);
                 tc_fence_after();
             }
-            if (t == 0 && j < 8) FM_STAMP(30 + j);
-            // pass 2: exp2, row sum, binary16 P in the UMMA K-major layout
+            // pass 2: exp2, partial row sum, binary16 P for this thread's 64 columns
             float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (uint32_t c = 0; c < kBlockK / 32; ++c) {
+            for (uint32_t c = 0; c < 2; ++c) {
+                const uint32_t col0 = hf * 64u + c * 32u;
                 Frag f;
-                frag_ld(tbase + lane_base + c * 32u, f);
+                frag_ld(tbase + lane_base + col0, f);
                 frag_wait1(f);
                 if (kvalid < kBlockK) {
 #pragma unroll
                     for (uint32_t i = 0; i < 32; ++i)
-                        if (c * 32u + i >= kvalid) f.r[i] = __float_as_uint(-INFINITY);
+                        if (col0 + i >= kvalid) f.r[i] = __float_as_uint(-INFINITY);
                 }
 #pragma unroll
                 for (uint32_t q = 0; q < 4; ++q) {
@@ -648,28 +652,31 @@ __global__ void __launch_bounds__(kFm2Threads, 1) flashmatch2_kernel(FmArgs a) {
                     w.y = pack_half2_rn(p[2], p[3]);
                     w.z = pack_half2_rn(p[4], p[5]);
                     w.w = pack_half2_rn(p[6], p[7]);
-                    *reinterpret_cast<uint4*>(pP + off_p(row, c * 4u + q)) = w;
+                    *reinterpret_cast<uint4*>(pP + off_p(row, col0 / 8u + q)) = w;
                 }
             }
             tc_fence_before();
             fence_async_smem();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&p_full[t]);  // P_t(j) written, S_t(j) drained
+            if (lane == 0) mbar_arrive(&p_full[t]);  // this warp's part of P_t(j) written, S drained
             if (t == 0) FM_STAMP(20 + j);
             if (j > 0) drain_o(j - 1, alpha_prev);
-            l = l * alpha + ((acc[0] + acc[1]) + (acc[2] + acc[3]));
+            l = l * alpha + ((acc[0] + acc[1]) + (acc[2] + acc[3]));  // partial: this thread's columns
             m = m_new;
             alpha_prev = alpha;
         }
         mbar_wait(&o_full[t][(nblk - 1) & 1u], ((nblk - 1) >> 1) & 1u);
         tc_fence_after();
         drain_o(nblk - 1, alpha_prev);
+        red[t][nblk & 1u][hf][row] = l;  // the slot of a block that never ran
+        tile_sync();
+        l += red[t][nblk & 1u][hf ^ 1u][row];
         const uint32_t grow = q0 + t * kBlockQ + row;
         if (grow < a.nq) {
             const float inv = 1.0f / l;
-            __half* go = a.o + b * a.o_sb + h * a.o_sh + (uint64_t)grow * a.o_sn;
+            __half* go = a.o + b * a.o_sb + h * a.o_sh + (uint64_t)grow * a.o_sn + hf * 32u;
 #pragma unroll
-            for (uint32_t c = 0; c < kHd / 8; ++c) {
+            for (uint32_t c = 0; c < kHd / 16; ++c) {
                 uint4 w;
                 w.x = pack_half2_rn(o[c * 8 + 0] * inv, o[c * 8 + 1] * inv);
                 w.y = pack_half2_rn(o[c * 8 + 2] * inv, o[c * 8 + 3] * inv);
