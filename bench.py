@@ -141,9 +141,15 @@ def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    ngpu = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    # FNL_BENCH_DIST_BACKEND=gloo (with more ranks than GPUs) is only for
+    # exercising the N>1 code path on a 1-GPU box; timings are then meaningless
+    forced = os.environ.get("FNL_BENCH_DIST_BACKEND")
+    if ngpu:
+        local = local % ngpu
     if world > 1 and not dist.is_initialized():
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
-        if backend == "nccl":
+        backend = forced or ("nccl" if ngpu else "gloo")
+        if ngpu:
             torch.cuda.set_device(local)
         dist.init_process_group(backend=backend)
     return world, rank, local
