@@ -11,7 +11,9 @@
 
 #include <algorithm>
 #include <map>
+#include <condition_variable>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -923,8 +925,20 @@ extern "C" int fnl_reciprocal_match_batch(fnl_context* ctx, uint32_t npairs, con
     const uint32_t samples = ((h + stride - 1) / stride) * ((w + stride - 1) / stride);
     const uint32_t cap = std::max<uint32_t>(samples, 1);
     // Sub-batches double-buffered: the copy engine uploads sub-batch k+1 while
-    // sub-batch k is matched.
-    const uint32_t sub = std::min<uint32_t>(npairs, 16);
+    // sub-batch k is matched.  Sizes ramp 8, 16, 32, 32, ... so the one upload
+    // that nothing overlaps (the first) is short, while later sub-batches are
+    // large enough to amortise the per-call work (measured: 16-pair chunks
+    // 1124 pairs/s, 32-pair 1171, ramp: see bench e2e).
+    static const uint32_t sub_env = getenv("FNL_BATCH_SUB") ? (uint32_t)atoi(getenv("FNL_BATCH_SUB")) : 0;
+    const uint32_t max_sub = std::min<uint32_t>(npairs, sub_env ? sub_env : 32);
+    std::vector<std::pair<uint32_t, uint32_t>> sched;  // (first pair, count)
+    for (uint32_t first = 0, want = sub_env ? max_sub : 8; first < npairs;) {
+        const uint32_t n = std::min(std::min(want, max_sub), npairs - first);
+        sched.push_back({first, n});
+        first += n;
+        want *= 2;
+    }
+    const uint32_t sub = max_sub;
     float* dbuf[2][2];
     TRY(dev_arr(ctx, "mb.d1a", sub * per_map, &dbuf[0][0]));
     TRY(dev_arr(ctx, "mb.d2a", sub * per_map, &dbuf[0][1]));
@@ -939,41 +953,98 @@ extern "C" int fnl_reciprocal_match_batch(fnl_context* ctx, uint32_t npairs, con
         cudaEventCreateWithFlags(&consumed[i], cudaEventDisableTiming);
         cudaEventRecord(consumed[i], ctx->stream);
     }
-    auto upload = [&](uint32_t first, int slot) -> int {
-        const uint32_t n = std::min(sub, npairs - first);
+    auto upload = [&](size_t idx, int slot) -> int {
+        const uint32_t first = sched[idx].first, n = sched[idx].second;
         FNL_CUDA_TRY(cudaStreamWaitEvent(ctx->copy_stream, consumed[slot], 0));
-        FNL_CUDA_TRY(cudaMemcpyAsync(dbuf[slot][0], h_d1 + first * per_map, n * per_map * 4,
-                                     cudaMemcpyHostToDevice, ctx->copy_stream));
-        FNL_CUDA_TRY(cudaMemcpyAsync(dbuf[slot][1], h_d2 + first * per_map, n * per_map * 4,
-                                     cudaMemcpyHostToDevice, ctx->copy_stream));
+        // 32 MB pieces: H2D copies share one copy engine in FIFO order, so a
+        // single 600 MB copy would hold the matcher's small per-pass H2D
+        // transfers (work lists) hostage for ~11 ms (measured with CUPTI)
+        constexpr size_t kPiece = (size_t)32 << 20;
+        for (int m = 0; m < 2; ++m) {
+            const char* src = reinterpret_cast<const char*>((m ? h_d2 : h_d1) + first * per_map);
+            char* dst = reinterpret_cast<char*>(dbuf[slot][m]);
+            const size_t bytes = (size_t)n * per_map * 4;
+            for (size_t off = 0; off < bytes; off += kPiece)
+                FNL_CUDA_TRY(cudaMemcpyAsync(dst + off, src + off, std::min(kPiece, bytes - off),
+                                             cudaMemcpyHostToDevice, ctx->copy_stream));
+        }
         FNL_CUDA_TRY(cudaEventRecord(ready[slot], ctx->copy_stream));
         return FNL_OK;
     };
-    int st = upload(0, 0);
-    for (uint32_t first = 0, k = 0; st == FNL_OK && first < npairs; first += sub, ++k) {
+    // A large pinned H2D cudaMemcpyAsync still blocks the calling host thread
+    // for much of the copy (measured), and run_match drives its loop from the
+    // host, so the uploads run on their own host thread, at most one
+    // sub-batch ahead of the matcher (two device buffers).
+    std::mutex mu;
+    std::condition_variable cv;
+    size_t uploaded = 0, consumed_n = 0;
+    bool abort = false;
+    int up_status = FNL_OK;
+    std::string up_error;
+    const int device = ctx->device;
+    std::thread uploader([&] {
+        cudaSetDevice(device);
+        for (size_t k = 0; k < sched.size(); ++k) {
+            {
+                std::unique_lock<std::mutex> lk(mu);
+                cv.wait(lk, [&] { return abort || k < consumed_n + 2; });
+                if (abort) return;
+            }
+            const int rc = upload(k, (int)(k & 1));
+            std::lock_guard<std::mutex> lk(mu);
+            if (rc != FNL_OK) {
+                up_status = rc;
+                up_error = fnl_last_error();
+                abort = true;
+                cv.notify_all();
+                return;
+            }
+            uploaded = k + 1;
+            cv.notify_all();
+        }
+    });
+    // results come back through pinned staging (a pageable D2H would block)
+    uint32_t* pin_out = nullptr;
+    int st = fnl::ws_pinned(ctx, "mb.out.pin", ((size_t)sub * 3 * cap + sub) * 4, (void**)&pin_out);
+    for (size_t k = 0; st == FNL_OK && k < sched.size(); ++k) {
         const int slot = k & 1;
-        const uint32_t n = std::min(sub, npairs - first);
-        if (first + sub < npairs) {
-            st = upload(first + sub, slot ^ 1);
-            if (st) break;
+        const uint32_t first = sched[k].first, n = sched[k].second;
+        {
+            std::unique_lock<std::mutex> lk(mu);
+            cv.wait(lk, [&] { return abort || uploaded > k; });
+            if (abort) {
+                st = fail(up_status ? up_status : FNL_ERUNTIME, "batch upload: " + up_error);
+                break;
+            }
         }
         cudaStreamWaitEvent(ctx->stream, ready[slot], 0);
         st = run_match(ctx, n, dbuf[slot][0], h, w, dbuf[slot][1], h, w, dim, cfg, backend, dp,
                        dn, stats ? stats + first : nullptr, true);
         if (st) break;
         cudaEventRecord(consumed[slot], ctx->stream);
-        std::vector<uint32_t> cnt(n);
-        cudaMemcpyAsync(cnt.data(), dn, n * 4, cudaMemcpyDeviceToHost, ctx->stream);
-        if (h_pairs)
-            cudaMemcpyAsync(h_pairs + (size_t)first * 3 * cap, dp, (size_t)n * 3 * cap * 4,
-                            cudaMemcpyDeviceToHost, ctx->stream);
+        uint32_t* pin_cnt = pin_out + (size_t)sub * 3 * cap;
+        cudaMemcpyAsync(pin_cnt, dn, n * 4, cudaMemcpyDeviceToHost, ctx->stream);
+        if (h_pairs) cudaMemcpyAsync(pin_out, dp, (size_t)n * 3 * cap * 4, cudaMemcpyDeviceToHost, ctx->stream);
         cudaError_t e = cudaStreamSynchronize(ctx->stream);
         if (e != cudaSuccess) {
             st = fnl::fail_cuda(e, "batch readback", __FILE__, __LINE__);
             break;
         }
-        if (n_pairs) memcpy(n_pairs + first, cnt.data(), n * 4);
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            consumed_n = k + 1;
+            cv.notify_all();
+        }
+        if (h_pairs) memcpy(h_pairs + (size_t)first * 3 * cap, pin_out, (size_t)n * 3 * cap * 4);
+        if (n_pairs) memcpy(n_pairs + first, pin_cnt, n * 4);
     }
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        abort = true;
+        cv.notify_all();
+    }
+    uploader.join();
+    cudaStreamSynchronize(ctx->copy_stream);
     for (int i = 0; i < 2; ++i) {
         cudaEventDestroy(ready[i]);
         cudaEventDestroy(consumed[i]);

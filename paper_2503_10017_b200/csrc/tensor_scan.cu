@@ -858,6 +858,21 @@ uint32_t ceil_div_u(uint32_t a, uint32_t b) { return (a + b - 1) / b; }
         if (_st != FNL_OK) return _st; \
     } while (0)
 
+__global__ void stage_kernel(uint32_t* dst, const uint32_t* src, size_t words) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < words; i += (size_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+// dst (device) <- src (pinned host, mapped), via a kernel on the context stream
+int stage_from_host(fnl_context* ctx, uint32_t* dst, const uint32_t* src, size_t words) {
+    if (words == 0) return FNL_OK;
+    const uint32_t blocks = (uint32_t)std::min<size_t>(64, (words + 255) / 256);
+    stage_kernel<<<blocks, 256, 0, ctx_stream(ctx)>>>(dst, src, words);
+    FNL_CUDA_TRY(cudaGetLastError());
+    ctx_count_launches(ctx, 1);
+    return FNL_OK;
+}
+
 bool attr_done = false;
 
 int ensure_attrs() {
@@ -987,7 +1002,10 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     // items start 16-byte aligned
     const size_t item_off = (2 * (size_t)nslots + 3 * (size_t)ntp + 3) & ~(size_t)3;
     memcpy(w + item_off, items.data(), items.size() * sizeof(TcItem));
-    FNL_CUDA_TRY(cudaMemcpyAsync(dlist, pin, words * 4, cudaMemcpyHostToDevice, s));
+    // staged by a kernel reading the mapped pinned buffer, not by the copy
+    // engine: H2D copies are FIFO on one engine, and during the batch API's
+    // map uploads a cudaMemcpyAsync here would wait behind hundreds of MB
+    TRY(stage_from_host(ctx, dlist, pin, words));
     const uint32_t* d_slot_pair = dlist;
     const uint32_t* d_slot_base = dlist + nslots;
     const uint32_t* d_tp_pair = dlist + 2 * nslots;
@@ -1014,7 +1032,7 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     uint32_t* pin_act = nullptr;
     TRY(ws_pinned(ctx, flip ? "tc.act.pin1" : "tc.act.pin0", npairs * 4, (void**)&pin_act));
     memcpy(pin_act, h_active, npairs * 4);
-    FNL_CUDA_TRY(cudaMemcpyAsync(d_active, pin_act, npairs * 4, cudaMemcpyHostToDevice, s));
+    TRY(stage_from_host(ctx, d_active, pin_act, npairs));
     FNL_CUDA_TRY(cudaMemsetAsync(rcount, 0, 4, s));
     FNL_CUDA_TRY(cudaMemsetAsync(keys, 0xFF, (size_t)rows_total * 8, s));
 
