@@ -415,7 +415,8 @@ __global__ void __launch_bounds__(kFmThreads, 2) flashmatch_kernel(FmArgs a) {
 // twice in 32-column chunks (pass 1 row max; pass 2 exp2, row sum, binary16 P)
 // so S never occupies 128 registers.  160 + 64 KB smem, 512 TMEM columns,
 // one CTA per SM.
-constexpr uint32_t kFm2Threads = 576;  // 16 softmax warps + MMA warp + load warp
+constexpr uint32_t kLoadWarps = 4;      // cp.async issue is the K/V ring's bottleneck with one warp
+constexpr uint32_t kFm2Threads = (16 + 1 + kLoadWarps) * 32;  // softmax warps + MMA warp + load warps
 constexpr uint32_t kKvStages = 3;  // K/V ring depth
 constexpr uint32_t kSmemFm2 = 2 * kTileQK + 2 * kKvStages * kTileQK + 2 * kTileP + 64;
 
@@ -431,10 +432,11 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
 
 // one 128 x 64 tile loaded by ONE warp (32 x 16 B per step, 32 steps)
 template <bool kV>
-__device__ __forceinline__ void load_tile_warp(uint32_t sbase, const __half* g, uint64_t sn, uint32_t nvalid) {
+__device__ __forceinline__ void load_tile_warp(uint32_t sbase, const __half* g, uint64_t sn, uint32_t nvalid,
+                                               uint32_t part = 0, uint32_t parts = 1) {
     const uint32_t lane = threadIdx.x & 31u;
 #pragma unroll 8
-    for (uint32_t combo = 0; combo < 32u; ++combo) {
+    for (uint32_t combo = part; combo < 32u; combo += parts) {
         const uint32_t chunk = (lane >> 3) + 4u * (combo & 1u);
         const uint32_t row = (combo >> 1) * 8u + (lane & 7u);
         const bool valid = row < nvalid;
@@ -478,7 +480,7 @@ __global__ void __launch_bounds__(kFm2Threads, 1) flashmatch2_kernel(FmArgs a) {
             mbar_init(&o_full[t][1], 1);
         }
         for (uint32_t st = 0; st < kKvStages; ++st) {
-            mbar_init(&kv_full[st], 32);  // one cp.async.mbarrier.arrive.noinc per loader lane
+            mbar_init(&kv_full[st], 32 * kLoadWarps);  // one cp.async.mbarrier.arrive.noinc per loader lane
             mbar_init(&kv_empty[st], 1);  // one tcgen05.commit after the block's last PV
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -493,22 +495,24 @@ __global__ void __launch_bounds__(kFm2Threads, 1) flashmatch2_kernel(FmArgs a) {
     tc_fence_after();
     const uint32_t tmem = tmem_slot;
 
-    if (warp == 17) {
+    if (warp >= 17) {
         // ---------------- loader
         const __half* gq = a.q + b * a.q_sb + h * a.q_sh + (uint64_t)q0 * a.q_sn;
         const __half* gk = a.k + b * a.k_sb + h * a.k_sh;
         const __half* gv = a.v + b * a.v_sb + h * a.v_sh;
         const uint32_t qvalid = a.nq - q0;
-        load_tile_warp<false>(sQ, gq, a.q_sn, qvalid);
+        const uint32_t part = warp - 17;
+        load_tile_warp<false>(sQ, gq, a.q_sn, qvalid, part, kLoadWarps);
         if (qvalid > kBlockQ)
-            load_tile_warp<false>(sQ + kTileQK, gq + (uint64_t)kBlockQ * a.q_sn, a.q_sn, qvalid - kBlockQ);
+            load_tile_warp<false>(sQ + kTileQK, gq + (uint64_t)kBlockQ * a.q_sn, a.q_sn, qvalid - kBlockQ, part,
+                                  kLoadWarps);
         for (uint32_t blk = 0; blk < nblk; ++blk) {
             const uint32_t st = blk % kKvStages;
             mbar_wait(&kv_empty[st], ((blk / kKvStages) & 1u) ^ 1u);
             load_tile_warp<false>(sK + st * kTileQK, gk + (uint64_t)blk * kBlockK * a.k_sn, a.k_sn,
-                                  a.nkv - blk * kBlockK);
+                                  a.nkv - blk * kBlockK, part, kLoadWarps);
             load_tile_warp<true>(sV + st * kTileQK, gv + (uint64_t)blk * kBlockK * a.v_sn, a.v_sn,
-                                 a.nkv - blk * kBlockK);
+                                 a.nkv - blk * kBlockK, part, kLoadWarps);
             asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(&kv_full[st]))
                          : "memory");
         }
@@ -541,9 +545,21 @@ __global__ void __launch_bounds__(kFm2Threads, 1) flashmatch2_kernel(FmArgs a) {
                 const uint32_t j = jt[t];
                 if (j >= nblk || (t == 1 && !started1)) continue;
                 if (!mbar_test(&p_full[t], j & 1u)) continue;
+                if (t == 0 && lane == 0 && a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && j < 6)
+                    g_fm_trace[48 + 2 * j] = clock64();
                 tc_fence_after();
                 // the second tile to finish block j is the last reader of K_j / V_j
                 const bool last_reader = jt[t ^ 1u] > j;
+                // S_t(j+1) first: the softmax waits on it, while PV_t(j) is only
+                // needed after the next block's row-max pass
+                if (j + 1 < nblk) {
+                    // the tile that reaches block j+1 first waits for its K/V
+                    if (jt[t ^ 1u] <= j + 1) kv_ready(j + 1);
+                    if (t == 0 && lane == 0 && a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 &&
+                        j < 6)
+                        g_fm_trace[49 + 2 * j] = clock64();
+                    issue_s(t, j + 1);  // softmax t drained S_t(j) before p_full
+                }
                 if (elect_one()) {
                     const uint32_t vb = sV + (j % kKvStages) * kTileQK, pb = sP + t * kTileP;
 #pragma unroll
@@ -554,11 +570,6 @@ __global__ void __launch_bounds__(kFm2Threads, 1) flashmatch2_kernel(FmArgs a) {
                     if (last_reader) tc_commit(&kv_empty[j % kKvStages]);
                 }
                 __syncwarp();
-                if (j + 1 < nblk) {
-                    // the tile that reaches block j+1 first waits for its K/V
-                    if (jt[t ^ 1u] <= j + 1) kv_ready(j + 1);
-                    issue_s(t, j + 1);  // softmax t drained S_t(j) before p_full
-                }
                 jt[t] = j + 1;
                 if (t == 0 && !started1) {  // tile 1 starts one softmax behind tile 0
                     issue_s(1, 0);
