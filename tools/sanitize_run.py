@@ -1,0 +1,29 @@
+"""Small invocations of every kernel family for compute-sanitizer
+(memcheck / racecheck / synccheck): tensor + exact reciprocal matching at C1,
+dense tensor NN, the sharded pass (1 process, no-op reduce), FlashMatch."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import paper_2503_10017_b200 as fnl
+from paper_2503_10017_b200 import _fastnn
+D1 = fnl.gen_random(64, 48, 24, 21)
+D2 = fnl.gen_random(64, 48, 24, 121)
+for be in ("tensor", "single", "hybrid", "double"):
+    m, _ = fnl.reciprocal_match(D1, D2, backend=be, metric="dot")
+    print(be, m.shape[0])
+print("l2", fnl.reciprocal_match(D1, D2, backend="tensor", metric="l2")[0].shape[0])
+r = fnl.nn_tensor(D1, D2, metric="dot")
+print("dense", len(r["nearest"]))
+print("mutual", fnl.mutual_nn_exact(D1, D2, metric="dot").shape[0])
+d1 = torch.from_numpy(D1).cuda(); d2 = torch.from_numpy(D2).cuda()
+S = 48
+keys = torch.empty(S, dtype=torch.int64, device="cuda")
+pairs = torch.empty((1, S, 3), dtype=torch.int32, device="cuda"); cnt = torch.empty(1, dtype=torch.int32, device="cuda")
+for rank in (0, 1):
+    _fastnn.reciprocal_match_sharded_device(d1.data_ptr(), d2.data_ptr(), 1, 64, 48, 24, pairs.data_ptr(),
+                                            cnt.data_ptr(), keys.data_ptr(), S, rank, 2, lambda c: None)
+q = torch.randn((1, 2, 200, 64), device="cuda").half(); k = torch.randn((1, 2, 150, 64), device="cuda").half()
+o = fnl.flashmatch(q, k, k)
+torch.cuda.synchronize()
+print("flashmatch", tuple(o.shape), bool(torch.isfinite(o.float()).all()))
