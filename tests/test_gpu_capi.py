@@ -78,3 +78,20 @@ def test_capi_errors(capi):
     assert rc == 1 and b"non-finite value at flat index 21" in lib.fnl_last_error()
     rc, _, _ = _match(lib, ctx, np.zeros((4, 4, 4), np.float32), np.zeros((4, 4, 4), np.float32), backend=9, metric=0)
     assert rc == 1
+
+
+def test_kernel_profile_classes(fnl):
+    """Per-kernel-class device time (fnl_kernel_profile): every class the
+    tensor matcher launches is timed, and the score class equals
+    fnl_kernel_timing's number."""
+    D1 = fnl.gen_random(128, 96, 24, 5)
+    D2 = fnl.gen_random(128, 96, 24, 6)
+    fnl.kernel_timing(reset=True)
+    fnl.kernel_profile(enable=1, reset=True)
+    fnl.reciprocal_match(D1, D2, backend="tensor", metric="dot")
+    prof = fnl.kernel_profile(enable=0, reset=True)
+    timing = fnl.kernel_timing(reset=True)
+    for cls in ("score", "pack", "gather", "merge", "rescan", "harvest"):
+        assert prof[cls]["launches"] > 0 and prof[cls]["ms"] > 0.0, cls
+    assert prof["score"]["launches"] == timing["score_launches"]
+    assert abs(prof["score"]["ms"] - timing["score_ms"]) < 1e-6
