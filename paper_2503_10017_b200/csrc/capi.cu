@@ -665,11 +665,12 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
         FNL_CUDA_TRY(cudaMemsetAsync(tbad, 0xFF, (size_t)npairs * 16, s));
         TRY(fnl::tensor_pack(ctx, "m.t1", d_d1, npairs, p1, dim, l2, tbad, tsat, &T1));
         TRY(fnl::tensor_pack(ctx, "m.t2", d_d2, npairs, p2, dim, l2, tbad + npairs, tsat + npairs, &T2));
-        // fold the per-pair first bad index into the shared slots (min over pairs)
-        std::vector<unsigned long long> hb(2 * (size_t)npairs);
-        FNL_CUDA_TRY(cudaMemcpyAsync(hb.data(), tbad, hb.size() * 8, cudaMemcpyDeviceToHost, s));
-        FNL_CUDA_TRY(cudaStreamSynchronize(s));
+        // host-buffer entry points validate finiteness like the reference
+        // FeatureMap (a host round trip); the device-resident batch API does not
         if (validate) {
+            std::vector<unsigned long long> hb(2 * (size_t)npairs);
+            FNL_CUDA_TRY(cudaMemcpyAsync(hb.data(), tbad, hb.size() * 8, cudaMemcpyDeviceToHost, s));
+            FNL_CUDA_TRY(cudaStreamSynchronize(s));
             for (uint32_t p = 0; p < npairs; ++p)
                 if (hb[p] != ~0ull) return fail(FNL_EINVAL, nonfinite_msg(hb[p]));
             for (uint32_t p = 0; p < npairs; ++p)

@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(kFmThreads, 2) flashmatch_kernel(FmArgs a) {
 // one CTA per SM.
 constexpr uint32_t kLoadWarps = 4;      // cp.async issue is the K/V ring's bottleneck with one warp
 constexpr uint32_t kFm2Threads = (16 + 1 + kLoadWarps) * 32;  // softmax warps + MMA warp + load warps
-constexpr uint32_t kKvStages = 3;  // K/V ring depth
+constexpr uint32_t kKvStages = 4;  // K/V ring depth
 constexpr uint32_t kSmemFm2 = 2 * kTileQK + 2 * kKvStages * kTileQK + 2 * kTileP + 64;
 
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
@@ -458,7 +458,7 @@ __device__ __forceinline__ void frag_wait1(Frag& f) {
 }
 
 __global__ void __launch_bounds__(kFm2Threads, 1) flashmatch2_kernel(FmArgs a) {
-    __shared__ float red[2][2][2][kBlockQ];  // [tile][block parity][column half][row] partial maxima / sums
+    __shared__ float red[2][2][kBlockQ];  // [tile][column half][row] partial maxima / sums
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint32_t tmem_slot;
     __shared__ __align__(8) uint64_t s_full[2], p_full[2], o_full[2][2];
@@ -628,9 +628,10 @@ __global__ void __launch_bounds__(kFm2Threads, 1) flashmatch2_kernel(FmArgs a) {
                         r4[u] = max3(r4[u], __uint_as_float(f.r[i + 2 * u]), __uint_as_float(f.r[i + 2 * u + 1]));
                 mx = max3(mx, fmaxf(r4[0], r4[1]), fmaxf(r4[2], r4[3]));
             }
-            red[t][j & 1u][hf][row] = mx;
+            red[t][hf][row] = mx;
             tile_sync();
-            mx = fmaxf(mx, red[t][j & 1u][hf ^ 1u][row]);
+            mx = fmaxf(mx, red[t][hf ^ 1u][row]);
+            tile_sync();  // both halves read before either writes the next block's maximum
             const float m_new = fmaxf(m, mx * sl2);
             const float alpha = ex2(m - m_new);
             if (t == 0 && j < 8) FM_STAMP(10 + j);
@@ -679,9 +680,9 @@ __global__ void __launch_bounds__(kFm2Threads, 1) flashmatch2_kernel(FmArgs a) {
         mbar_wait(&o_full[t][(nblk - 1) & 1u], ((nblk - 1) >> 1) & 1u);
         tc_fence_after();
         drain_o(nblk - 1, alpha_prev);
-        red[t][nblk & 1u][hf][row] = l;  // the slot of a block that never ran
+        red[t][hf][row] = l;
         tile_sync();
-        l += red[t][nblk & 1u][hf ^ 1u][row];
+        l += red[t][hf ^ 1u][row];
         const uint32_t grow = q0 + t * kBlockQ + row;
         if (grow < a.nq) {
             const float inv = 1.0f / l;
