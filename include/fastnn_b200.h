@@ -157,6 +157,13 @@ int fnl_mutual_nn(fnl_context* ctx, const float* h_d1, uint32_t h1, uint32_t w1,
                   const float* h_d2, uint32_t h2, uint32_t w2, uint32_t dim, int metric,
                   uint32_t* h_pairs, uint32_t* n_pairs);
 
+/* Dense mutual NN on the tensor cores (binary16 in, fp32 accumulate, certified
+ * exact resolution): equals fnl_mutual_nn on binary16-rounded maps.  Same
+ * arguments and output layout as fnl_mutual_nn. */
+int fnl_mutual_nn_tensor(fnl_context* ctx, const float* h_d1, uint32_t h1, uint32_t w1,
+                         const float* h_d2, uint32_t h2, uint32_t w2, uint32_t dim, int metric,
+                         uint32_t* h_pairs, uint32_t* n_pairs);
+
 /* ---- target-sharded matching (config C5: one oversized pair over N GPUs) -----
  * Every process holds both maps; for each NN pass, shard `rank` of `count`
  * scans only its contiguous range of 128-target tiles of the target map (image

@@ -29,6 +29,7 @@ try:
         kernel_profile,
         kernel_timing,
         mutual_nn_exact,
+        mutual_nn_tensor,
         nn_bruteforce,
         nn_double_loop,
         nn_hybridcast,
@@ -68,6 +69,7 @@ __all__ = [
     "write_fmap",
     # extensions of this build
     "nn_tensor",
+    "mutual_nn_tensor",
     "reciprocal_match_batch",
     "reciprocal_match_device",
     "kernel_timing",

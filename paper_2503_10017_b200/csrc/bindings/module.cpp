@@ -276,6 +276,28 @@ PYBIND11_MODULE(_fastnn, m) {
           },
           py::arg("D1"), py::arg("D2"), py::arg("metric") = "l2");
 
+    m.def("mutual_nn_tensor",
+          [](const F32& D1, const F32& D2, const std::string& metric) {
+              if (D1.ndim() != 3 || D2.ndim() != 3 || D1.shape(2) != D2.shape(2))
+                  throw std::invalid_argument("mutual_nn_tensor: expects (H, W, d) maps with equal d");
+              const auto mt = fastnn::metric_from_string(metric);
+              const std::uint32_t h1 = std::uint32_t(D1.shape(0)), w1 = std::uint32_t(D1.shape(1));
+              std::vector<std::uint32_t> pairs(2 * std::size_t(h1) * w1 + 2);
+              std::uint32_t n = 0;
+              {
+                  py::gil_scoped_release nogil;
+                  fastnn::b200::check(fnl_mutual_nn_tensor(
+                      fastnn::b200::context(), D1.data(), h1, w1, D2.data(), std::uint32_t(D2.shape(0)),
+                      std::uint32_t(D2.shape(1)), std::uint32_t(D1.shape(2)),
+                      mt == fastnn::DistanceMetric::SquaredL2 ? FNL_METRIC_L2 : FNL_METRIC_DOT, pairs.data(), &n));
+              }
+              U32Array out({py::ssize_t(n), py::ssize_t(2)});
+              std::memcpy(out.mutable_data(), pairs.data(), std::size_t(n) * 8);
+              return out;
+          },
+          py::arg("D1"), py::arg("D2"), py::arg("metric") = "l2",
+          "dense mutual NN on the tensor cores; equals mutual_nn_exact on binary16-rounded maps");
+
     // The maps go straight from the numpy buffers to the device (no FeatureMap
     // copy); finiteness is validated on the GPU with the reference's message.
     m.def("reciprocal_match",

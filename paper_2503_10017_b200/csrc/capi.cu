@@ -1053,6 +1053,41 @@ extern "C" int fnl_reciprocal_match_batch(fnl_context* ctx, uint32_t npairs, con
     return st;
 }
 
+// Dense mutual NN on the tensor backend: the K3 scan
+// in both directions plus the mutual filter.  The result equals
+// mutual_nn_exact (src/reciprocal.cpp:82-95) run on binary16-rounded maps.
+extern "C" int fnl_mutual_nn_tensor(fnl_context* ctx, const float* h_d1, uint32_t h1, uint32_t w1,
+                                    const float* h_d2, uint32_t h2, uint32_t w2, uint32_t dim, int metric,
+                                    uint32_t* h_pairs, uint32_t* n_pairs) {
+    TRY(check_device(ctx));
+    if (!valid_metric(metric)) return fail(FNL_EINVAL, "mutual_nn_tensor: bad metric");
+    const uint32_t p1 = h1 * w1, p2 = h2 * w2;
+    if (p1 == 0 || p2 == 0 || dim == 0) return fail(FNL_EINVAL, "mutual_nn_tensor: empty map");
+    const bool l2 = metric == FNL_METRIC_L2;
+    float *d1, *d2;
+    uint32_t *fwd, *bwd, *pairs, *cnt;
+    TRY(dev_arr(ctx, "mt.d1", (size_t)p1 * dim, &d1));
+    TRY(dev_arr(ctx, "mt.d2", (size_t)p2 * dim, &d2));
+    TRY(dev_arr(ctx, "mt.fwd", p1, &fwd));
+    TRY(dev_arr(ctx, "mt.bwd", p2, &bwd));
+    TRY(dev_arr(ctx, "mt.pairs", (size_t)2 * p1 + 2, &pairs));
+    TRY(dev_arr(ctx, "mt.cnt", 1, &cnt));
+    cudaStream_t s = ctx->stream;
+    FNL_CUDA_TRY(cudaMemcpyAsync(d1, h_d1, (size_t)p1 * dim * 4, cudaMemcpyHostToDevice, s));
+    FNL_CUDA_TRY(cudaMemcpyAsync(d2, h_d2, (size_t)p2 * dim * 4, cudaMemcpyHostToDevice, s));
+    TRY(fnl::tensor_nn_dense(ctx, d1, p1, d2, p2, dim, l2, fwd, nullptr));
+    TRY(fnl::tensor_nn_dense(ctx, d2, p2, d1, p1, dim, l2, bwd, nullptr));
+    FNL_CUDA_TRY(fnl::launch_mutual_filter(fwd, bwd, p1, pairs, cnt, s));
+    uint32_t n = 0;
+    FNL_CUDA_TRY(cudaMemcpyAsync(&n, cnt, 4, cudaMemcpyDeviceToHost, s));
+    FNL_CUDA_TRY(cudaStreamSynchronize(s));
+    if (n && h_pairs) FNL_CUDA_TRY(cudaMemcpyAsync(h_pairs, pairs, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+    FNL_CUDA_TRY(cudaStreamSynchronize(s));
+    timing_harvest(ctx);
+    if (n_pairs) *n_pairs = n;
+    return FNL_OK;
+}
+
 // ============================================================== diagnostics
 extern "C" int fnl_tensor_selftest(fnl_context* ctx, const float* h_q, const float* h_t, uint32_t dim,
                                    int metric, int mode, float* h_scores) {

@@ -126,3 +126,27 @@ def test_batch_api_matches_single(fnl, ref):
     for k in range(5):
         m, _ = ref.reciprocal_match(D1[k], D2[k], backend="single", metric="dot")
         assert np.array_equal(pairs_e[k, : counts_e[k]], m)
+
+
+@pytest.mark.parametrize("metric", ["dot", "l2"])
+def test_mutual_nn_tensor_equals_reference_on_half_maps(fnl, ref, metric):
+    """dense mutual NN on the tensor cores equals the
+    reference mutual_nn_exact on binary16-rounded maps (index pairs, order)."""
+    from oracle import oracle
+    D1 = fnl.gen_random(64, 48, 24, 31)
+    D2 = fnl.gen_random(64, 48, 24, 131)
+    got = fnl.mutual_nn_tensor(D1, D2, metric=metric)
+    want = ref.mutual_nn_exact(oracle.half_round_array(D1), oracle.half_round_array(D2), metric=metric)
+    assert np.array_equal(got, np.asarray(want, dtype=np.uint32))
+
+
+@pytest.mark.slow
+def test_mutual_nn_tensor_full_resolution(fnl):
+    """512x384 dense mutual NN (2 x 3.87e10 scores) on the tensor path equals
+    the exact CUDA-core path on binary16-rounded maps."""
+    from oracle import oracle
+    D1 = oracle.half_round_array(fnl.gen_random(512, 384, 24, 606))
+    D2 = oracle.half_round_array(fnl.gen_random(512, 384, 24, 607))
+    got = fnl.mutual_nn_tensor(D1, D2, metric="dot")
+    want = fnl.mutual_nn_exact(D1, D2, metric="dot")
+    assert np.array_equal(got, want)
