@@ -118,7 +118,9 @@ __global__ void __launch_bounds__(kScanThreads) exact_scan_kernel(ScanArgs a, ui
         __syncthreads();
         const float* src = T + (size_t)c0 * dim;
         const uint32_t total = n * dim;
-        if (((reinterpret_cast<uintptr_t>(src) | total) & 3u) == 0) {
+        // float4 staging needs a 16 B aligned source (rows of dim % 4 != 0
+        // floats start at 8 B boundaries) and a whole number of float4s
+        if ((reinterpret_cast<uintptr_t>(src) & 15u) == 0 && (total & 3u) == 0) {
             const float4* s4 = reinterpret_cast<const float4*>(src);
             for (uint32_t i = threadIdx.x; i < total / 4; i += kScanThreads) smem4[i] = __ldg(s4 + i);
         } else {
