@@ -72,3 +72,42 @@ def test_permutation_recovered_at_iteration_one(fnl, seed, backend):
     assert np.array_equal(m[:, 0], samples)
     assert np.array_equal(m[:, 1], inv[m[:, 0]])
     assert (m[:, 2] == 1).all()
+
+
+def _nn_instances(n, seed):
+    rng = np.random.default_rng(seed)
+    for i in range(n):
+        hq, wq = int(rng.integers(1, 40)), int(rng.integers(1, 40))
+        ht, wt = int(rng.integers(1, 60)), int(rng.integers(1, 60))
+        d = int(rng.choice([1, 5, 7, 24, 30, 31, 33, 64]))
+        metric = str(rng.choice(["dot", "l2"]))
+        bs = int(rng.choice([1, 3, 64, 100000]))
+        yield i, (hq, wq, ht, wt, d, metric, bs, 9000 + 2 * i)
+
+
+@pytest.mark.parametrize("i,cfg", list(_nn_instances(60, 3)))
+def test_nn_sweep_all_backends(fnl, ref, i, cfg):
+    """AC1 (tests/acceptance.cpp:47-118): bruteforce == double == single (and
+    hybrid) bitwise on nearest AND min_dist, ragged shapes, odd dims, block
+    sizes from 1 to beyond the map."""
+    hq, wq, ht, wt, d, metric, bs, seed = cfg
+    Q = fnl.gen_random(hq, wq, d, seed)
+    T = fnl.gen_random(ht, wt, d, seed + 1)
+    for name in ("nn_single_loop", "nn_double_loop"):
+        got = getattr(fnl, name)(Q, T, metric=metric, block_size=bs)
+        want = getattr(ref, name)(Q, T, metric=metric, block_size=bs)
+        for key in ("nearest", "min_dist", "a_block_fetches", "b_block_fetches"):
+            assert np.array_equal(np.asarray(got[key]), np.asarray(want[key])), (name, key, cfg)
+    got = fnl.nn_bruteforce(Q, T, metric=metric)
+    want = ref.nn_bruteforce(Q, T, metric=metric)
+    assert np.array_equal(got["nearest"], want["nearest"]) and np.array_equal(got["min_dist"], want["min_dist"])
+    got = fnl.nn_hybridcast(Q, T, metric=metric, block_size=bs)
+    want = ref.nn_hybridcast(Q, T, metric=metric, block_size=bs)
+    for key in ("nearest", "min_dist", "half_saturation_events"):
+        assert np.array_equal(np.asarray(got[key]), np.asarray(want[key])), ("hybrid", key, cfg)
+    if d + (2 if metric == "l2" else 0) <= 32:
+        Qh, Th = oracle.half_round_array(Q), oracle.half_round_array(T)
+        got = fnl.nn_tensor(Qh, Th, metric=metric)
+        want = ref.nn_single_loop(Qh, Th, metric=metric)
+        assert np.array_equal(got["nearest"], want["nearest"]), ("tensor", cfg)
+        assert np.array_equal(got["min_dist"], want["min_dist"]), ("tensor min_dist", cfg)
