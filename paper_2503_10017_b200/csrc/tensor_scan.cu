@@ -183,6 +183,14 @@ __global__ void __launch_bounds__(kPackThreads) pack_kernel(PackArgs a, uint32_t
         const uint64_t left = end - g;
         const uint32_t n = left < (uint64_t)(groups - gi) ? (uint32_t)left : groups - gi;
         uint32_t j = 0;
+        for (; j + 3 < n; j += 4) {  // four row groups (3 KB of fp32) in flight per warp
+            float v[4][8];
+            const uint32_t r0 = (gi + j) * 8 + sub;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) pack_load(a, src, r0 + 8 * q, chunk, v[q]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) nmax = fmaxf(nmax, pack_store(a, dst, pair, r0 + 8 * q, chunk, v[q], sat));
+        }
         for (; j + 1 < n; j += 2) {
             float v0[8], v1[8];
             const uint32_t r0 = (gi + j) * 8 + sub, r1 = r0 + 8;
