@@ -510,8 +510,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
                     }
                     tc_fence_after();
                     const uint32_t taddr = tmem + lane_base + qt * 256u + ch * kSubTile;
-                    frag_ld(taddr + 0, f0);
-                    frag_ld(taddr + 32, f1);
+                    frag_ld64(taddr, f0, f1);
                     frag_wait2(f0, f1);
                     tc_fence_before();
                     __syncwarp();
