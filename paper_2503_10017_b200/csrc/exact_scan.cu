@@ -81,8 +81,13 @@ __device__ __forceinline__ float reg_chain(const QueryRegs<DMAX>& q, const float
     return kL2 ? acc : -acc;
 }
 
-// DMAX > 0: query in registers (dim <= DMAX; kExactDim when dim == DMAX).
+// DMAX > 0: queries in registers (dim <= DMAX; kExactDim when dim == DMAX).
 // DMAX == 0: generic dim, query re-read from global memory (L1 resident).
+// Each thread scores kQB queries (q, q + kScanThreads, ...) against every
+// staged target, so one broadcast shared-memory read of a target channel feeds
+// kQB independent FMA chains (the scan is otherwise bound by LDS issue).
+constexpr int kQB = 2;
+
 template <bool kL2, bool kHyb, int DMAX, bool kExactDim>
 __global__ void __launch_bounds__(kScanThreads) exact_scan_kernel(ScanArgs a, uint32_t chunk) {
     extern __shared__ float4 smem4[];
@@ -90,27 +95,39 @@ __global__ void __launch_bounds__(kScanThreads) exact_scan_kernel(ScanArgs a, ui
     const uint32_t pair = blockIdx.z;
     if (a.pair_done && a.pair_done[pair]) return;
     const uint32_t nq = a.qcount ? a.qcount[pair] : a.qcount_const;
-    if (blockIdx.x * kScanThreads >= nq) return;
+    if (blockIdx.x * kScanThreads * kQB >= nq) return;
     const uint32_t t0 = blockIdx.y * a.split_len;
     if (t0 >= a.nt) return;
     const uint32_t t1 = min(a.nt, t0 + a.split_len);
     const uint32_t dim = a.dim;
 
-    const uint32_t q = blockIdx.x * kScanThreads + threadIdx.x;
-    const bool active = q < nq;
-    uint32_t row = 0;
-    if (active) row = a.qids ? a.qids[(size_t)pair * a.qids_pair_stride + q] : q;
-    const float* qsrc = a.qmap + pair * a.qmap_pair_stride + (size_t)row * dim;
-
-    QueryRegs<(DMAX > 0 ? DMAX : 1)> qr;
-    if constexpr (DMAX > 0) {
+    uint32_t qi[kQB], row[kQB];
+    bool active[kQB];
+    const float* qsrc[kQB];
+    QueryRegs<(DMAX > 0 ? DMAX : 1)> qr[kQB];
 #pragma unroll
-        for (int c = 0; c < DMAX; ++c) qr.v[c] = (active && (kExactDim || (uint32_t)c < dim)) ? qsrc[c] : 0.0f;
+    for (int b = 0; b < kQB; ++b) {
+        qi[b] = blockIdx.x * kScanThreads * kQB + b * kScanThreads + threadIdx.x;
+        active[b] = qi[b] < nq;
+        row[b] = 0;
+        if (active[b]) row[b] = a.qids ? a.qids[(size_t)pair * a.qids_pair_stride + qi[b]] : qi[b];
+        qsrc[b] = a.qmap + pair * a.qmap_pair_stride + (size_t)row[b] * dim;
+        if constexpr (DMAX > 0) {
+#pragma unroll
+            for (int c = 0; c < DMAX; ++c)
+                qr[b].v[c] = (active[b] && (kExactDim || (uint32_t)c < dim)) ? qsrc[b][c] : 0.0f;
+        }
     }
+    const bool any_active = active[0];
 
     const float* T = a.tmap + pair * a.tmap_pair_stride;
-    float best = INFINITY;
-    uint32_t bidx = t0;
+    float best[kQB];
+    uint32_t bidx[kQB];
+#pragma unroll
+    for (int b = 0; b < kQB; ++b) {
+        best[b] = INFINITY;
+        bidx[b] = t0;
+    }
     uint32_t dsat = 0;
 
     for (uint32_t c0 = t0; c0 < t1; c0 += chunk) {
@@ -127,29 +144,42 @@ __global__ void __launch_bounds__(kScanThreads) exact_scan_kernel(ScanArgs a, ui
             for (uint32_t i = threadIdx.x; i < total; i += kScanThreads) tile[i] = __ldg(src + i);
         }
         __syncthreads();
-        if (active) {
-#pragma unroll 4
+        if (any_active) {
+#pragma unroll 2
             for (uint32_t j = 0; j < n; ++j) {
-                float d;
-                if constexpr (DMAX > 0) {
-                    d = reg_chain<kL2, DMAX, kExactDim>(qr, tile + (size_t)j * dim, dim);
-                } else {
-                    d = chain<kL2>(qsrc, tile + (size_t)j * dim, dim);
-                }
-                if constexpr (kHyb) d = half_round_sat(d, dsat);
-                if (d < best) {  // strict: earlier index keeps a tie; NaN never wins
-                    best = d;
-                    bidx = c0 + j;
+                const float* t = tile + (size_t)j * dim;
+#pragma unroll
+                for (int b = 0; b < kQB; ++b) {
+                    float d;
+                    if constexpr (DMAX > 0) {
+                        d = reg_chain<kL2, DMAX, kExactDim>(qr[b], t, dim);
+                    } else {
+                        d = chain<kL2>(qsrc[b], t, dim);
+                    }
+                    if constexpr (kHyb) {
+                        uint32_t sb = 0;
+                        d = half_round_sat(d, sb);
+                        if (active[b]) dsat += sb;
+                    }
+                    if (d < best[b]) {  // strict: earlier index keeps a tie; NaN never wins
+                        best[b] = d;
+                        bidx[b] = c0 + j;
+                    }
                 }
             }
         }
     }
-    if (active) atomicMin(a.keys + (size_t)pair * a.keys_pair_stride + q, pack_key(best, bidx));
+#pragma unroll
+    for (int b = 0; b < kQB; ++b)
+        if (active[b]) atomicMin(a.keys + (size_t)pair * a.keys_pair_stride + qi[b], pack_key(best[b], bidx[b]));
 
     if constexpr (kHyb) {
         uint32_t qsat = 0;
-        if (active && blockIdx.y == 0 && a.q_row_sat)
-            qsat = a.q_row_sat[pair * a.q_row_sat_pair_stride + row];
+        if (blockIdx.y == 0 && a.q_row_sat) {
+#pragma unroll
+            for (int b = 0; b < kQB; ++b)
+                if (active[b]) qsat += a.q_row_sat[pair * a.q_row_sat_pair_stride + row[b]];
+        }
         const uint32_t ws = warp_sum(dsat), wq = warp_sum(qsat);
         if ((threadIdx.x & 31) == 0) {
             if (wq) atomicAdd(a.counters + 2 * pair + 0, (unsigned long long)wq);
@@ -186,7 +216,7 @@ cudaError_t launch_exact_scan(const ScanArgs& a, uint32_t max_q, uint32_t npairs
     uint32_t chunk = 8192u / a.dim;
     chunk = chunk < 1 ? 1 : (chunk > 256 ? 256 : chunk);
     const size_t smem = (size_t)chunk * a.dim * sizeof(float);
-    const uint32_t gx = (max_q + kScanThreads - 1) / kScanThreads;
+    const uint32_t gx = (max_q + kScanThreads * kQB - 1) / (kScanThreads * kQB);
     // Split targets so that the grid covers the machine several times over.
     const uint32_t want_ctas = 148u * 8u;
     uint32_t splits = (want_ctas + gx * npairs - 1) / (gx * npairs);
