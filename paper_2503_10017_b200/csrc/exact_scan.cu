@@ -86,7 +86,7 @@ __device__ __forceinline__ float reg_chain(const QueryRegs<DMAX>& q, const float
 // Each thread scores kQB queries (q, q + kScanThreads, ...) against every
 // staged target, so one broadcast shared-memory read of a target channel feeds
 // kQB independent FMA chains (the scan is otherwise bound by LDS issue).
-constexpr int kQB = 2;
+constexpr int kQB = 4;
 
 template <bool kL2, bool kHyb, int DMAX, bool kExactDim>
 __global__ void __launch_bounds__(kScanThreads) exact_scan_kernel(ScanArgs a, uint32_t chunk) {
