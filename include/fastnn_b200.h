@@ -151,6 +151,18 @@ int fnl_reciprocal_match_batch_device(fnl_context* ctx, uint32_t npairs, const f
                                       uint32_t* d_pairs, uint32_t* d_n_pairs,
                                       fnl_run_stats* h_stats);
 
+/* Confidence-thresholded correspondence compaction (extension; the reference
+ * has no threshold, so it is off unless called): for each of npairs finished
+ * MatchSets in device memory (d_pairs[p*3*cap ..], d_n_pairs[p], as written by
+ * fnl_reciprocal_match_batch_device), keep the matches (i, j, iter) whose
+ * reference distance dist_scalar(D1[i], D2[j]) on the device maps d_d1 / d_d2
+ * (npairs stacked h*w*dim fp32 maps) is <= max_distance, in place and in
+ * emission order.  d_dropped (optional) receives the per-pair drop count. */
+int fnl_confidence_compact_device(fnl_context* ctx, uint32_t npairs, const float* d_d1, const float* d_d2,
+                                  uint32_t h, uint32_t w, uint32_t dim, int metric, float max_distance,
+                                  uint32_t* d_pairs, uint32_t* d_n_pairs, uint32_t cap,
+                                  uint32_t* d_dropped);
+
 /* src/reciprocal.cpp:82-95 mutual_nn_exact (reciprocal.hpp:26): exhaustive
  * mutual NN, full precision, lowest-index ties; h_pairs capacity 2*h1*w1. */
 int fnl_mutual_nn(fnl_context* ctx, const float* h_d1, uint32_t h1, uint32_t w1,

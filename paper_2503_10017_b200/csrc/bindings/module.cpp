@@ -392,7 +392,9 @@ PYBIND11_MODULE(_fastnn, m) {
              std::uint32_t d, std::uintptr_t out_pairs, std::uintptr_t out_counts,
              const std::string& backend, std::uint32_t k, std::uint32_t stride, std::uint32_t max_iters,
              double convergence, const std::string& metric, const std::string& precision,
-             std::uint32_t block_size, py::object stream) {
+             std::uint32_t block_size, py::object stream, py::object max_distance) {
+              const bool conf = !max_distance.is_none();
+              const float max_dist = conf ? max_distance.cast<float>() : 0.0f;
               void* const sh = stream_handle(stream);  // with the GIL held
               const auto cfg = make_cfg(k, stride, max_iters, convergence, metric, precision, block_size);
               cfg.validate();
@@ -403,10 +405,20 @@ PYBIND11_MODULE(_fastnn, m) {
                   py::gil_scoped_release nogil;
                   fnl_context* ctx = fastnn::b200::context();
                   fastnn::b200::check(fnl_context_set_stream(ctx, sh));
-                  const int rc = fnl_reciprocal_match_batch_device(
+                  int rc = fnl_reciprocal_match_batch_device(
                       ctx, n, reinterpret_cast<const float*>(d1), reinterpret_cast<const float*>(d2), h, w, d,
                       &cc, be, reinterpret_cast<std::uint32_t*>(out_pairs),
                       reinterpret_cast<std::uint32_t*>(out_counts), st.data());
+                  if (rc == FNL_OK && conf) {
+                      // confidence-thresholded compaction of the finished MatchSets (extension)
+                      const fastnn::FeatureMap shape(h, w, 1);
+                      const std::uint32_t cap = std::max<std::uint32_t>(
+                          1, std::uint32_t(fastnn::grid_subsample(shape, cfg.k, cfg.grid_stride).size()));
+                      rc = fnl_confidence_compact_device(
+                          ctx, n, reinterpret_cast<const float*>(d1), reinterpret_cast<const float*>(d2), h, w, d,
+                          cc.metric, max_dist, reinterpret_cast<std::uint32_t*>(out_pairs),
+                          reinterpret_cast<std::uint32_t*>(out_counts), cap, nullptr);
+                  }
                   fnl_context_set_stream(ctx, nullptr);
                   fastnn::b200::check(rc);
               }
@@ -418,7 +430,7 @@ PYBIND11_MODULE(_fastnn, m) {
           py::arg("dim"), py::arg("out_pairs"), py::arg("out_counts"), py::arg("backend") = "tensor",
           py::arg("k") = 0, py::arg("stride") = 8, py::arg("max_iters") = 10,
           py::arg("convergence") = 0.99, py::arg("metric") = "dot", py::arg("precision") = "full",
-          py::arg("block_size") = 4096, py::arg("stream") = py::none());
+          py::arg("block_size") = 4096, py::arg("stream") = py::none(), py::arg("max_distance") = py::none());
 
     // Target-sharded matcher (config C5).  `reduce(count)` must MIN-all-reduce
     // the first `count` int64 entries of the caller's key buffer (`keys`, a

@@ -1088,6 +1088,32 @@ extern "C" int fnl_mutual_nn_tensor(fnl_context* ctx, const float* h_d1, uint32_
     return FNL_OK;
 }
 
+extern "C" int fnl_confidence_compact_device(fnl_context* ctx, uint32_t npairs, const float* d_d1,
+                                             const float* d_d2, uint32_t h, uint32_t w, uint32_t dim, int metric,
+                                             float max_distance, uint32_t* d_pairs, uint32_t* d_n_pairs,
+                                             uint32_t cap, uint32_t* d_dropped) {
+    TRY(check_device(ctx));
+    if (!valid_metric(metric)) return fail(FNL_EINVAL, "confidence_compact: bad metric");
+    if (npairs == 0) return FNL_OK;
+    if (!d_d1 || !d_d2 || !d_pairs || !d_n_pairs || dim == 0 || cap == 0)
+        return fail(FNL_EINVAL, "confidence_compact: null buffer or empty shape");
+    fnl::ConfArgs a{};
+    a.d1 = d_d1;
+    a.d2 = d_d2;
+    a.map1_stride = a.map2_stride = (uint64_t)h * w * dim;
+    a.dim = dim;
+    a.l2 = metric == FNL_METRIC_L2;
+    a.max_dist = max_distance;
+    a.pairs = d_pairs;
+    a.n_pairs = d_n_pairs;
+    a.cap = cap;
+    a.dropped = d_dropped;
+    fnl::ProfScope prof(ctx, FNL_KCLASS_HARVEST);
+    FNL_CUDA_TRY(fnl::launch_confidence_compact(a, npairs, ctx->stream));
+    ctx->total_launches += 1;
+    return FNL_OK;
+}
+
 // ============================================================== diagnostics
 extern "C" int fnl_tensor_selftest(fnl_context* ctx, const float* h_q, const float* h_t, uint32_t dim,
                                    int metric, int mode, float* h_scores) {

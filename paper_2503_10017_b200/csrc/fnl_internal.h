@@ -139,6 +139,21 @@ constexpr int kStatWords = 4 + 64;
 cudaError_t launch_match_init(const MatchState& m, cudaStream_t s);
 cudaError_t launch_harvest(const MatchState& m, uint32_t iteration, cudaStream_t s);
 
+// confidence-thresholded compaction of finished MatchSets (in place, stable)
+struct ConfArgs {
+    const float* d1;
+    const float* d2;
+    uint64_t map1_stride, map2_stride;  // floats between consecutive pairs' maps
+    uint32_t dim;
+    bool l2;
+    float max_dist;
+    uint32_t* pairs;      // [npairs][3*cap]
+    uint32_t* n_pairs;    // [npairs], updated
+    uint32_t cap;
+    uint32_t* dropped;    // [npairs] or null
+};
+cudaError_t launch_confidence_compact(const ConfArgs& a, uint32_t npairs, cudaStream_t s);
+
 // exhaustive mutual filter: i kept iff bwd[fwd[i]] == i, in ascending i
 cudaError_t launch_mutual_filter(const uint32_t* fwd, const uint32_t* bwd, uint32_t n,
                                  uint32_t* pairs, uint32_t* count, cudaStream_t s);

@@ -188,6 +188,57 @@ __global__ void expand_pairs_kernel(const uint32_t* idx, const uint32_t* count, 
     }
 }
 
+// Confidence-thresholded correspondence compaction (north-star extension; the
+// reference has no threshold): per pair, keep the matches (i, j, iter) whose
+// reference distance dist_scalar(D1[i], D2[j]) (src/kernels.cpp:277-285, the
+// FMA chain in channel order on the maps as given) is <= max_dist.  Keep
+// flags are counted per warp with ballot/popc and the warp offsets are scanned
+// in warp order, so the compaction is in place and stable (the MatchSet keeps
+// the reference emission order).
+__global__ void __launch_bounds__(kHarvestThreads) confidence_compact_kernel(ConfArgs a) {
+    __shared__ uint32_t warp_tot[33];
+    const uint32_t p = blockIdx.x;
+    const uint32_t n = a.n_pairs[p];
+    uint32_t* P = a.pairs + (size_t)p * 3 * a.cap;
+    const float* D1 = a.d1 + (size_t)p * a.map1_stride;
+    const float* D2 = a.d2 + (size_t)p * a.map2_stride;
+    uint32_t kept = 0;
+    for (uint32_t c0 = 0; c0 < n; c0 += kHarvestThreads) {
+        const uint32_t s = c0 + threadIdx.x;
+        const bool valid = s < n;
+        uint32_t i = 0, j = 0, it = 0;
+        bool keep = false;
+        if (valid) {
+            i = P[3 * s];
+            j = P[3 * s + 1];
+            it = P[3 * s + 2];
+            const float d = a.l2 ? chain<true>(D1 + (size_t)i * a.dim, D2 + (size_t)j * a.dim, a.dim)
+                                 : chain<false>(D1 + (size_t)i * a.dim, D2 + (size_t)j * a.dim, a.dim);
+            keep = d <= a.max_dist;  // NaN is never kept
+        }
+        uint32_t nk;
+        const uint32_t pos = block_scan(keep ? 1u : 0u, warp_tot, nk);
+        if (keep) {  // kept + pos <= s: every source entry of this chunk is already in registers
+            uint32_t* o = P + 3 * (kept + pos);
+            o[0] = i;
+            o[1] = j;
+            o[2] = it;
+        }
+        kept += nk;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        a.n_pairs[p] = kept;
+        if (a.dropped) a.dropped[p] = n - kept;
+    }
+}
+
+cudaError_t launch_confidence_compact(const ConfArgs& a, uint32_t npairs, cudaStream_t s) {
+    if (npairs == 0) return cudaSuccess;
+    confidence_compact_kernel<<<npairs, kHarvestThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_mutual_filter(const uint32_t* fwd, const uint32_t* bwd, uint32_t n,
                                  uint32_t* pairs, uint32_t* count, cudaStream_t s) {
     // pairs doubles as scratch: selected indices land in its upper half first.

@@ -150,3 +150,34 @@ def test_mutual_nn_tensor_full_resolution(fnl):
     got = fnl.mutual_nn_tensor(D1, D2, metric="dot")
     want = fnl.mutual_nn_exact(D1, D2, metric="dot")
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("metric", ["dot", "l2"])
+def test_confidence_compaction_equals_post_filter(fnl, ref, metric):
+    """Confidence-thresholded compaction (fnl_confidence_compact_device): the
+    kept matches are exactly the unthresholded MatchSet filtered by the
+    reference dist_scalar <= threshold, in emission order."""
+    import torch
+    B, H, W, D = 3, 96, 64, 24
+    maps1 = [fnl.gen_random(H, W, D, 70 + p) for p in range(B)]
+    maps2 = [fnl.gen_random(H, W, D, 170 + p) for p in range(B)]
+    d1 = torch.from_numpy(np.stack(maps1)).cuda()
+    d2 = torch.from_numpy(np.stack(maps2)).cuda()
+    S = len(fnl.grid_subsample(H, W, stride=8))
+    out = torch.zeros((B, S, 3), dtype=torch.int32, device="cuda")
+    cnt = torch.zeros((B,), dtype=torch.int32, device="cuda")
+
+    def run(**kw):
+        fnl.reciprocal_match_device(d1.data_ptr(), d2.data_ptr(), B, H, W, D, out.data_ptr(), cnt.data_ptr(),
+                                    backend="tensor", stride=8, metric=metric, **kw)
+        torch.cuda.synchronize()
+        return [out[p, :int(cnt[p])].cpu().numpy().astype(np.uint32) for p in range(B)]
+
+    full = run()
+    dists = [np.array([ref.dist_scalar(maps1[p].reshape(-1, D)[i], maps2[p].reshape(-1, D)[j], metric=metric)
+                       for i, j, _ in full[p]], dtype=np.float32) for p in range(B)]
+    thr = float(np.median(np.concatenate(dists)))
+    kept = run(max_distance=thr)
+    for p in range(B):
+        assert np.array_equal(kept[p], full[p][dists[p] <= np.float32(thr)])
+    assert 0 < sum(len(k) for k in kept) < sum(len(f) for f in full)
