@@ -317,8 +317,9 @@ constexpr uint32_t kBTileBytes = kBTileRows * kPackRowBytes;  // 16 KB
 constexpr int kStages = 4;
 // warps: 0 loader, 1-2 MMA issuers (query tile 0 / 1), 3..18 epilogue
 // (column quarter = (w-3)/4, TMEM lane quadrant = w%4)
-constexpr int kEpiColSplit = 4;  // 64-target sub-tiles per 256-target tile, one epilogue warp each
-constexpr int kEpiWarps = 4 * kEpiColSplit;
+constexpr uint32_t kSubPerTile = 4;  // 64-target sub-tiles per 256-target tile
+constexpr int kPartialSplit = 2;     // partial states per (work unit, row): one per 128-column half
+constexpr int kEpiWarps = 16;
 constexpr int kFirstEpiWarp = 3;
 constexpr int kScanThreads = (kFirstEpiWarp + kEpiWarps) * 32;
 constexpr uint32_t kSmemA = 2 * kTileBytes;                  // 16 KB: two query tiles
@@ -409,7 +410,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
         }
         for (int q = 0; q < 2; ++q) {
             mbar_init(&tfull[q], 1);
-            mbar_init(&accfree[q], kEpiWarps);
+            mbar_init(&accfree[q], kEpiWarps / 2);  // the eight warps of that query tile
             mbar_init(&afull[q], 1);
             mbar_init(&afree[q], 2);  // both MMA issuers
         }
@@ -484,52 +485,67 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
             __syncwarp();
         }
     } else {
-        // ---------------- epilogue: 16 warps = (64-column quarter ch, TMEM lane
-        // quadrant w%4); every warp drains both query tiles' buffers, keeping
-        // one running top-3 state per query tile
-        const uint32_t e = warp - kFirstEpiWarp, ch = e >> 2, quad = warp & 3u;
+        // ---------------- epilogue: 16 warps; warps 3..10 drain query tile 0,
+        // warps 11..18 query tile 1 (warp = (query tile, 128-column half h,
+        // TMEM lane quadrant w%4)), so while one tile's warps load, the other
+        // tile's warps compare.  Per tile a warp loads its two 64-target
+        // sub-tiles one after the other (the first is reduced before the
+        // second is loaded, keeping 64 fragment registers), then releases.
+        const uint32_t e = warp - kFirstEpiWarp, quad = warp & 3u;
+        const uint32_t qt = e >> 3, h = (e >> 2) & 1u;
         const uint32_t lane_base = (quad * 32u) << 16;
         uint32_t k = 0;
         Frag f0, f1;
         for (uint32_t u = blockIdx.x; u < a.nitems; u += G) {
             const TcItem item = a.items[u];
-            RowState st[2];
-#pragma unroll
-            for (int q = 0; q < 2; ++q) st[q] = RowState{-INFINITY, -INFINITY, -INFINITY, 0xFFFFFFFFu, 0xFFFFFFFFu};
+            RowState st{-INFINITY, -INFINITY, -INFINITY, 0xFFFFFFFFu, 0xFFFFFFFFu};
+            const bool warp_real = qt * 128u + quad * 32u < item.nvalid;  // else all rows padding
             for (uint32_t t = item.tile_begin; t < item.tile_end; ++t, ++k) {
-#pragma unroll
-                for (uint32_t qt = 0; qt < 2; ++qt) {
-                    const bool warp_real = qt * 128u + quad * 32u < item.nvalid;  // else all rows padding
-                    mbar_wait(&tfull[qt], k & 1u);
-                    const bool tw = trace && qt == 0 && warp == kFirstEpiWarp && k < 4096;
-                    if (tw && lane == 0) a.trace[12288 + k] = clock64();
-                    if (!warp_real || (a.debug & 1)) {  // nothing to score: hand the buffer straight back
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&accfree[qt]);
-                        continue;
-                    }
-                    tc_fence_after();
-                    const uint32_t taddr = tmem + lane_base + qt * 256u + ch * kSubTile;
-                    frag_ld64(taddr, f0, f1);
-                    frag_wait2(f0, f1);
-                    tc_fence_before();
+                mbar_wait(&tfull[qt], k & 1u);
+                const bool tw = trace && warp == kFirstEpiWarp && k < 4096;
+                if (tw && lane == 0) a.trace[12288 + k] = clock64();
+                if (!warp_real || (a.debug & 1)) {  // nothing to score: hand the buffer straight back
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&accfree[qt]);  // this warp's columns drained
-                    if (tw && lane == 0) a.trace[16384 + k] = clock64();
-                    subtile_scan(st[qt], f0, f1, t * kEpiColSplit + ch, a.nt);
-                    if (tw) {
-                        __syncwarp();
-                        if (lane == 0) a.trace[20480 + k] = clock64() + (st[qt].b1 > 1e30f ? 1 : 0);
+                    if (lane == 0) mbar_arrive(&accfree[qt]);
+                    continue;
+                }
+                tc_fence_after();
+                const uint32_t taddr = tmem + lane_base + qt * 256u + h * 128u;
+                const uint32_t sub0 = t * kSubPerTile + 2u * h;
+                frag_ld64(taddr, f0, f1);
+                frag_wait2(f0, f1);
+                float m0;
+                {
+                    float v[64];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        v[j] = __uint_as_float(f0.r[j]);
+                        v[32 + j] = __uint_as_float(f1.r[j]);
                     }
+                    if ((sub0 + 1) * kSubTile > a.nt) {
+#pragma unroll
+                        for (int j = 0; j < 64; ++j)
+                            if (sub0 * kSubTile + j >= a.nt) v[j] = -INFINITY;
+                    }
+                    m0 = tile_max64(v);
+                }
+                frag_ld64(taddr + 64u, f0, f1);
+                frag_wait2(f0, f1);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&accfree[qt]);  // this warp's 128 columns drained
+                if (tw && lane == 0) a.trace[16384 + k] = clock64();
+                if (__any_sync(0xFFFFFFFFu, m0 > st.b3)) tile_update(st, m0, sub0);
+                subtile_scan(st, f0, f1, sub0 + 1, a.nt);
+                if (tw) {
+                    __syncwarp();
+                    if (lane == 0) a.trace[20480 + k] = clock64() + (st.b1 > 1e30f ? 1 : 0);
                 }
             }
-#pragma unroll
-            for (uint32_t qt = 0; qt < 2; ++qt) {
-                const uint32_t row = qt * 128u + quad * 32u + lane;  // 0..255 within the tile pair
-                float4* po = a.partial + (((uint64_t)u * kEpiColSplit + ch) * kQueryTilePair + row) * 2;
-                po[0] = make_float4(st[qt].b1, st[qt].b2, st[qt].b3, __uint_as_float(st[qt].t1));
-                po[1] = make_float4(__uint_as_float(st[qt].t2), 0.0f, 0.0f, 0.0f);
-            }
+            const uint32_t row = qt * 128u + quad * 32u + lane;  // 0..255 within the tile pair
+            float4* po = a.partial + (((uint64_t)u * kPartialSplit + h) * kQueryTilePair + row) * 2;
+            po[0] = make_float4(st.b1, st.b2, st.b3, __uint_as_float(st.t1));
+            po[1] = make_float4(__uint_as_float(st.t2), 0.0f, 0.0f, 0.0f);
         }
     }
     tc_fence_before();
@@ -600,8 +616,8 @@ __global__ void __launch_bounds__(kQueryTilePair) merge_kernel(MergeArgs a) {
                 B3 = fmaxf(B3, v);
             }
         };
-        for (uint32_t s = 0; s < a.splits * kEpiColSplit; ++s) {
-            const float4* pp = a.partial + (((uint64_t)tp * a.splits * kEpiColSplit + s) * kQueryTilePair + r) * 2;
+        for (uint32_t s = 0; s < a.splits * kPartialSplit; ++s) {
+            const float4* pp = a.partial + (((uint64_t)tp * a.splits * kPartialSplit + s) * kQueryTilePair + r) * 2;
             const float4 p = pp[0];
             const float4 p2 = pp[1];
             insert(p.x, __float_as_uint(p.w));
@@ -1034,7 +1050,7 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     uint32_t* d_active;
     TRY(ws_arr(ctx, "tc.qbuf", (size_t)rows_total * kPackRowBytes, &qbuf));
     TRY(ws_arr(ctx, "tc.margin", rows_total, &margin));
-    TRY(ws_arr(ctx, "tc.partial", (size_t)nitems * kEpiColSplit * kQueryTilePair * 2, &partial));
+    TRY(ws_arr(ctx, "tc.partial", (size_t)nitems * kPartialSplit * kQueryTilePair * 2, &partial));
     TRY(ws_arr(ctx, "tc.rescan", (size_t)3 * rows_total, &rescan));
     TRY(ws_arr(ctx, "tc.rcount", 1, &rcount));
     TRY(ws_arr(ctx, "tc.keys", rows_total, &keys));
