@@ -58,7 +58,6 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
 }
 // kind::f16 instruction descriptor: A/B fp16, D fp32, both K-major, M=128, N=128.
 constexpr uint32_t kIdescF16M128N128 = (1u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
-constexpr uint32_t kIdescF16M128N256 = (1u << 4) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
 
 __host__ __device__ __forceinline__ uint64_t packed_offset(uint32_t row, uint32_t chunk) {
     return (uint64_t)(row >> 3) * 512u + chunk * 128u + (row & 7u) * 16u;
@@ -324,7 +323,7 @@ constexpr int kFirstEpiWarp = 3;
 constexpr int kScanThreads = (kFirstEpiWarp + kEpiWarps) * 32;
 constexpr uint32_t kSmemA = 2 * kTileBytes;                  // 16 KB: two query tiles
 constexpr uint32_t kSmemB = kStages * kBTileBytes;           // 64 KB ring
-constexpr uint32_t kSmemBars = (2 * kStages + 4 + 2 + 2) * 8;
+constexpr uint32_t kSmemBars = (2 * kStages + 8 + 2 + 2) * 8;
 // A double buffered (next unit's queries load under the current unit); padded
 // past half the SM's shared memory so no second CTA co-resides and spins in
 // tcgen05.alloc for the 512 TMEM columns.
@@ -394,9 +393,9 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kSmemA + kSmemB);
     uint64_t* full = bars;                     // [kStages]  B tile landed
     uint64_t* empty = bars + kStages;          // [kStages]  both query tiles' MMAs on the slot retired
-    uint64_t* tfull = bars + 2 * kStages;      // [2]  accumulator of query tile qt ready
-    uint64_t* accfree = tfull + 2;             // [2]  accumulator of query tile qt drained
-    uint64_t* afull = accfree + 2;             // [2]
+    uint64_t* tfull = bars + 2 * kStages;      // [2 qt][2 halves]  accumulator half ready
+    uint64_t* accfree = tfull + 4;             // [2 qt][2 halves]  accumulator half drained
+    uint64_t* afull = accfree + 4;             // [2]
     uint64_t* afree = afull + 2;               // [2]
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -408,9 +407,11 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 2);  // one commit per issuer
         }
-        for (int q = 0; q < 2; ++q) {
+        for (int q = 0; q < 4; ++q) {
             mbar_init(&tfull[q], 1);
-            mbar_init(&accfree[q], kEpiWarps / 2);  // the eight warps of that query tile
+            mbar_init(&accfree[q], kEpiWarps / 4);  // the four warps of that query tile and half
+        }
+        for (int q = 0; q < 2; ++q) {
             mbar_init(&afull[q], 1);
             mbar_init(&afree[q], 2);  // both MMA issuers
         }
@@ -468,18 +469,25 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
                 const uint32_t s = k % kStages;
                 if (trace && qt == 0 && lane == 0 && k < 4096) a.trace[4096 + k] = clock64();
                 mbar_wait(&full[s], (k / kStages) & 1u);
-                mbar_wait(&accfree[qt], (k & 1u) ^ 1u);
-                if (trace && qt == 0 && lane == 0 && k < 4096) a.trace[8192 + k] = clock64();
-                tc_fence_after();
-                if (elect_one()) {
-                    const uint64_t bd = umma_desc(b_addr + s * kBTileBytes);
-                    // K-step 1 starts 256 B (two 8-channel chunks) further: +16 in descriptor units
-                    tc_mma_f16(d, ad, bd, kIdescF16M128N256, 0u);
-                    tc_mma_f16(d, ad + 16u, bd + 16u, kIdescF16M128N256, 1u);
-                    tc_commit(&tfull[qt]);
-                    tc_commit(&empty[s]);
+                const uint64_t bd = umma_desc(b_addr + s * kBTileBytes);
+#pragma unroll
+                for (uint32_t h = 0; h < 2; ++h) {
+                    // each 128-target half of the tile is its own accumulator chain,
+                    // refilled as soon as its four epilogue warps drained it
+                    mbar_wait(&accfree[qt * 2 + h], (k & 1u) ^ 1u);
+                    if (trace && qt == 0 && h == 0 && lane == 0 && k < 4096) a.trace[8192 + k] = clock64();
+                    tc_fence_after();
+                    if (elect_one()) {
+                        // half h starts 16 row groups (8 KB) further; K-step 1 starts 256 B
+                        // (two 8-channel chunks) further: +16 in descriptor units
+                        const uint64_t bh = bd + (uint64_t)h * (8192u >> 4);
+                        tc_mma_f16(d + h * 128u, ad, bh, kIdescF16M128N128, 0u);
+                        tc_mma_f16(d + h * 128u, ad + 16u, bh + 16u, kIdescF16M128N128, 1u);
+                        tc_commit(&tfull[qt * 2 + h]);
+                        if (h == 1) tc_commit(&empty[s]);
+                    }
+                    __syncwarp();
                 }
-                __syncwarp();
             }
             if (elect_one()) tc_commit(&afree[ab]);  // this issuer no longer reads this unit's query tile
             __syncwarp();
@@ -501,12 +509,12 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
             RowState st{-INFINITY, -INFINITY, -INFINITY, 0xFFFFFFFFu, 0xFFFFFFFFu};
             const bool warp_real = qt * 128u + quad * 32u < item.nvalid;  // else all rows padding
             for (uint32_t t = item.tile_begin; t < item.tile_end; ++t, ++k) {
-                mbar_wait(&tfull[qt], k & 1u);
+                mbar_wait(&tfull[qt * 2 + h], k & 1u);
                 const bool tw = trace && warp == kFirstEpiWarp && k < 4096;
                 if (tw && lane == 0) a.trace[12288 + k] = clock64();
                 if (!warp_real || (a.debug & 1)) {  // nothing to score: hand the buffer straight back
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&accfree[qt]);
+                    if (lane == 0) mbar_arrive(&accfree[qt * 2 + h]);
                     continue;
                 }
                 tc_fence_after();
@@ -533,7 +541,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
                 frag_wait2(f0, f1);
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&accfree[qt]);  // this warp's 128 columns drained
+                if (lane == 0) mbar_arrive(&accfree[qt * 2 + h]);  // this warp's 128 columns drained
                 if (tw && lane == 0) a.trace[16384 + k] = clock64();
                 if (__any_sync(0xFFFFFFFFu, m0 > st.b3)) tile_update(st, m0, sub0);
                 subtile_scan(st, f0, f1, sub0 + 1, a.nt);
