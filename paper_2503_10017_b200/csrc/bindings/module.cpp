@@ -392,7 +392,7 @@ PYBIND11_MODULE(_fastnn, m) {
              std::uint32_t d, std::uintptr_t out_pairs, std::uintptr_t out_counts,
              const std::string& backend, std::uint32_t k, std::uint32_t stride, std::uint32_t max_iters,
              double convergence, const std::string& metric, const std::string& precision,
-             std::uint32_t block_size, py::object stream, py::object max_distance) {
+             std::uint32_t block_size, py::object stream, py::object max_distance, bool with_stats) {
               const bool conf = !max_distance.is_none();
               const float max_dist = conf ? max_distance.cast<float>() : 0.0f;
               void* const sh = stream_handle(stream);  // with the GIL held
@@ -408,7 +408,7 @@ PYBIND11_MODULE(_fastnn, m) {
                   int rc = fnl_reciprocal_match_batch_device(
                       ctx, n, reinterpret_cast<const float*>(d1), reinterpret_cast<const float*>(d2), h, w, d,
                       &cc, be, reinterpret_cast<std::uint32_t*>(out_pairs),
-                      reinterpret_cast<std::uint32_t*>(out_counts), st.data());
+                      reinterpret_cast<std::uint32_t*>(out_counts), with_stats ? st.data() : nullptr);
                   if (rc == FNL_OK && conf) {
                       // confidence-thresholded compaction of the finished MatchSets (extension)
                       const fastnn::FeatureMap shape(h, w, 1);
@@ -423,14 +423,16 @@ PYBIND11_MODULE(_fastnn, m) {
                   fastnn::b200::check(rc);
               }
               py::list stats;
-              for (const auto& s : st) stats.append(stats_dict(s));
+              if (with_stats)
+                  for (const auto& s : st) stats.append(stats_dict(s));
               return stats;
           },
           py::arg("d1"), py::arg("d2"), py::arg("npairs"), py::arg("height"), py::arg("width"),
           py::arg("dim"), py::arg("out_pairs"), py::arg("out_counts"), py::arg("backend") = "tensor",
           py::arg("k") = 0, py::arg("stride") = 8, py::arg("max_iters") = 10,
           py::arg("convergence") = 0.99, py::arg("metric") = "dot", py::arg("precision") = "full",
-          py::arg("block_size") = 4096, py::arg("stream") = py::none(), py::arg("max_distance") = py::none());
+          py::arg("block_size") = 4096, py::arg("stream") = py::none(), py::arg("max_distance") = py::none(),
+          py::arg("with_stats") = true);
 
     // Target-sharded matcher (config C5).  `reduce(count)` must MIN-all-reduce
     // the first `count` int64 entries of the caller's key buffer (`keys`, a

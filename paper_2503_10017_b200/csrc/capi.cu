@@ -136,25 +136,31 @@ void timing_end(fnl_context* ctx, cudaEvent_t b, int cls = FNL_KCLASS_SCORE) {
     if (b) cudaEventRecord(b, ctx->stream);
 }
 void timing_harvest(fnl_context* ctx) {
-    // caller has synchronised the stream
+    // consumes the marks whose end event has completed (all of them when the
+    // caller synchronised the stream); later marks wait for the next harvest
+    size_t done = 0;
     for (auto& m : ctx->ev_used) {
+        if (cudaEventQuery(m.b) != cudaSuccess) break;
         float ms = 0.0f;
         if (cudaEventElapsedTime(&ms, m.a, m.b) == cudaSuccess) {
             if (m.cls == FNL_KCLASS_SCORE) ctx->score_ms += ms;
             ctx->class_ms[m.cls] += ms;
         }
         ctx->ev_free.push_back({m.a, m.b});
+        ++done;
     }
-    ctx->ev_used.clear();
+    ctx->ev_used.erase(ctx->ev_used.begin(), ctx->ev_used.begin() + done);
 }
 
 // Phase timers for the RunReport *_us fields (device time, microseconds).
 struct PhaseTimer {
     fnl_context* ctx;
+    bool enabled = true;  // off when the caller asked for no stats (no event churn)
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
     cudaEvent_t open = nullptr;
     int open_phase = -1;
     void begin(int phase) {
+        if (!enabled) return;
         cudaEvent_t e;
         cudaEventCreate(&e);
         cudaEventRecord(e, ctx->stream);
@@ -162,6 +168,7 @@ struct PhaseTimer {
         open_phase = phase;
     }
     void end() {
+        if (!enabled) return;
         cudaEvent_t e;
         cudaEventCreate(&e);
         cudaEventRecord(e, ctx->stream);
@@ -690,6 +697,7 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
         if (hb[1] != ~0ull) return fail(FNL_EINVAL, nonfinite_msg(hb[1] % ((uint64_t)p2 * dim)));
     }
     PhaseTimer timer{ctx};
+    timer.enabled = h_stats != nullptr;
     timer.begin(kPhaseSubsample);
     {
         fnl::ProfScope prof(ctx, FNL_KCLASS_HARVEST);
