@@ -66,6 +66,7 @@ struct fnl_context {
     uint64_t score_launches = 0, total_launches = 0;
     double class_ms[FNL_KCLASS_COUNT] = {};
     uint64_t class_launches[FNL_KCLASS_COUNT] = {};
+    cudaEvent_t lag[2] = {nullptr, nullptr};  // lagged convergence check of the reciprocal loop
 };
 
 namespace {
@@ -76,6 +77,13 @@ int check_device(fnl_context* ctx) {
     if (!ctx) return fail(FNL_EINVAL, "fastnn_b200: null context");
     cudaError_t e = cudaSetDevice(ctx->device);
     if (e != cudaSuccess) return fnl::fail_cuda(e, "cudaSetDevice", __FILE__, __LINE__);
+    return FNL_OK;
+}
+
+int lag_events(fnl_context* ctx, cudaEvent_t** out) {
+    for (auto& e : ctx->lag)
+        if (!e) FNL_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    *out = ctx->lag;
     return FNL_OK;
 }
 
@@ -369,6 +377,8 @@ extern "C" int fnl_context_destroy(fnl_context* ctx) {
     for (auto& kv : ctx->pinned) cudaFreeHost(kv.second.p);
     for (auto& m : ctx->ev_used) { cudaEventDestroy(m.a); cudaEventDestroy(m.b); }
     for (auto& ev : ctx->ev_free) { cudaEventDestroy(ev.first); cudaEventDestroy(ev.second); }
+    for (auto& e : ctx->lag)
+        if (e) cudaEventDestroy(e);
     cudaStreamDestroy(ctx->own_stream);
     cudaStreamDestroy(ctx->copy_stream);
     delete ctx;
@@ -707,9 +717,6 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
 
     // ---- NN pass helper: queries = rows of qmap at ids, targets = tmap
     uint32_t call = 0;
-    // host mirror of the per-pair active counts / done flags (tensor work lists)
-    std::vector<uint32_t> h_active(npairs, samples);
-    std::vector<uint8_t> h_done(npairs, samples == 0 ? 1 : 0);
     auto nn_pass = [&](const Prepared& Q, uint32_t qrows, const uint32_t* ids, const Prepared& Tm,
                        uint32_t nt, uint32_t* out) -> int {
         if (tensor) {
@@ -717,8 +724,8 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
             const fnl::PackedMaps& TT = (qrows == p1 && ids == m.active_u) ? T2 : T1;
             ++call;
             if (!sharded)
-                return fnl::tensor_nn_pass(ctx, npairs, TQ, ids, cap, h_active.data(), h_done.data(), TT, dim,
-                                           l2, out, cap, nullptr, near_ties);
+                return fnl::tensor_nn_pass(ctx, npairs, TQ, ids, cap, m.n_active, m.done, TT, dim, l2, out, cap,
+                                           nullptr, near_ties);
             // target shard of this rank: contiguous 128-target tiles
             const uint64_t tiles = ceil_div(nt, fnl::kTargetTileRows);
             const uint32_t tb = (uint32_t)(tiles * shard->rank / shard->count);
@@ -726,8 +733,8 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
             const uint64_t nkeys = (uint64_t)npairs * cap;
             TRY(fnl::tensor_shard_reset(ctx, reinterpret_cast<long long*>(shard->d_keys), nkeys));
             if (te > tb)
-                TRY(fnl::tensor_nn_pass(ctx, npairs, TQ, ids, cap, h_active.data(), h_done.data(), TT, dim, l2,
-                                        out, cap, nullptr, near_ties, tb, te,
+                TRY(fnl::tensor_nn_pass(ctx, npairs, TQ, ids, cap, m.n_active, m.done, TT, dim, l2, out, cap,
+                                        nullptr, near_ties, tb, te,
                                         reinterpret_cast<long long*>(shard->d_keys)));
             if (shard->reduce(shard->user, shard->d_keys, nkeys, ctx->stream) != 0)
                 return fail(FNL_ERUNTIME, "sharded reciprocal_match: key reduction callback failed");
@@ -762,6 +769,12 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
         return exact_nn(ctx, sa, cap, npairs, l2, hyb, fa);
     };
 
+    unsigned int* lag_done = nullptr;  // pinned [2]: n_done after iterations t-1, t
+    cudaEvent_t* lag_ev = nullptr;
+    if (tensor) {
+        TRY(fnl::ws_pinned(ctx, "m.lagdone", 8, (void**)&lag_done));
+        TRY(lag_events(ctx, &lag_ev));
+    }
     if (samples > 0) {
         timer.begin(kPhaseForward);
         TRY(nn_pass(P1, p1, m.active_u, P2, p2, m.active_v));
@@ -778,14 +791,25 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
         }
         timer.end();
         ctx->total_launches += 1;
-        unsigned int ndone = 0;
-        FNL_CUDA_TRY(cudaMemcpyAsync(&ndone, m.n_done, 4, cudaMemcpyDeviceToHost, s));
         if (tensor) {
-            FNL_CUDA_TRY(cudaMemcpyAsync(h_active.data(), m.n_active, npairs * 4, cudaMemcpyDeviceToHost, s));
-            FNL_CUDA_TRY(cudaMemcpyAsync(h_done.data(), m.done, npairs, cudaMemcpyDeviceToHost, s));
+            // Lagged convergence check: iteration t is enqueued before the
+            // host looks at the done count of iteration t-1, so the GPU never
+            // idles on the round trip.  Passes enqueued after the last pair
+            // finished skip every pair on the device (done flags) and change
+            // nothing; every rank of a sharded run sees the same counts, so
+            // the collectives stay matched.
+            FNL_CUDA_TRY(cudaMemcpyAsync(lag_done + (t & 1), m.n_done, 4, cudaMemcpyDeviceToHost, s));
+            FNL_CUDA_TRY(cudaEventRecord(lag_ev[t & 1], s));
+            if (t >= 2) {
+                FNL_CUDA_TRY(cudaEventSynchronize(lag_ev[(t - 1) & 1]));
+                if (lag_done[(t - 1) & 1] >= npairs) break;
+            }
+        } else {
+            unsigned int ndone = 0;
+            FNL_CUDA_TRY(cudaMemcpyAsync(&ndone, m.n_done, 4, cudaMemcpyDeviceToHost, s));
+            FNL_CUDA_TRY(cudaStreamSynchronize(s));
+            if (ndone >= npairs) break;
         }
-        FNL_CUDA_TRY(cudaStreamSynchronize(s));
-        if (ndone >= npairs) break;
         timer.begin(kPhaseForward);
         TRY(nn_pass(P1, p1, m.active_u, P2, p2, m.active_v));
         timer.end();

@@ -224,10 +224,12 @@ struct GatherArgs {
     const float* tmax;    // per pair max target norm
     uint32_t dim;
     bool l2;
+    const uint32_t* nslots;  // device slot count (plan header), or null = gridDim.y
 };
 
 __global__ void gather_kernel(GatherArgs a) {
     const uint32_t slot = blockIdx.y;
+    if (a.nslots && slot >= *a.nslots) return;
     const uint32_t pair = a.slot_pair[slot];
     const uint32_t n = a.n_active[pair];
     const uint32_t npad = (n + kQueryTilePair - 1) / kQueryTilePair * kQueryTilePair;
@@ -294,7 +296,7 @@ struct TcArgs {
     uint64_t t_pair_bytes;
     uint32_t nt;
     const TcItem* items;
-    uint32_t nitems;
+    const uint32_t* nitems;  // device item count (plan header)
     float4* partial;  // [item][col half][256][2] = (b1, b2, b3, t1 bits), (t2 bits, 0, 0, 0)
     int debug;        // profiling only: 1 = epilogue releases buffers unread, 16 = clock trace of CTA 0
     unsigned long long* trace;  // [4][4096] clock64 stamps (debug & 16)
@@ -401,6 +403,8 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t G = gridDim.x;
     const bool trace = (a.debug & 16) && blockIdx.x == 0;
+    const uint32_t nitems = *a.nitems;
+    if (blockIdx.x >= nitems) return;  // CTA-uniform, before any barrier or TMEM allocation
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -430,7 +434,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
     if (warp == 0) {
         // ---------------- loader: query tile pair per unit, then the target ring
         uint32_t k = 0, i = 0;
-        for (uint32_t u = blockIdx.x; u < a.nitems; u += G, ++i) {
+        for (uint32_t u = blockIdx.x; u < nitems; u += G, ++i) {
             const TcItem item = a.items[u];
             const uint32_t ab = i & 1u;
             mbar_wait(&afree[ab], ((i >> 1) & 1u) ^ 1u);
@@ -459,7 +463,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
         const uint32_t b_addr = smem_addr(sB);
         const uint32_t d = tmem + qt * 256u;
         uint32_t k = 0, i = 0;
-        for (uint32_t u = blockIdx.x; u < a.nitems; u += G, ++i) {
+        for (uint32_t u = blockIdx.x; u < nitems; u += G, ++i) {
             const uint32_t nt_unit = a.items[u].tile_end - a.items[u].tile_begin;
             const uint32_t ab = i & 1u;
             mbar_wait(&afull[ab], (i >> 1) & 1u);
@@ -504,7 +508,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
         const uint32_t lane_base = (quad * 32u) << 16;
         uint32_t k = 0;
         Frag f0, f1;
-        for (uint32_t u = blockIdx.x; u < a.nitems; u += G) {
+        for (uint32_t u = blockIdx.x; u < nitems; u += G) {
             const TcItem item = a.items[u];
             RowState st{-INFINITY, -INFINITY, -INFINITY, 0xFFFFFFFFu, 0xFFFFFFFFu};
             const bool warp_real = qt * 128u + quad * 32u < item.nvalid;  // else all rows padding
@@ -570,7 +574,7 @@ struct MergeArgs {
     const uint32_t* tp_pair;   // tile pair -> pair
     const uint32_t* tp_row0;   // tile pair -> first gathered row
     const uint32_t* tp_qi0;    // tile pair -> first query index within the pair
-    uint32_t splits;
+    const uint32_t* hdr;       // plan header: [1] tile pairs, [3] target splits
     const uint32_t* n_active;
     const float* margin;
     const uint8_t* qbuf;
@@ -600,6 +604,8 @@ __global__ void __launch_bounds__(kQueryTilePair) merge_kernel(MergeArgs a) {
     __shared__ uint32_t s_t[kQueryTilePair][2];  // candidate sub-tiles; t[1] = ~0 when one suffices
     __shared__ uint32_t s_go[kQueryTilePair];    // 1 = resolve here
     const uint32_t tp = blockIdx.x, r = threadIdx.x;
+    if (tp >= a.hdr[1]) return;
+    const uint32_t splits = a.hdr[3];
     const uint32_t pair = a.tp_pair[tp];
     const uint32_t nrows = min(kQueryTilePair, a.n_active[pair] - a.tp_qi0[tp]);
     const uint32_t row0 = a.tp_row0[tp];
@@ -624,8 +630,8 @@ __global__ void __launch_bounds__(kQueryTilePair) merge_kernel(MergeArgs a) {
                 B3 = fmaxf(B3, v);
             }
         };
-        for (uint32_t s = 0; s < a.splits * kPartialSplit; ++s) {
-            const float4* pp = a.partial + (((uint64_t)tp * a.splits * kPartialSplit + s) * kQueryTilePair + r) * 2;
+        for (uint32_t s = 0; s < splits * kPartialSplit; ++s) {
+            const float4* pp = a.partial + (((uint64_t)tp * splits * kPartialSplit + s) * kQueryTilePair + r) * 2;
             const float4 p = pp[0];
             const float4 p2 = pp[1];
             insert(p.x, __float_as_uint(p.w));
@@ -938,6 +944,113 @@ static bool debug_mode_trace_dump(fnl_context* ctx, cudaStream_t s) {
     return true;
 }
 
+// ---------------------------------------------------------------- K2p plan
+// One block builds the pass's work lists from the DEVICE per-pair state
+// (n_active, done), so the reciprocal loop never waits on the host between
+// passes: gather slots (one per live pair), 256-query tile pairs, the target
+// split count (the modelled makespan of the persistent K3 grid: waves x
+// (tiles per unit + switch cost)) and the K3 work units.  Consumers read the
+// counts from the header and early-exit past them (grids are upper bounds).
+struct PlanArgs {
+    uint32_t npairs;
+    const uint32_t* n_active;
+    const uint8_t* done;  // may be null
+    uint32_t tile_begin, ntiles;
+    uint32_t sms;
+    uint32_t nitems_cap;
+    uint32_t* hdr;  // [0] slots [1] tile pairs [2] items [3] splits [4] tiles per split
+    uint32_t* slot_pair;
+    uint32_t* slot_base;
+    uint32_t* tp_pair;
+    uint32_t* tp_row0;
+    uint32_t* tp_qi0;
+    TcItem* items;
+};
+
+constexpr int kPlanThreads = 1024;
+
+__global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a) {
+    __shared__ uint32_t s_warp[2][32];
+    __shared__ uint32_t s_carry[2];
+    __shared__ uint32_t s_split[2];
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_carry[0] = s_carry[1] = 0;
+    __syncthreads();
+    for (uint32_t base = 0; base < a.npairs; base += kPlanThreads) {
+        const uint32_t p = base + tid;
+        uint32_t act = p < a.npairs ? a.n_active[p] : 0u;
+        if (p < a.npairs && a.done && a.done[p]) act = 0;
+        const uint32_t has = act ? 1u : 0u;
+        const uint32_t ntp = (act + kQueryTilePair - 1) / kQueryTilePair;
+        // block exclusive scan of (has, ntp)
+        uint32_t ih = has, it = ntp;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t h = __shfl_up_sync(0xffffffffu, ih, o), t = __shfl_up_sync(0xffffffffu, it, o);
+            if (lane >= (uint32_t)o) ih += h, it += t;
+        }
+        if (lane == 31) s_warp[0][warp] = ih, s_warp[1][warp] = it;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t wh = s_warp[0][lane], wt = s_warp[1][lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t h = __shfl_up_sync(0xffffffffu, wh, o), t = __shfl_up_sync(0xffffffffu, wt, o);
+                if (lane >= (uint32_t)o) wh += h, wt += t;
+            }
+            s_warp[0][lane] = wh - s_warp[0][lane];  // exclusive warp offsets
+            s_warp[1][lane] = wt - s_warp[1][lane];
+        }
+        __syncthreads();
+        const uint32_t slot = s_carry[0] + s_warp[0][warp] + ih - has;
+        const uint32_t tp0 = s_carry[1] + s_warp[1][warp] + it - ntp;
+        if (has) {
+            a.slot_pair[slot] = p;
+            a.slot_base[slot] = tp0 * kQueryTilePair;
+            for (uint32_t j = 0; j < ntp; ++j) {
+                a.tp_pair[tp0 + j] = p;
+                a.tp_row0[tp0 + j] = (tp0 + j) * kQueryTilePair;
+                a.tp_qi0[tp0 + j] = j * kQueryTilePair;
+            }
+        }
+        __syncthreads();
+        if (tid == kPlanThreads - 1) s_carry[0] = slot + has, s_carry[1] = tp0 + ntp;
+        __syncthreads();
+    }
+    const uint32_t nslots = s_carry[0], ntp = s_carry[1];
+    if (tid == 0) {
+        uint32_t best = 1;
+        float best_cost = 3.0e38f;
+        const uint32_t smax = min(min(a.ntiles, 64u), ntp ? max(1u, a.nitems_cap / ntp) : 1u);
+        for (uint32_t sp = 1; sp <= smax; ++sp) {
+            const float waves = (float)((ntp * sp + a.sms - 1) / a.sms);
+            const float cost = waves * (float)((a.ntiles + sp - 1) / sp + 3u);
+            if (cost < best_cost) best_cost = cost, best = sp;
+        }
+        const uint32_t per = (a.ntiles + best - 1) / best;
+        const uint32_t splits = (a.ntiles + per - 1) / per;
+        s_split[0] = splits;
+        s_split[1] = per;
+        a.hdr[0] = nslots;
+        a.hdr[1] = ntp;
+        a.hdr[2] = ntp * splits;
+        a.hdr[3] = splits;
+        a.hdr[4] = per;
+    }
+    __syncthreads();
+    const uint32_t splits = s_split[0], per = s_split[1];
+    for (uint32_t u = tid; u < ntp * splits; u += kPlanThreads) {
+        const uint32_t j = u / splits, sp = u - j * splits;
+        const uint32_t pair = a.tp_pair[j], qi0 = a.tp_qi0[j];
+        TcItem it;
+        it.pair = pair;
+        it.qrow0 = a.tp_row0[j];
+        it.tile_begin = a.tile_begin + sp * per;
+        it.tile_end = a.tile_begin + min(a.ntiles, (sp + 1) * per);
+        it.nvalid = min(kQueryTilePair, a.n_active[pair] - qi0);
+        it.pad0 = it.pad1 = it.pad2 = 0;
+        a.items[u] = it;
+    }
+}
+
 // ====================================================================== host
 int tensor_pack(fnl_context* ctx, const char* tag, const float* d_src, uint32_t npairs, uint32_t rows,
                 uint32_t dim, bool l2, unsigned long long* d_bad, unsigned long long* d_sat, PackedMaps* out) {
@@ -967,7 +1080,7 @@ int tensor_pack(fnl_context* ctx, const char* tag, const float* d_src, uint32_t 
 }
 
 int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const uint32_t* ids, uint32_t cap,
-                   const uint32_t* h_active, const uint8_t* h_done, const PackedMaps& T, uint32_t dim, bool l2,
+                   const uint32_t* d_active, const uint8_t* d_done, const PackedMaps& T, uint32_t dim, bool l2,
                    uint32_t* out, uint32_t out_stride, float* min_dist, unsigned long long* d_near_ties,
                    uint32_t tile_begin, uint32_t tile_end, long long* shard_keys) {
     TRY(ensure_attrs());
@@ -976,77 +1089,28 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     const uint32_t all_tiles = ceil_div_u(nt, kBTileRows);
     if (tile_end == 0 || tile_end > all_tiles) tile_end = all_tiles;
     if (tile_begin >= tile_end) return fail(FNL_EINVAL, "tensor_nn_pass: empty target tile range");
+    if (npairs == 0 || cap == 0) return FNL_OK;
     const uint32_t ntiles = tile_end - tile_begin;  // tiles of this shard
-
-    // ---- host work list: gather slots (one per active pair) and tile pairs
-    std::vector<uint32_t> slot_pair, slot_base, tp_pair, tp_row0, tp_qi0;
-    uint32_t rows_total = 0;
-    for (uint32_t p = 0; p < npairs; ++p) {
-        if (h_active[p] == 0 || (h_done && h_done[p])) continue;
-        slot_pair.push_back(p);
-        slot_base.push_back(rows_total);
-        const uint32_t ntp = ceil_div_u(h_active[p], kQueryTilePair);
-        for (uint32_t j = 0; j < ntp; ++j) {
-            tp_pair.push_back(p);
-            tp_row0.push_back(rows_total + j * kQueryTilePair);
-            tp_qi0.push_back(j * kQueryTilePair);
-        }
-        rows_total += ntp * kQueryTilePair;
-    }
-    if (slot_pair.empty()) return FNL_OK;
-    const uint32_t ntp = (uint32_t)tp_pair.size();
-    // Target splits: pick the split count that minimises the modelled makespan
-    // of the persistent grid (units per CTA x (tiles per unit + switch cost)).
     const uint32_t sms = (uint32_t)ctx_sm_count(ctx);
-    uint32_t best_s = 1;
-    double best_cost = 1e300;
-    for (uint32_t sp = 1; sp <= std::min<uint32_t>(ntiles, 64); ++sp) {
-        const double waves = std::ceil((double)ntp * sp / sms);
-        const double cost = waves * (std::ceil((double)ntiles / sp) + 3.0);
-        if (cost < best_cost - 1e-9) {
-            best_cost = cost;
-            best_s = sp;
-        }
-    }
-    const uint32_t per = ceil_div_u(ntiles, best_s);
-    const uint32_t splits = ceil_div_u(ntiles, per);
-    std::vector<TcItem> items;
-    items.reserve((size_t)ntp * splits);
-    for (uint32_t j = 0; j < ntp; ++j)
-        for (uint32_t sp = 0; sp < splits; ++sp)
-            items.push_back({tp_pair[j], tp_row0[j], tile_begin + sp * per, tile_begin + std::min(ntiles, (sp + 1) * per),
-                             std::min<uint32_t>(kQueryTilePair, h_active[tp_pair[j]] - tp_qi0[j]), 0, 0, 0});
-    const uint32_t nitems = (uint32_t)items.size();
-    const uint32_t nslots = (uint32_t)slot_pair.size();
 
-    // ---- stage the lists (pinned, alternating halves so an in-flight copy of
-    // the previous pass is never overwritten)
-    static thread_local int flip = 0;
-    flip ^= 1;
-    const size_t words = 2 * (size_t)nslots + 3 * (size_t)ntp + 8 * (size_t)nitems + 4;
-    uint32_t* pin = nullptr;
+    // ---- upper bounds: every pair live with all `cap` queries.  The actual
+    // lists are built on the device (K2p) from n_active / done, so no pass
+    // waits for the host.
+    const uint32_t tp_per_pair = ceil_div_u(cap, kQueryTilePair);
+    const uint32_t tp_max = npairs * tp_per_pair;
+    const uint32_t rows_max = tp_max * kQueryTilePair;
+    const uint32_t nitems_cap = std::max<uint32_t>(2 * tp_max, std::min<uint32_t>(64 * tp_max, 64 * sms));
+    const size_t item_off = (8 + 2 * (size_t)npairs + 3 * (size_t)tp_max + 3) & ~(size_t)3;
+    const size_t words = item_off + 8 * (size_t)nitems_cap;
     uint32_t* dlist = nullptr;
-    TRY(ws_pinned(ctx, flip ? "tc.list.pin1" : "tc.list.pin0", words * 4, (void**)&pin));
-    TRY(ws_arr(ctx, flip ? "tc.list1" : "tc.list0", words, &dlist));
-    uint32_t* w = pin;
-    std::copy(slot_pair.begin(), slot_pair.end(), w);
-    std::copy(slot_base.begin(), slot_base.end(), w + nslots);
-    std::copy(tp_pair.begin(), tp_pair.end(), w + 2 * nslots);
-    std::copy(tp_row0.begin(), tp_row0.end(), w + 2 * nslots + ntp);
-    std::copy(tp_qi0.begin(), tp_qi0.end(), w + 2 * nslots + 2 * ntp);
-    // items start 16-byte aligned
-    const size_t item_off = (2 * (size_t)nslots + 3 * (size_t)ntp + 3) & ~(size_t)3;
-    memcpy(w + item_off, items.data(), items.size() * sizeof(TcItem));
-    // staged by a kernel reading the mapped pinned buffer, not by the copy
-    // engine: H2D copies are FIFO on one engine, and during the batch API's
-    // map uploads a cudaMemcpyAsync here would wait behind hundreds of MB
-    TRY(stage_from_host(ctx, dlist, pin, words));
-    const uint32_t* d_slot_pair = dlist;
-    const uint32_t* d_slot_base = dlist + nslots;
-    const uint32_t* d_tp_pair = dlist + 2 * nslots;
-    const uint32_t* d_tp_row0 = d_tp_pair + ntp;
-    const uint32_t* d_tp_qi0 = d_tp_row0 + ntp;
-    const TcItem* d_items = reinterpret_cast<const TcItem*>(dlist + item_off);
+    TRY(ws_arr(ctx, "tc.plan", words, &dlist));
+    uint32_t* d_hdr = dlist;
+    uint32_t* d_slot_pair = dlist + 8;
+    uint32_t* d_slot_base = d_slot_pair + npairs;
+    uint32_t* d_tp_pair = d_slot_base + npairs;
+    uint32_t* d_tp_row0 = d_tp_pair + tp_max;
+    uint32_t* d_tp_qi0 = d_tp_row0 + tp_max;
+    TcItem* d_items = reinterpret_cast<TcItem*>(dlist + item_off);
 
     // ---- device scratch
     uint8_t* qbuf;
@@ -1055,29 +1119,28 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     uint32_t* rescan;
     unsigned int* rcount;
     unsigned long long* keys;
-    uint32_t* d_active;
-    TRY(ws_arr(ctx, "tc.qbuf", (size_t)rows_total * kPackRowBytes, &qbuf));
-    TRY(ws_arr(ctx, "tc.margin", rows_total, &margin));
-    TRY(ws_arr(ctx, "tc.partial", (size_t)nitems * kPartialSplit * kQueryTilePair * 2, &partial));
-    TRY(ws_arr(ctx, "tc.rescan", (size_t)3 * rows_total, &rescan));
+    TRY(ws_arr(ctx, "tc.qbuf", (size_t)rows_max * kPackRowBytes, &qbuf));
+    TRY(ws_arr(ctx, "tc.margin", rows_max, &margin));
+    TRY(ws_arr(ctx, "tc.partial", (size_t)nitems_cap * kPartialSplit * kQueryTilePair * 2, &partial));
+    TRY(ws_arr(ctx, "tc.rescan", (size_t)3 * rows_max, &rescan));
     TRY(ws_arr(ctx, "tc.rcount", 1, &rcount));
-    TRY(ws_arr(ctx, "tc.keys", rows_total, &keys));
-    TRY(ws_arr(ctx, "tc.active", npairs, &d_active));
-    // active counts as the host saw them (the pass must use exactly these)
-    uint32_t* pin_act = nullptr;
-    TRY(ws_pinned(ctx, flip ? "tc.act.pin1" : "tc.act.pin0", npairs * 4, (void**)&pin_act));
-    memcpy(pin_act, h_active, npairs * 4);
-    TRY(stage_from_host(ctx, d_active, pin_act, npairs));
+    TRY(ws_arr(ctx, "tc.keys", rows_max, &keys));
     FNL_CUDA_TRY(cudaMemsetAsync(rcount, 0, 4, s));
-    FNL_CUDA_TRY(cudaMemsetAsync(keys, 0xFF, (size_t)rows_total * 8, s));
+    FNL_CUDA_TRY(cudaMemsetAsync(keys, 0xFF, (size_t)rows_max * 8, s));
 
+    // ---- K2p plan
+    {
+        PlanArgs pa{npairs, d_active, d_done, tile_begin, ntiles, sms, nitems_cap, d_hdr,
+                    d_slot_pair, d_slot_base, d_tp_pair, d_tp_row0, d_tp_qi0, d_items};
+        ProfScope prof(ctx, FNL_KCLASS_GATHER);
+        plan_kernel<<<1, kPlanThreads, 0, s>>>(pa);
+        FNL_CUDA_TRY(cudaGetLastError());
+    }
     // ---- K2 gather
     {
         GatherArgs g{Q.data, Q.pair_bytes, ids, cap, d_active, d_slot_pair, d_slot_base, qbuf, margin,
-                     T.max_norm, dim, l2};
-        uint32_t max_rows = 0;
-        for (uint32_t p : slot_pair) max_rows = std::max(max_rows, ceil_div_u(h_active[p], kQueryTilePair) * kQueryTilePair);
-        dim3 grid(ceil_div_u(max_rows * 4, 256), nslots);
+                     T.max_norm, dim, l2, d_hdr};
+        dim3 grid(ceil_div_u(tp_per_pair * kQueryTilePair * 4, 256), npairs);
         ProfScope prof(ctx, FNL_KCLASS_GATHER);
         gather_kernel<<<grid, 256, 0, s>>>(g);
         FNL_CUDA_TRY(cudaGetLastError());
@@ -1090,8 +1153,8 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
             TRY(ws_arr(ctx, "tc.trace", 6 * 4096, &trace));
             FNL_CUDA_TRY(cudaMemsetAsync(trace, 0, 6 * 4096 * 8, s));
         }
-        TcArgs t{qbuf, T.data, T.pair_bytes, nt, d_items, nitems, partial, debug_mode, trace};
-        const uint32_t grid = std::min<uint32_t>(nitems, sms);
+        TcArgs t{qbuf, T.data, T.pair_bytes, nt, d_items, d_hdr + 2, partial, debug_mode, trace};
+        const uint32_t grid = std::min<uint32_t>(nitems_cap, sms);
         cudaEvent_t end_ev;
         ctx_score_begin(ctx, &end_ev);
         tc_scan_kernel<<<grid, kScanThreads, kSmemTotal, s>>>(t);
@@ -1100,15 +1163,15 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     }
     // ---- K3b merge + certification
     {
-        MergeArgs m{partial, d_tp_pair, d_tp_row0, d_tp_qi0, splits, d_active, margin, qbuf, T.data,
+        MergeArgs m{partial, d_tp_pair, d_tp_row0, d_tp_qi0, d_hdr, d_active, margin, qbuf, T.data,
                     T.pair_bytes, nt, dim, out, min_dist, out_stride, rescan, rcount, d_near_ties, shard_keys};
         ProfScope prof(ctx, FNL_KCLASS_MERGE);
         if (dim == 24) {
-            if (l2) merge_kernel<true, 24><<<ntp, kQueryTilePair, 0, s>>>(m);
-            else merge_kernel<false, 24><<<ntp, kQueryTilePair, 0, s>>>(m);
+            if (l2) merge_kernel<true, 24><<<tp_max, kQueryTilePair, 0, s>>>(m);
+            else merge_kernel<false, 24><<<tp_max, kQueryTilePair, 0, s>>>(m);
         } else {
-            if (l2) merge_kernel<true, 0><<<ntp, kQueryTilePair, 0, s>>>(m);
-            else merge_kernel<false, 0><<<ntp, kQueryTilePair, 0, s>>>(m);
+            if (l2) merge_kernel<true, 0><<<tp_max, kQueryTilePair, 0, s>>>(m);
+            else merge_kernel<false, 0><<<tp_max, kQueryTilePair, 0, s>>>(m);
         }
         FNL_CUDA_TRY(cudaGetLastError());
     }
@@ -1130,7 +1193,7 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
         FNL_CUDA_TRY(cudaGetLastError());
     }
     if (debug_mode_trace_dump(ctx, s)) {}
-    ctx_count_launches(ctx, 5);
+    ctx_count_launches(ctx, 6);
     return FNL_OK;
 }
 
@@ -1165,8 +1228,10 @@ int tensor_nn_dense(fnl_context* ctx, const float* d_q, uint32_t nq, const float
     unsigned long long* ties;
     TRY(ws_arr(ctx, "tc.dense.ties", 1, &ties));
     FNL_CUDA_TRY(cudaMemsetAsync(ties, 0, 8, s));
-    const uint8_t done = 0;
-    return tensor_nn_pass(ctx, 1, Q, nullptr, nq, &nq, &done, T, dim, l2, d_nearest, nq, d_min_dist, ties);
+    uint32_t* d_nq;
+    TRY(ws_arr(ctx, "tc.dense.nq", 1, &d_nq));
+    FNL_CUDA_TRY(cudaMemcpyAsync(d_nq, &nq, 4, cudaMemcpyHostToDevice, s));  // pageable: staged before return
+    return tensor_nn_pass(ctx, 1, Q, nullptr, nq, d_nq, nullptr, T, dim, l2, d_nearest, nq, d_min_dist, ties);
 }
 
 int tensor_selftest_scores(fnl_context* ctx, const float* d_q, const float* d_t, uint32_t dim, bool l2,

@@ -44,8 +44,10 @@ int tensor_pack(fnl_context* ctx, const char* tag, const float* d_src, uint32_t 
                 PackedMaps* out);
 
 // One NN pass of gathered query rows against target maps, batched over pairs.
-// Query rows of pair p: ids[p*cap + i] (or i when ids is null), i < h_active[p];
-// pairs with h_active[p] == 0 or h_done[p] are skipped.  Winner indices land in
+// Query rows of pair p: ids[p*cap + i] (or i when ids is null), i < d_active[p];
+// pairs with d_active[p] == 0 or d_done[p] (d_done may be null) are skipped.  Both
+// are DEVICE arrays: the work lists are planned on the device, so consecutive
+// passes are enqueued without a host round trip.  Winner indices land in
 // out[p*out_stride + i]; if min_dist is non-null the exact reference distance of
 // the winner is written beside it.  d_near_ties[p] counts re-decided rows.
 //
@@ -57,7 +59,7 @@ int tensor_pack(fnl_context* ctx, const char* tag, const float* d_src, uint32_t 
 // the keys over the shards (NCCL / gloo int64 MIN) yields the global winner
 // with the reference's lowest-index tie rule; tensor_shard_finalize decodes.
 int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const uint32_t* ids,
-                   uint32_t cap, const uint32_t* h_active, const uint8_t* h_done,
+                   uint32_t cap, const uint32_t* d_active, const uint8_t* d_done,
                    const PackedMaps& T, uint32_t dim, bool l2, uint32_t* out, uint32_t out_stride,
                    float* min_dist, unsigned long long* d_near_ties, uint32_t tile_begin = 0,
                    uint32_t tile_end = 0, long long* shard_keys = nullptr);
