@@ -26,6 +26,8 @@
 // (16 ex2/clk/SM) and the rest barrier-separated latency phases -- the next
 // step is FA4-style warp specialisation (ping-pong softmax warpgroups) so the
 // latency phases hide under the other tile's exponentials.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_fp16.h>
 #include <math.h>
 #include <stdint.h>
@@ -969,6 +971,262 @@ __global__ void __launch_bounds__(kFm3Threads, 1) flashmatch3_kernel(FmArgs a) {
     }
 }
 
+// ---------------------------------------------------------------- K7 v4
+// v3 with TMA: Q, K_j and V_j arrive by cp.async.bulk.tensor (one elected
+// thread, 128B-swizzled boxes of 128 rows x 64 channels, zero fill past N)
+// instead of 16-byte cp.async from three loader warps, which spent ~2.5k
+// cycles just issuing the first Q tiles.  Operand descriptors switch to the
+// SWIZZLE_128B canonical layouts: Q / K K-major (8-row atoms of 1 KB, K step
+// = +32 B), V MN-major (hd contiguous, 8-key atoms 1 KB apart, K step of 16
+// keys = +2 KB).  P keeps the no-swizzle layout the softmax writes.
+constexpr uint32_t kKvStages4 = 3;
+constexpr uint32_t kFm4Threads = (16 + 1 + 1) * 32;
+constexpr uint32_t kSmemFm4 = 2 * kTileQK + 2 * kKvStages4 * kTileQK + 2 * kTileP + 1024;  // + alignment slack
+
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(sbo >> 4) << 32) |
+           (1ull << 46) | (2ull << 61);
+}
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+        "[%6];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_addr(bar))
+        : "memory");
+}
+
+__global__ void __launch_bounds__(kFm4Threads, 1)
+    flashmatch4_kernel(FmArgs a, const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                       const __grid_constant__ CUtensorMap tv) {
+    __shared__ float red[2][2][kBlockQ];  // [tile][column half][row] partial maxima / sums
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint32_t tmem_slot;
+    __shared__ __align__(8) uint64_t s_full[2], s_free[2], p_full[2], o_full[2];
+    __shared__ __align__(8) uint64_t kv_full[kKvStages4], kv_empty[kKvStages4];
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
+    const uint32_t q0 = blockIdx.x * 2 * kBlockQ, h = blockIdx.y, b = blockIdx.z;
+    FM_STAMP(0);
+    // SWIZZLE_128B operands need 1 KB aligned tiles
+    const uint32_t base_pad = (1024u - (smem_addr(smem) & 1023u)) & 1023u;
+    const uint32_t sQ = smem_addr(smem) + base_pad;
+    const uint32_t sK = sQ + 2 * kTileQK, sV = sK + kKvStages4 * kTileQK, sP = sV + kKvStages4 * kTileQK;
+    uint8_t* pP0 = smem + base_pad + (2 + 2 * kKvStages4) * kTileQK;
+    const uint32_t nblk = (a.nkv + kBlockK - 1) / kBlockK;
+
+    if (tid == 0) {
+        for (int t = 0; t < 2; ++t) {
+            mbar_init(&s_full[t], 1);
+            mbar_init(&s_free[t], 8);  // the tile's 8 softmax warps
+            mbar_init(&p_full[t], 8);
+            mbar_init(&o_full[t], 1);
+        }
+        for (uint32_t st = 0; st < kKvStages4; ++st) {
+            mbar_init(&kv_full[st], 1);   // the loader's expect_tx arrival; TMA completes the bytes
+            mbar_init(&kv_empty[st], 1);  // one tcgen05.commit after the block's last PV
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_slot)),
+                     "r"(512u));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+    FM_STAMP(34);
+
+    if (warp == 17) {
+        // ---------------- loader: one elected thread issues every TMA box
+        if (elect_one()) {
+            const int hh = (int)h, bb = (int)b;
+            // Q tiles ride on K/V stage 0's barrier (the first S needs all three)
+            mbar_expect_tx(&kv_full[0], 4 * kTileQK);
+            tma_load_4d(sQ, &tq, 0, (int)q0, hh, bb, &kv_full[0]);
+            tma_load_4d(sQ + kTileQK, &tq, 0, (int)(q0 + kBlockQ), hh, bb, &kv_full[0]);
+            tma_load_4d(sK, &tk, 0, 0, hh, bb, &kv_full[0]);
+            tma_load_4d(sV, &tv, 0, 0, hh, bb, &kv_full[0]);
+            for (uint32_t blk = 1; blk < nblk; ++blk) {
+                const uint32_t st = blk % kKvStages4;
+                mbar_wait(&kv_empty[st], ((blk / kKvStages4) & 1u) ^ 1u);
+                mbar_expect_tx(&kv_full[st], 2 * kTileQK);
+                tma_load_4d(sK + st * kTileQK, &tk, 0, (int)(blk * kBlockK), hh, bb, &kv_full[st]);
+                tma_load_4d(sV + st * kTileQK, &tv, 0, (int)(blk * kBlockK), hh, bb, &kv_full[st]);
+            }
+        }
+        __syncwarp();
+    } else if (warp == 16) {
+        // ---------------- MMA warp: S_t(j+1) as soon as S_t(j) is drained,
+        // PV_t(j) as soon as P_t(j) is published
+        auto kv_ready = [&](uint32_t blk) {
+            mbar_wait(&kv_full[blk % kKvStages4], (blk / kKvStages4) & 1u);
+        };
+        auto issue_s = [&](uint32_t t, uint32_t blk) {
+            tc_fence_after();
+            if (elect_one()) {
+                const uint32_t kb = sK + (blk % kKvStages4) * kTileQK, qb = sQ + t * kTileQK;
+#pragma unroll
+                for (uint32_t ks = 0; ks < kHd / 16; ++ks)
+                    tc_mma_f16(tmem + t * 256u, sw128_desc(qb + ks * 32u, 16u, 1024u),
+                               sw128_desc(kb + ks * 32u, 16u, 1024u), kIdescS, ks > 0 ? 1u : 0u);
+                tc_commit(&s_full[t]);
+            }
+            __syncwarp();
+        };
+        kv_ready(0);  // also covers Q (issued before K0/V0 by the same lanes)
+        issue_s(0, 0);
+        issue_s(1, 0);
+        uint32_t js[2] = {1u, 1u}, jp[2] = {0u, 0u};
+        while (jp[0] < nblk || jp[1] < nblk) {
+#pragma unroll
+            for (uint32_t t = 0; t < 2; ++t) {
+                if (js[t] < nblk && mbar_test(&s_free[t], (js[t] - 1u) & 1u)) {
+                    kv_ready(js[t]);  // the stage cannot have been refilled: its PVs are not issued yet
+                    issue_s(t, js[t]);
+                    ++js[t];
+                }
+                const uint32_t j = jp[t];
+                if (j < nblk && mbar_test(&p_full[t], j & 1u)) {
+                    tc_fence_after();
+                    const bool last_reader = jp[t ^ 1u] > j;  // the other tile's PV_j is already issued
+                    if (elect_one()) {
+                        const uint32_t vb = sV + (j % kKvStages4) * kTileQK, pb = sP + t * kTileP;
+#pragma unroll
+                        for (uint32_t ks = 0; ks < kBlockK / 16; ++ks)
+                            tc_mma_f16(tmem + t * 256u + 128u, fm_desc(pb + ks * 256u, 128u, 2048u),
+                                       sw128_desc(vb + ks * 2048u, 1024u, 1024u), kIdescPV, (ks | j) > 0 ? 1u : 0u);
+                        tc_commit(&o_full[t]);
+                        if (last_reader) tc_commit(&kv_empty[j % kKvStages4]);
+                    }
+                    __syncwarp();
+                    jp[t] = j + 1;
+                }
+            }
+        }
+    } else {
+        // ---------------- softmax warpgroup t: warps 8t..8t+7; warp w reads TMEM
+        // lane quadrant w%4 and column half hf = (w/4)%2: two threads per query
+        // row, 64 key columns and 32 O columns each
+        const uint32_t t = warp >> 3, hf = (warp >> 2) & 1u, row = ((warp & 3u) << 5) | lane;
+        const uint32_t lane_base = ((warp & 3u) * 32u) << 16;
+        const uint32_t tS = tmem + lane_base + t * 256u, tO = tS + 128u + 32u * hf;
+        uint8_t* pP = pP0 + t * kTileP;
+        float m = -INFINITY, l = 0.0f;
+        const float sl2 = a.scale_log2;
+        auto tile_sync = [&]() { asm volatile("bar.sync %0, 256;" ::"r"(1u + t) : "memory"); };
+        for (uint32_t j = 0; j < nblk; ++j) {
+            mbar_wait(&s_full[t], j & 1u);
+            if (t == 0) FM_STAMP(3 + j);
+            tc_fence_after();
+            Frag f0, f1;
+            frag_ld64(tS + hf * 64u, f0, f1);
+            frag_wait2(f0, f1);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_free[t]);  // S_t(j) is in registers: S_t(j+1) may overwrite it
+            const uint32_t kvalid = a.nkv - j * kBlockK;
+            if (kvalid < kBlockK) {
+#pragma unroll
+                for (uint32_t i = 0; i < 32; ++i) {
+                    if (hf * 64u + i >= kvalid) f0.r[i] = __float_as_uint(-INFINITY);
+                    if (hf * 64u + 32u + i >= kvalid) f1.r[i] = __float_as_uint(-INFINITY);
+                }
+            }
+            float r4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+            for (uint32_t i = 0; i < 32; i += 8)
+#pragma unroll
+                for (uint32_t u = 0; u < 4; ++u) {
+                    r4[u] = max3(r4[u], __uint_as_float(f0.r[i + 2 * u]), __uint_as_float(f0.r[i + 2 * u + 1]));
+                    r4[u] = max3(r4[u], __uint_as_float(f1.r[i + 2 * u]), __uint_as_float(f1.r[i + 2 * u + 1]));
+                }
+            float mx = fmaxf(fmaxf(r4[0], r4[1]), fmaxf(r4[2], r4[3]));
+            red[t][hf][row] = mx;
+            tile_sync();
+            mx = fmaxf(mx, red[t][hf ^ 1u][row]);
+            tile_sync();  // both halves read before either writes the next value
+            // lazy rescale: keep the stale max unless the row max grew by more
+            // than 2^kRescaleLog2 (both threads of a row decide identically)
+            const float mc = mx * sl2;
+            const bool grow = mc > m + kRescaleLog2;
+            const float m_new = grow ? mc : m;
+            const float alpha = (grow && j > 0) ? ex2(m - m_new) : 1.0f;
+            if (t == 0 && j < 8) FM_STAMP(10 + j);
+            // PV_t(j-1) must have retired before P is overwritten or O rescaled
+            if (j > 0) {
+                mbar_wait(&o_full[t], (j - 1) & 1u);
+                tc_fence_after();
+            }
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (uint32_t c = 0; c < 2; ++c) {
+                const Frag& f = c ? f1 : f0;
+                const uint32_t col0 = hf * 64u + c * 32u;
+#pragma unroll
+                for (uint32_t q = 0; q < 4; ++q) {
+                    float p[8];
+#pragma unroll
+                    for (uint32_t i = 0; i < 8; ++i) p[i] = ex2(fmaf(__uint_as_float(f.r[q * 8 + i]), sl2, -m_new));
+                    acc[q] += ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
+                    uint4 w;
+                    w.x = pack_half2_rn(p[0], p[1]);
+                    w.y = pack_half2_rn(p[2], p[3]);
+                    w.z = pack_half2_rn(p[4], p[5]);
+                    w.w = pack_half2_rn(p[6], p[7]);
+                    *reinterpret_cast<uint4*>(pP + off_p(row, col0 / 8u + q)) = w;
+                }
+            }
+            if (__any_sync(0xFFFFFFFFu, alpha != 1.0f)) {  // warp-collective TMEM round trip of O
+                Frag o;
+                frag_ld(tO, o);
+                frag_wait1(o);
+#pragma unroll
+                for (uint32_t i = 0; i < 32; ++i) o.r[i] = __float_as_uint(__uint_as_float(o.r[i]) * alpha);
+                frag_st(tO, o);
+                tmem_st_wait();
+            }
+            tc_fence_before();
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_full[t]);  // P_t(j) written, O_t rescaled
+            if (t == 0) FM_STAMP(20 + j);
+            l = l * alpha + ((acc[0] + acc[1]) + (acc[2] + acc[3]));  // partial: this thread's columns
+            m = m_new;
+        }
+        mbar_wait(&o_full[t], (nblk - 1) & 1u);
+        tc_fence_after();
+        Frag o;
+        frag_ld(tO, o);
+        frag_wait1(o);
+        red[t][hf][row] = l;
+        tile_sync();
+        l += red[t][hf ^ 1u][row];
+        const uint32_t grow_ = q0 + t * kBlockQ + row;
+        if (grow_ < a.nq) {
+            const float inv = 1.0f / l;
+            __half* go = a.o + b * a.o_sb + h * a.o_sh + (uint64_t)grow_ * a.o_sn + hf * 32u;
+#pragma unroll
+            for (uint32_t c = 0; c < kHd / 16; ++c) {
+                uint4 w;
+                w.x = pack_half2_rn(__uint_as_float(o.r[c * 8 + 0]) * inv, __uint_as_float(o.r[c * 8 + 1]) * inv);
+                w.y = pack_half2_rn(__uint_as_float(o.r[c * 8 + 2]) * inv, __uint_as_float(o.r[c * 8 + 3]) * inv);
+                w.z = pack_half2_rn(__uint_as_float(o.r[c * 8 + 4]) * inv, __uint_as_float(o.r[c * 8 + 5]) * inv);
+                w.w = pack_half2_rn(__uint_as_float(o.r[c * 8 + 6]) * inv, __uint_as_float(o.r[c * 8 + 7]) * inv);
+                *reinterpret_cast<uint4*>(go + c * 8) = w;
+            }
+        }
+    }
+    FM_STAMP(63);
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
+    }
+}
+
 bool fm_attr_done = false;
 
 }  // namespace
@@ -991,6 +1249,7 @@ int flashmatch_forward(fnl_context* ctx, const fnl_attention_desc& d) {
         FNL_CUDA_TRY(cudaFuncSetAttribute(flashmatch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFm));
         FNL_CUDA_TRY(cudaFuncSetAttribute(flashmatch2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFm2));
         FNL_CUDA_TRY(cudaFuncSetAttribute(flashmatch3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFm2));
+        FNL_CUDA_TRY(cudaFuncSetAttribute(flashmatch4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFm4));
         fm_attr_done = true;
     }
     FmArgs a{};
@@ -1013,8 +1272,38 @@ int flashmatch_forward(fnl_context* ctx, const fnl_attention_desc& d) {
     ProfScope prof(ctx, FNL_KCLASS_ATTN);
     // v2 (warp-specialised, two query tiles per CTA) is the product kernel;
     // FNL_FM_VERSION=1 selects the barrier-synchronous v1 for comparison
-    static const int ver = getenv("FNL_FM_VERSION") ? atoi(getenv("FNL_FM_VERSION")) : 3;
-    if (ver == 1)
+    static const int ver = getenv("FNL_FM_VERSION") ? atoi(getenv("FNL_FM_VERSION")) : 4;
+    if (ver == 4) {
+        // TMA tensor maps of Q, K, V viewed as [batch][heads][rows][64] binary16
+        static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+        if (!encode) {
+            void* fn = nullptr;
+            cudaDriverEntryPointQueryResult qr{};
+            FNL_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr));
+            if (!fn || qr != cudaDriverEntryPointSuccess)
+                return fail(FNL_ERUNTIME, "flashmatch: cuTensorMapEncodeTiled unavailable");
+            encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        }
+        auto make_map = [&](CUtensorMap* m, const void* ptr, uint32_t rows, const uint64_t* st) -> int {
+            const cuuint64_t dims[4] = {kHd, rows, d.heads, d.batch};
+            const cuuint64_t strides[3] = {st[2] * 2, st[1] * 2, st[0] * 2};
+            const cuuint32_t box[4] = {kHd, kBlockQ, 1, 1}, es[4] = {1, 1, 1, 1};
+            const CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(ptr), dims, strides, box, es,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS)
+                return fail(FNL_EINVAL, "flashmatch: cuTensorMapEncodeTiled rejected the layout (error " +
+                                            std::to_string((int)r) + ")");
+            return FNL_OK;
+        };
+        CUtensorMap tq, tk, tv;
+        int rc = make_map(&tq, d.q, d.nq, d.q_stride);
+        if (rc == FNL_OK) rc = make_map(&tk, d.k, d.nkv, d.k_stride);
+        if (rc == FNL_OK) rc = make_map(&tv, d.v, d.nkv, d.v_stride);
+        if (rc != FNL_OK) return rc;
+        flashmatch4_kernel<<<dim3((d.nq + 2 * kBlockQ - 1) / (2 * kBlockQ), d.heads, d.batch), kFm4Threads, kSmemFm4,
+                             s>>>(a, tq, tk, tv);
+    } else if (ver == 1)
         flashmatch_kernel<<<grid, kFmThreads, kSmemFm, s>>>(a);
     else if (ver == 3)
         flashmatch3_kernel<<<dim3((d.nq + 2 * kBlockQ - 1) / (2 * kBlockQ), d.heads, d.batch), kFm3Threads,
