@@ -133,7 +133,8 @@ struct FmArgs {
     uint64_t k_sb, k_sh, k_sn;
     uint64_t v_sb, v_sh, v_sn;
     uint64_t o_sb, o_sh, o_sn;
-    float scale_log2;  // softmax scale * log2(e)
+    float scale_log2;
+    uint32_t tiles;  // query tiles per CTA (v4: 1 or 2)  // softmax scale * log2(e)
     int trace;
 };
 
@@ -1005,7 +1006,7 @@ __global__ void __launch_bounds__(kFm4Threads, 1)
     __shared__ __align__(8) uint64_t s_full[2], s_free[2], p_full[2], o_full[2];
     __shared__ __align__(8) uint64_t kv_full[kKvStages4], kv_empty[kKvStages4];
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
-    const uint32_t q0 = blockIdx.x * 2 * kBlockQ, h = blockIdx.y, b = blockIdx.z;
+    const uint32_t ntile = a.tiles, q0 = blockIdx.x * ntile * kBlockQ, h = blockIdx.y, b = blockIdx.z;
     FM_STAMP(0);
     // SWIZZLE_128B operands need 1 KB aligned tiles
     const uint32_t base_pad = (1024u - (smem_addr(smem) & 1023u)) & 1023u;
@@ -1043,9 +1044,9 @@ __global__ void __launch_bounds__(kFm4Threads, 1)
         if (elect_one()) {
             const int hh = (int)h, bb = (int)b;
             // Q tiles ride on K/V stage 0's barrier (the first S needs all three)
-            mbar_expect_tx(&kv_full[0], 4 * kTileQK);
+            mbar_expect_tx(&kv_full[0], (ntile + 2) * kTileQK);
             tma_load_4d(sQ, &tq, 0, (int)q0, hh, bb, &kv_full[0]);
-            tma_load_4d(sQ + kTileQK, &tq, 0, (int)(q0 + kBlockQ), hh, bb, &kv_full[0]);
+            if (ntile == 2) tma_load_4d(sQ + kTileQK, &tq, 0, (int)(q0 + kBlockQ), hh, bb, &kv_full[0]);
             tma_load_4d(sK, &tk, 0, 0, hh, bb, &kv_full[0]);
             tma_load_4d(sV, &tv, 0, 0, hh, bb, &kv_full[0]);
             for (uint32_t blk = 1; blk < nblk; ++blk) {
@@ -1077,8 +1078,9 @@ __global__ void __launch_bounds__(kFm4Threads, 1)
         };
         kv_ready(0);  // also covers Q (issued before K0/V0 by the same lanes)
         issue_s(0, 0);
-        issue_s(1, 0);
-        uint32_t js[2] = {1u, 1u}, jp[2] = {0u, 0u};
+        if (ntile == 2) issue_s(1, 0);
+        // a single-tile CTA never serves tile 1
+        uint32_t js[2] = {1u, ntile == 2 ? 1u : nblk}, jp[2] = {0u, ntile == 2 ? 0u : nblk};
         while (jp[0] < nblk || jp[1] < nblk) {
 #pragma unroll
             for (uint32_t t = 0; t < 2; ++t) {
@@ -1090,7 +1092,7 @@ __global__ void __launch_bounds__(kFm4Threads, 1)
                 const uint32_t j = jp[t];
                 if (j < nblk && mbar_test(&p_full[t], j & 1u)) {
                     tc_fence_after();
-                    const bool last_reader = jp[t ^ 1u] > j;  // the other tile's PV_j is already issued
+                    const bool last_reader = jp[t ^ 1u] > j;  // the other tile's PV_j is issued (or no other tile)
                     if (elect_one()) {
                         const uint32_t vb = sV + (j % kKvStages4) * kTileQK, pb = sP + t * kTileP;
 #pragma unroll
@@ -1105,7 +1107,7 @@ __global__ void __launch_bounds__(kFm4Threads, 1)
                 }
             }
         }
-    } else {
+    } else if ((warp >> 3) < ntile) {
         // ---------------- softmax warpgroup t: warps 8t..8t+7; warp w reads TMEM
         // lane quadrant w%4 and column half hf = (w/4)%2: two threads per query
         // row, 64 key columns and 32 O columns each
@@ -1301,8 +1303,14 @@ int flashmatch_forward(fnl_context* ctx, const fnl_attention_desc& d) {
         if (rc == FNL_OK) rc = make_map(&tk, d.k, d.nkv, d.k_stride);
         if (rc == FNL_OK) rc = make_map(&tv, d.v, d.nkv, d.v_stride);
         if (rc != FNL_OK) return rc;
-        flashmatch4_kernel<<<dim3((d.nq + 2 * kBlockQ - 1) / (2 * kBlockQ), d.heads, d.batch), kFm4Threads, kSmemFm4,
-                             s>>>(a, tq, tk, tv);
+        // two query tiles per CTA share the SM's MUFU / tensor core; when one
+        // tile per CTA still fits in a single wave, spread the tiles instead
+        const uint64_t tiles1 = (uint64_t)((d.nq + kBlockQ - 1) / kBlockQ) * d.heads * d.batch;
+        static const int force_tiles = getenv("FNL_FM_TILES") ? atoi(getenv("FNL_FM_TILES")) : 0;
+        a.tiles = force_tiles == 1 || force_tiles == 2 ? (uint32_t)force_tiles
+                                                       : (tiles1 <= (uint64_t)ctx_sm_count(ctx) ? 1u : 2u);
+        flashmatch4_kernel<<<dim3((d.nq + a.tiles * kBlockQ - 1) / (a.tiles * kBlockQ), d.heads, d.batch), kFm4Threads,
+                             kSmemFm4, s>>>(a, tq, tk, tv);
     } else if (ver == 1)
         flashmatch_kernel<<<grid, kFmThreads, kSmemFm, s>>>(a);
     else if (ver == 3)
