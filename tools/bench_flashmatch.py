@@ -12,15 +12,15 @@ def attention_flops(calls):
 
 
 def time_calls(calls, attn, reps=20, warmup=3):
-    bufs = []
+    bufs = {}
     g = torch.Generator(device="cpu").manual_seed(0)
-    for b, h, nq, nkv in calls[:2]:
+    for shape in dict.fromkeys(calls):  # one input set per distinct (batch, heads, nq, nkv)
+        b, h, nq, nkv = shape
         q = torch.randn((b, h, nq, 64), generator=g).to("cuda", torch.float16)
         k = torch.randn((b, h, nkv, 64), generator=g).to("cuda", torch.float16)
         v = torch.randn((b, h, nkv, 64), generator=g).to("cuda", torch.float16)
-        bufs.append((q, k, v, torch.empty_like(q)))
-    # encoder calls use bufs[0], decoder calls bufs[1] (same shapes as calls)
-    seq = [bufs[0] if c == calls[0] else bufs[1] for c in calls]
+        bufs[shape] = (q, k, v, torch.empty_like(q))
+    seq = [bufs[c] for c in calls]
 
     def run():
         for q, k, v, o in seq:
