@@ -6,26 +6,25 @@
 //   binary16 Q/K/V/O, fp32 scores, fp32 softmax statistics, fp32 accumulation
 //   (HybridCast numerics).
 //
-// One CTA = 128 query rows of one (batch, head); kColGroups threads per row
-// (warp w reads TMEM lane quadrant w%4, key columns of column group w/4).  Per
-// 128-key block j (software-pipelined: S_{j+1} is issued as soon as S_j is
-// drained and runs under softmax j; PV_j runs under softmax j+1 and its TMEM
-// buffer is drained one block late):
-//   S_j = Q K_j^T        tcgen05.mma kind::f16 M128 N128 K16 x4 (SS) -> TMEM cols [0,128)
-//   softmax              tcgen05.ld of the thread's scores, online max /
-//                        rescale / exp2 / row sum in registers, P_j (binary16)
-//                        st.shared in the UMMA K-major layout
-//   O_j = P_j V_j        tcgen05.mma M128 N64 K16 x8 (SS, V MN-major)  -> TMEM cols 128 + 64 (j&1)
-//   o = o * alpha + O_j  (registers; the final 1/l and binary16 cast in the epilogue)
-// K/V blocks are double-buffered with cp.async (zero-filled past the ends); two
-// CTAs share an SM (112 KB smem, 256 TMEM columns each).  The N x N score
-// matrix never leaves the SM.
-//
-// Measured (tools/fm_trace.py clock stamps): one block
-// costs ~5k SM cycles per CTA pair, of which ~2.2k are the MUFU ex2 phase
-// (16 ex2/clk/SM) and the rest barrier-separated latency phases -- the next
-// step is FA4-style warp specialisation (ping-pong softmax warpgroups) so the
-// latency phases hide under the other tile's exponentials.
+// Product kernel: flashmatch4_kernel (v4).  One CTA = one or two 128-row
+// query tiles of one (batch, head), warp-specialised, mbarrier hand-offs only:
+//   warps 0-15  softmax: warpgroup t (8 warps) owns query tile t, two threads
+//               per row (TMEM lane quadrant w%4, key-column half (w/4)%2)
+//   warp 16     MMA issuer: S_t(j) = Q_t K_j^T (M128 N128 K16 x4, SS) into
+//               TMEM [256t, 256t+128) as soon as S_t(j-1) is in registers;
+//               O_t += P_t(j) V_j (M128 N64 K16 x8, V MN-major) into
+//               [256t+128, 256t+192) as soon as P_t(j) is published
+//   warp 17     loader: one elected thread, TMA tensor-map boxes of 128 rows
+//               x 64 channels (128B swizzle, zero fill past N) into a 3-stage
+//               K/V ring
+// Per block the softmax reads S once (tcgen05.ld.x64), releases it, takes
+// the row max across the two half-row threads through shared memory, writes
+// binary16 P = 2^(s*scale*log2e - m) to shared memory (UMMA K-major layout)
+// and rescales O in TMEM only when the row max grew by more than 2^8 (lazy
+// rescale; O and l carry the same stale max).  The N x N score matrix never
+// leaves the SM.  flashmatch3_kernel (v3) is the same pipeline fed by
+// cp.async loader warps, kept for comparison (FNL_FM_VERSION=3).
+// Measurements and the variants that lost: DESIGN.md section 7.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_fp16.h>
@@ -45,15 +44,11 @@ namespace fnl {
 
 namespace {
 
-constexpr uint32_t kColGroups = 1;   // threads per query row (each owns 128/kColGroups key columns)
-constexpr uint32_t kFmThreads = 128 * kColGroups;
 constexpr uint32_t kHd = 64;         // head_dim
 constexpr uint32_t kBlockQ = 128;    // query rows per CTA
 constexpr uint32_t kBlockK = 128;    // keys per block
 constexpr uint32_t kTileQK = kBlockQ * kHd * 2;   // 16 KB (Q, K blocks and V blocks alike)
 constexpr uint32_t kTileP = kBlockQ * kBlockK * 2;  // 32 KB
-constexpr uint32_t kSmemFm = kTileQK /*Q*/ + 2 * kTileQK /*K*/ + 2 * kTileQK /*V*/ + kTileP + 64;
-constexpr uint32_t kTmemCols = 256;  // S [0,128) + O_j double buffer [128,256)
 
 // UMMA shared-memory descriptor, no swizzle, version 1 (sm_100).
 __device__ __forceinline__ uint64_t fm_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -82,11 +77,6 @@ __device__ __forceinline__ uint32_t off_p(uint32_t row, uint32_t chunk) {
 __device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g, bool valid) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "r"(valid ? 16u : 0u)
                  : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void fence_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -141,292 +131,7 @@ struct FmArgs {
 // 128 rows x 64 hd of a [token][hd] operand into smem.  Warp lanes: row%8 and
 // 4 consecutive 16 B chunks, so global reads are 64 B runs and every quarter
 // warp writes one 128 B core matrix.
-template <bool kV>
-__device__ __forceinline__ void load_tile(uint32_t sbase, const __half* g, uint64_t sn, uint32_t nvalid) {
-    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (uint32_t j = 0; j < 1024u / kFmThreads; ++j) {
-        const uint32_t combo = j * (kFmThreads / 32u) + warp;
-        const uint32_t chunk = (lane >> 3) + 4u * (combo & 1u);
-        const uint32_t row = (combo >> 1) * 8u + (lane & 7u);
-        const bool valid = row < nvalid;
-        const __half* src = g + (valid ? (uint64_t)row * sn + chunk * 8u : 0);
-        cp_async16(sbase + (kV ? off_v(row, chunk) : off_qk(row, chunk)), src, valid);
-    }
-}
-
-__global__ void __launch_bounds__(kFmThreads, 2) flashmatch_kernel(FmArgs a) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ uint32_t tmem_slot;
-    __shared__ __align__(8) uint64_t bar_s, bar_o;
-    __shared__ float red[kColGroups][kBlockQ];  // per-row partials across the column groups
-    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
-    // warp w reads TMEM lane quadrant w%4 (rows 32*(w%4) + lane), key columns
-    // [32*cg, 32*cg + 32) of S and O columns [16*cg, 16*cg + 16)
-    const uint32_t quad = warp & 3u, cg = warp >> 2;
-    const uint32_t row = quad * 32u + lane;
-    const uint32_t q0 = blockIdx.x * kBlockQ, h = blockIdx.y, b = blockIdx.z;
-    FM_STAMP(0);
-    const uint32_t sQ = smem_addr(smem);
-    const uint32_t sK = sQ + kTileQK, sV = sK + 2 * kTileQK, sP = sV + 2 * kTileQK;
-    uint8_t* pP = smem + 5 * kTileQK;
-
-    if (tid == 0) {
-        mbar_init(&bar_s, 1);
-        mbar_init(&bar_o, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_slot)),
-                     "r"(kTmemCols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-
-    const __half* gq = a.q + b * a.q_sb + h * a.q_sh + (uint64_t)q0 * a.q_sn;
-    const __half* gk = a.k + b * a.k_sb + h * a.k_sh;
-    const __half* gv = a.v + b * a.v_sb + h * a.v_sh;
-    const uint32_t nblk = (a.nkv + kBlockK - 1) / kBlockK;
-    auto load_k = [&](uint32_t blk) {
-        if (blk < nblk)
-            load_tile<false>(sK + (blk & 1u) * kTileQK, gk + (uint64_t)blk * kBlockK * a.k_sn, a.k_sn,
-                             a.nkv - blk * kBlockK);
-        cp_async_commit();
-    };
-    auto load_v = [&](uint32_t blk) {
-        if (blk < nblk)
-            load_tile<true>(sV + (blk & 1u) * kTileQK, gv + (uint64_t)blk * kBlockK * a.v_sn, a.v_sn,
-                            a.nkv - blk * kBlockK);
-        cp_async_commit();
-    };
-    // cp.async groups in commit order: {Q, K0, V0}, K1, {}, then per block j:
-    // K_{j+2} (top of j), V_{j+1} (middle of j).  Every wait below is
-    // wait_group 2: it retires exactly the group the next MMA needs.
-    load_tile<false>(sQ, gq, a.q_sn, a.nq - q0);
-    load_tile<false>(sK, gk, a.k_sn, a.nkv);
-    load_tile<true>(sV, gv, a.v_sn, a.nkv);
-    cp_async_commit();
-    load_k(1);
-    cp_async_commit();
-
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = tmem_slot;
-    const uint32_t lane_base = (quad * 32u) << 16;
-
-    auto issue_s = [&](uint32_t kb) {
-        if (warp == 0) {
-            tc_fence_after();
-            if (elect_one()) {
-#pragma unroll
-                for (uint32_t ks = 0; ks < kHd / 16; ++ks)
-                    tc_mma_f16(tmem, fm_desc(sQ + ks * 256u, 128u, 1024u), fm_desc(kb + ks * 256u, 128u, 1024u),
-                               kIdescS, ks > 0 ? 1u : 0u);
-                tc_commit(&bar_s);
-            }
-            __syncwarp();
-        }
-    };
-    FM_STAMP(1);
-    cp_async_wait<2>();
-    fence_async_smem();
-    __syncthreads();
-    FM_STAMP(2);
-    issue_s(sK);  // S_0
-
-    constexpr uint32_t kSc = kBlockK / kColGroups;  // S columns per thread
-    constexpr uint32_t kOc = kHd / kColGroups;      // O columns per thread
-    float o[kOc];
-#pragma unroll
-    for (uint32_t i = 0; i < kOc; ++i) o[i] = 0.0f;
-    float m = -INFINITY, l = 0.0f, alpha_prev = 0.0f;
-    const float sl2 = a.scale_log2;
-
-    // o = o * alpha_{j-1} + O_{j-1}  (TMEM buffer (j-1)&1, this thread's 16 columns)
-    auto drain_o = [&](uint32_t jj, float alpha) {
-        const uint32_t ob = tmem + lane_base + 128u + 64u * (jj & 1u) + cg * kOc;
-#pragma unroll
-        for (uint32_t c = 0; c < kOc; c += 16) {
-            uint32_t r[16];
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-                  "=r"(r[15])
-                : "r"(ob + c));
-            asm volatile("tcgen05.wait::ld.sync.aligned;"
-                         : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]),
-                           "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]),
-                           "+r"(r[14]), "+r"(r[15])
-                         :
-                         : "memory");
-#pragma unroll
-            for (uint32_t i = 0; i < 16; ++i) o[c + i] = fmaf(o[c + i], alpha, __uint_as_float(r[i]));
-        }
-    };
-
-    for (uint32_t j = 0; j < nblk; ++j) {
-        mbar_wait(&bar_s, j & 1u);
-        FM_STAMP(3 + 6 * j);
-        tc_fence_after();
-        float s[kSc];
-#pragma unroll
-        for (uint32_t c = 0; c < kSc; c += 32) {
-            Frag f;
-            frag_ld(tmem + lane_base + cg * kSc + c, f);
-            asm volatile("tcgen05.wait::ld.sync.aligned;"
-                         : "+r"(f.r[0]), "+r"(f.r[1]), "+r"(f.r[2]), "+r"(f.r[3]), "+r"(f.r[4]), "+r"(f.r[5]),
-                           "+r"(f.r[6]), "+r"(f.r[7]), "+r"(f.r[8]), "+r"(f.r[9]), "+r"(f.r[10]), "+r"(f.r[11]),
-                           "+r"(f.r[12]), "+r"(f.r[13]), "+r"(f.r[14]), "+r"(f.r[15]), "+r"(f.r[16]), "+r"(f.r[17]),
-                           "+r"(f.r[18]), "+r"(f.r[19]), "+r"(f.r[20]), "+r"(f.r[21]), "+r"(f.r[22]), "+r"(f.r[23]),
-                           "+r"(f.r[24]), "+r"(f.r[25]), "+r"(f.r[26]), "+r"(f.r[27]), "+r"(f.r[28]), "+r"(f.r[29]),
-                           "+r"(f.r[30]), "+r"(f.r[31])
-                         :
-                         : "memory");
-#pragma unroll
-            for (uint32_t i = 0; i < 32; ++i) s[c + i] = __uint_as_float(f.r[i]);
-        }
-        const uint32_t kvalid = a.nkv - j * kBlockK;
-        if (kvalid < kBlockK) {
-#pragma unroll
-            for (uint32_t i = 0; i < kSc; ++i)
-                if (cg * kSc + i >= kvalid) s[i] = -INFINITY;
-        }
-        {   // partial row max: four independent 3-input chains
-            float r4[4] = {s[0], s[1], s[2], s[3]};
-#pragma unroll
-            for (uint32_t i = 4; i < kSc; i += 8) {
-#pragma unroll
-                for (uint32_t u = 0; u < 4; ++u) r4[u] = max3(r4[u], s[i + 2 * u], s[i + 2 * u + 1]);
-            }
-            red[cg][row] = fmaxf(fmaxf(r4[0], r4[1]), fmaxf(r4[2], r4[3]));
-        }
-        load_k(j + 2);       // K buffer j&1 is free (S_j retired)
-        cp_async_wait<2>();  // K_{j+1} landed
-        fence_async_smem();
-        tc_fence_before();
-        FM_STAMP(4 + 6 * j);
-        __syncthreads();     // [A] S_j drained by every thread, partial maxima posted
-        FM_STAMP(5 + 6 * j);
-        if (j + 1 < nblk) issue_s(sK + ((j + 1) & 1u) * kTileQK);  // runs under this softmax
-        if ((a.trace & 2) && j + 1 < nblk && tid == 0) {  // profiling: S MMA latency in isolation
-            mbar_wait(&bar_s, (j + 1) & 1u);
-            FM_STAMP(40 + 2 * j);
-        }
-
-        float mx = red[0][row];
-#pragma unroll
-        for (uint32_t g = 1; g < kColGroups; ++g) mx = fmaxf(mx, red[g][row]);
-        const float m_new = fmaxf(m, mx * sl2);
-        const float alpha = ex2(m - m_new);
-        // PV_{j-1} must have retired before P is overwritten
-        if (j > 0) {
-            mbar_wait(&bar_o, (j - 1) & 1u);
-            tc_fence_after();
-        }
-        FM_STAMP(6 + 6 * j);
-        float acc[kSc / 8];
-#pragma unroll
-        for (uint32_t c = 0; c < kSc / 8; ++c) {
-            float p[8];
-#pragma unroll
-            for (uint32_t i = 0; i < 8; ++i) p[i] = ex2(fmaf(s[c * 8 + i], sl2, -m_new));
-            acc[c] = ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
-            uint4 w;
-            w.x = pack_half2_rn(p[0], p[1]);
-            w.y = pack_half2_rn(p[2], p[3]);
-            w.z = pack_half2_rn(p[4], p[5]);
-            w.w = pack_half2_rn(p[6], p[7]);
-            *reinterpret_cast<uint4*>(pP + off_p(row, cg * (kSc / 8) + c)) = w;
-        }
-#pragma unroll
-        for (uint32_t w = kSc / 16; w > 0; w >>= 1)
-#pragma unroll
-            for (uint32_t c = 0; c < w; ++c) acc[c] += acc[c + w];
-        l = l * alpha + acc[0];  // this thread's partial row sum
-        m = m_new;
-        if (j > 0) drain_o(j - 1, alpha_prev);  // V buffer (j-1)&1 free too
-        alpha_prev = alpha;
-        load_v(j + 1);
-        FM_STAMP(7 + 6 * j);
-        cp_async_wait<2>();  // V_j landed
-        fence_async_smem();
-        tc_fence_before();
-        __syncthreads();     // [B] P_j complete, O_{j-1} drained, maxima read
-        FM_STAMP(8 + 6 * j);
-        if (warp == 0) {
-            tc_fence_after();
-            if (elect_one()) {
-                const uint32_t vb = sV + (j & 1u) * kTileQK;
-#pragma unroll
-                for (uint32_t ks = 0; ks < kBlockK / 16; ++ks)
-                    tc_mma_f16(tmem + 128u + 64u * (j & 1u), fm_desc(sP + ks * 256u, 128u, 2048u),
-                               fm_desc(vb + ks * 256u, 128u, 2048u), kIdescPV, ks > 0 ? 1u : 0u);
-                tc_commit(&bar_o);
-            }
-            __syncwarp();
-        }
-        if ((a.trace & 2) && tid == 0) {  // profiling: PV MMA latency in isolation
-            mbar_wait(&bar_o, j & 1u);
-            FM_STAMP(41 + 2 * j);
-        }
-    }
-    mbar_wait(&bar_o, (nblk - 1) & 1u);
-    tc_fence_after();
-    drain_o(nblk - 1, alpha_prev);
-
-    FM_STAMP(62);
-    // ---- epilogue: full row sum, normalise, binary16; 32 B of the row per thread
-    red[cg][row] = l;
-    __syncthreads();
-    float lsum = red[0][row];
-#pragma unroll
-    for (uint32_t g = 1; g < kColGroups; ++g) lsum += red[g][row];
-    const uint32_t grow = q0 + row;
-    if (grow < a.nq) {
-        const float inv = 1.0f / lsum;
-        __half* go = a.o + b * a.o_sb + h * a.o_sh + (uint64_t)grow * a.o_sn + cg * kOc;
-#pragma unroll
-        for (uint32_t c = 0; c < kOc / 8; ++c) {
-            uint4 w;
-            w.x = pack_half2_rn(o[c * 8 + 0] * inv, o[c * 8 + 1] * inv);
-            w.y = pack_half2_rn(o[c * 8 + 2] * inv, o[c * 8 + 3] * inv);
-            w.z = pack_half2_rn(o[c * 8 + 4] * inv, o[c * 8 + 5] * inv);
-            w.w = pack_half2_rn(o[c * 8 + 6] * inv, o[c * 8 + 7] * inv);
-            *reinterpret_cast<uint4*>(go + c * 8) = w;
-        }
-    }
-    FM_STAMP(63);
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 0) {
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
-    }
-}
-
-// ---------------------------------------------------------------- v2 (product)
-// Two query tiles per CTA, warp-specialised (FA4-style ping-pong):
-//   warps 0-3  softmax warpgroup of query tile 0, warps 4-7 of tile 1
-//              (thread = query row = TMEM lane; tile t owns TMEM columns
-//              [256 t, 256 t + 256): S in the first 128, O_j double buffer)
-//   warp 8     MMA issuer for both tiles (S = Q K^T, O_j = P V)
-//   warp 9     loader: Q tiles, then a 3-stage K/V ring (cp.async, completion
-//              signalled with cp.async.mbarrier.arrive.noinc)
-// Hand-offs are mbarriers only (no CTA barrier in the loop):
-//   kv_full[st] / kv_empty[st]  loader <-> MMA warp
-//   s_full[t]   S_t(j) ready                   MMA -> softmax t
-//   p_full[t]   P_t(j) written, S_t(j) drained  softmax t -> MMA (4 warp arrivals)
-//   o_full[t][b] PV_t(j) retired, b = j&1      MMA -> softmax t
-// The MMA warp serves whichever tile published P first, and tile 1 starts
-// one softmax behind tile 0, so the two warpgroups take turns on the MUFU
-// (16 ex2/clk/SM, measured: tools/ubench_mufu.cu) while the other tile's S /
-// PV run on the tensor core.  The softmax streams its 128 scores through TMEM
-// twice in 32-column chunks (pass 1 row max; pass 2 exp2, row sum, binary16 P)
-// so S never occupies 128 registers.  160 + 64 KB smem, 512 TMEM columns,
-// one CTA per SM.
-constexpr uint32_t kLoadWarps = 4;      // cp.async issue is the K/V ring's bottleneck with one warp
-constexpr uint32_t kFm2Threads = (16 + 1 + kLoadWarps) * 32;  // softmax warps + MMA warp + load warps
+// ---------------------------------------------------------------- shared by v3 / v4
 constexpr uint32_t kKvStages = 4;  // K/V ring depth
 constexpr uint32_t kSmemFm2 = 2 * kTileQK + 2 * kKvStages * kTileQK + 2 * kTileP + 64;
 
@@ -465,260 +170,6 @@ __device__ __forceinline__ void frag_wait1(Frag& f) {
                    "+r"(f.r[31])
                  :
                  : "memory");
-}
-
-__global__ void __launch_bounds__(kFm2Threads, 1) flashmatch2_kernel(FmArgs a) {
-    __shared__ float red[2][2][kBlockQ];  // [tile][column half][row] partial maxima / sums
-    extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ uint32_t tmem_slot;
-    __shared__ __align__(8) uint64_t s_full[2], p_full[2], o_full[2][2];
-    __shared__ __align__(8) uint64_t kv_full[kKvStages], kv_empty[kKvStages];
-    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
-    const uint32_t q0 = blockIdx.x * 2 * kBlockQ, h = blockIdx.y, b = blockIdx.z;
-    FM_STAMP(0);
-    // smem: Q[2] | K ring | V ring | P[2]
-    const uint32_t sQ = smem_addr(smem);
-    const uint32_t sK = sQ + 2 * kTileQK, sV = sK + kKvStages * kTileQK, sP = sV + kKvStages * kTileQK;
-    uint8_t* pP0 = smem + (2 + 2 * kKvStages) * kTileQK;
-    const uint32_t nblk = (a.nkv + kBlockK - 1) / kBlockK;
-
-    if (tid == 0) {
-        for (int t = 0; t < 2; ++t) {
-            mbar_init(&s_full[t], 1);
-            mbar_init(&p_full[t], 8);  // the tile's 8 softmax warps
-            mbar_init(&o_full[t][0], 1);
-            mbar_init(&o_full[t][1], 1);
-        }
-        for (uint32_t st = 0; st < kKvStages; ++st) {
-            mbar_init(&kv_full[st], 32 * kLoadWarps);  // one cp.async.mbarrier.arrive.noinc per loader lane
-            mbar_init(&kv_empty[st], 1);  // one tcgen05.commit after the block's last PV
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_slot)),
-                     "r"(512u));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = tmem_slot;
-    FM_STAMP(34);
-
-    if (warp >= 17) {
-        // ---------------- loader
-        const __half* gq = a.q + b * a.q_sb + h * a.q_sh + (uint64_t)q0 * a.q_sn;
-        const __half* gk = a.k + b * a.k_sb + h * a.k_sh;
-        const __half* gv = a.v + b * a.v_sb + h * a.v_sh;
-        const uint32_t qvalid = a.nq - q0;
-        const uint32_t part = warp - 17;
-        if (part == 0) FM_STAMP_L(30);
-        load_tile_warp<false>(sQ, gq, a.q_sn, qvalid, part, kLoadWarps);
-        if (qvalid > kBlockQ)
-            load_tile_warp<false>(sQ + kTileQK, gq + (uint64_t)kBlockQ * a.q_sn, a.q_sn, qvalid - kBlockQ, part,
-                                  kLoadWarps);
-        if (part == 0) FM_STAMP_L(31);
-        for (uint32_t blk = 0; blk < nblk; ++blk) {
-            const uint32_t st = blk % kKvStages;
-            mbar_wait(&kv_empty[st], ((blk / kKvStages) & 1u) ^ 1u);
-            load_tile_warp<false>(sK + st * kTileQK, gk + (uint64_t)blk * kBlockK * a.k_sn, a.k_sn,
-                                  a.nkv - blk * kBlockK, part, kLoadWarps);
-            load_tile_warp<true>(sV + st * kTileQK, gv + (uint64_t)blk * kBlockK * a.v_sn, a.v_sn,
-                                 a.nkv - blk * kBlockK, part, kLoadWarps);
-            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(&kv_full[st]))
-                         : "memory");
-        }
-    } else if (warp == 16) {
-        // ---------------- MMA warp
-        auto kv_ready = [&](uint32_t blk) {
-            mbar_wait(&kv_full[blk % kKvStages], (blk / kKvStages) & 1u);
-            fence_async_smem();
-        };
-        auto issue_s = [&](uint32_t t, uint32_t blk) {
-            tc_fence_after();
-            if (elect_one()) {
-                const uint32_t kb = sK + (blk % kKvStages) * kTileQK, qb = sQ + t * kTileQK;
-#pragma unroll
-                for (uint32_t ks = 0; ks < kHd / 16; ++ks)
-                    tc_mma_f16(tmem + t * 256u, fm_desc(qb + ks * 256u, 128u, 1024u),
-                               fm_desc(kb + ks * 256u, 128u, 1024u), kIdescS, ks > 0 ? 1u : 0u);
-                tc_commit(&s_full[t]);
-            }
-            __syncwarp();
-        };
-        kv_ready(0);  // also covers Q (issued before K0/V0 by the same lanes)
-        FM_STAMP_L(33);
-        issue_s(0, 0);
-        FM_STAMP(1);
-        uint32_t jt[2] = {0, 0};  // next block whose PV each tile needs
-        bool started1 = false;
-        while (jt[0] < nblk || jt[1] < nblk) {
-#pragma unroll
-            for (uint32_t t = 0; t < 2; ++t) {
-                const uint32_t j = jt[t];
-                if (j >= nblk || (t == 1 && !started1)) continue;
-                if (!mbar_test(&p_full[t], j & 1u)) continue;
-                if (t == 0 && lane == 0 && a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && j < 6)
-                    g_fm_trace[48 + 2 * j] = clock64();
-                tc_fence_after();
-                // the second tile to finish block j is the last reader of K_j / V_j
-                const bool last_reader = jt[t ^ 1u] > j;
-                // S_t(j+1) first: the softmax waits on it, while PV_t(j) is only
-                // needed after the next block's row-max pass
-                if (j + 1 < nblk) {
-                    // the tile that reaches block j+1 first waits for its K/V
-                    if (jt[t ^ 1u] <= j + 1) kv_ready(j + 1);
-                    if (t == 0 && lane == 0 && a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 &&
-                        j < 6)
-                        g_fm_trace[49 + 2 * j] = clock64();
-                    issue_s(t, j + 1);  // softmax t drained S_t(j) before p_full
-                }
-                if (elect_one()) {
-                    const uint32_t vb = sV + (j % kKvStages) * kTileQK, pb = sP + t * kTileP;
-#pragma unroll
-                    for (uint32_t ks = 0; ks < kBlockK / 16; ++ks)
-                        tc_mma_f16(tmem + t * 256u + 128u + 64u * (j & 1u), fm_desc(pb + ks * 256u, 128u, 2048u),
-                                   fm_desc(vb + ks * 256u, 128u, 2048u), kIdescPV, ks > 0 ? 1u : 0u);
-                    tc_commit(&o_full[t][j & 1u]);
-                    if (last_reader) tc_commit(&kv_empty[j % kKvStages]);
-                }
-                __syncwarp();
-                jt[t] = j + 1;
-                if (t == 0 && !started1) {  // tile 1 starts one softmax behind tile 0
-                    issue_s(1, 0);
-                    started1 = true;
-                }
-                if (t == 0 && lane == 0 && a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 &&
-                    j < 16)
-                    g_fm_trace[40 + j] = clock64();
-            }
-        }
-    } else {
-        // ---------------- softmax warpgroup t: warps 8t..8t+7; warp w reads TMEM
-        // lane quadrant w%4 and column half hf = (w/4)%2, i.e. two threads per
-        // query row, each owning 64 of the 128 key columns and 32 of the 64
-        // O columns; the row max / row sum halves meet in shared memory
-        const uint32_t t = warp >> 3, hf = (warp >> 2) & 1u, row = ((warp & 3u) << 5) | lane;
-        const uint32_t lane_base = ((warp & 3u) * 32u) << 16;
-        const uint32_t tbase = tmem + t * 256u;
-        uint8_t* pP = pP0 + t * kTileP;
-        float o[kHd / 2];
-#pragma unroll
-        for (uint32_t i = 0; i < kHd / 2; ++i) o[i] = 0.0f;
-        float m = -INFINITY, l = 0.0f, alpha_prev = 0.0f;
-        const float sl2 = a.scale_log2;
-        auto tile_sync = [&]() { asm volatile("bar.sync %0, 256;" ::"r"(1u + t) : "memory"); };
-        auto drain_o = [&](uint32_t jj, float alpha) {
-            Frag g;
-            frag_ld(tbase + lane_base + 128u + 64u * (jj & 1u) + 32u * hf, g);
-            frag_wait1(g);
-#pragma unroll
-            for (uint32_t i = 0; i < 32; ++i) o[i] = fmaf(o[i], alpha, __uint_as_float(g.r[i]));
-        };
-        for (uint32_t j = 0; j < nblk; ++j) {
-            mbar_wait(&s_full[t], j & 1u);
-            if (t == 0) FM_STAMP(3 + j);
-            tc_fence_after();
-            const uint32_t kvalid = a.nkv - j * kBlockK;
-            // pass 1: partial row max over this thread's 64 columns
-            float mx = -INFINITY;
-#pragma unroll
-            for (uint32_t c = 0; c < 2; ++c) {
-                const uint32_t col0 = hf * 64u + c * 32u;
-                Frag f;
-                frag_ld(tbase + lane_base + col0, f);
-                frag_wait1(f);
-                if (kvalid < kBlockK) {
-#pragma unroll
-                    for (uint32_t i = 0; i < 32; ++i)
-                        if (col0 + i >= kvalid) f.r[i] = __float_as_uint(-INFINITY);
-                }
-                float r4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-                for (uint32_t i = 0; i < 32; i += 8)
-#pragma unroll
-                    for (uint32_t u = 0; u < 4; ++u)
-                        r4[u] = max3(r4[u], __uint_as_float(f.r[i + 2 * u]), __uint_as_float(f.r[i + 2 * u + 1]));
-                mx = max3(mx, fmaxf(r4[0], r4[1]), fmaxf(r4[2], r4[3]));
-            }
-            red[t][hf][row] = mx;
-            tile_sync();
-            mx = fmaxf(mx, red[t][hf ^ 1u][row]);
-            tile_sync();  // both halves read before either writes the next block's maximum
-            const float m_new = fmaxf(m, mx * sl2);
-            const float alpha = ex2(m - m_new);
-            if (t == 0 && j < 8) FM_STAMP(10 + j);
-            // P_{j-1} / O_{j-1}: PV_t(j-1) must have retired before P is overwritten
-            if (j > 0) {
-                mbar_wait(&o_full[t][(j - 1) & 1u], ((j - 1) >> 1) & 1u);
-                tc_fence_after();
-            }
-            // pass 2: exp2, partial row sum, binary16 P for this thread's 64 columns
-            float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-            for (uint32_t c = 0; c < 2; ++c) {
-                const uint32_t col0 = hf * 64u + c * 32u;
-                Frag f;
-                frag_ld(tbase + lane_base + col0, f);
-                frag_wait1(f);
-                if (kvalid < kBlockK) {
-#pragma unroll
-                    for (uint32_t i = 0; i < 32; ++i)
-                        if (col0 + i >= kvalid) f.r[i] = __float_as_uint(-INFINITY);
-                }
-#pragma unroll
-                for (uint32_t q = 0; q < 4; ++q) {
-                    float p[8];
-#pragma unroll
-                    for (uint32_t i = 0; i < 8; ++i) p[i] = ex2(fmaf(__uint_as_float(f.r[q * 8 + i]), sl2, -m_new));
-                    acc[q] += ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
-                    uint4 w;
-                    w.x = pack_half2_rn(p[0], p[1]);
-                    w.y = pack_half2_rn(p[2], p[3]);
-                    w.z = pack_half2_rn(p[4], p[5]);
-                    w.w = pack_half2_rn(p[6], p[7]);
-                    *reinterpret_cast<uint4*>(pP + off_p(row, col0 / 8u + q)) = w;
-                }
-            }
-            tc_fence_before();
-            fence_async_smem();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&p_full[t]);  // this warp's part of P_t(j) written, S drained
-            if (t == 0) FM_STAMP(20 + j);
-            if (j > 0) drain_o(j - 1, alpha_prev);
-            l = l * alpha + ((acc[0] + acc[1]) + (acc[2] + acc[3]));  // partial: this thread's columns
-            m = m_new;
-            alpha_prev = alpha;
-        }
-        mbar_wait(&o_full[t][(nblk - 1) & 1u], ((nblk - 1) >> 1) & 1u);
-        tc_fence_after();
-        drain_o(nblk - 1, alpha_prev);
-        red[t][hf][row] = l;
-        tile_sync();
-        l += red[t][hf ^ 1u][row];
-        const uint32_t grow = q0 + t * kBlockQ + row;
-        if (grow < a.nq) {
-            const float inv = 1.0f / l;
-            __half* go = a.o + b * a.o_sb + h * a.o_sh + (uint64_t)grow * a.o_sn + hf * 32u;
-#pragma unroll
-            for (uint32_t c = 0; c < kHd / 16; ++c) {
-                uint4 w;
-                w.x = pack_half2_rn(o[c * 8 + 0] * inv, o[c * 8 + 1] * inv);
-                w.y = pack_half2_rn(o[c * 8 + 2] * inv, o[c * 8 + 3] * inv);
-                w.z = pack_half2_rn(o[c * 8 + 4] * inv, o[c * 8 + 5] * inv);
-                w.w = pack_half2_rn(o[c * 8 + 6] * inv, o[c * 8 + 7] * inv);
-                *reinterpret_cast<uint4*>(go + c * 8) = w;
-            }
-        }
-    }
-    FM_STAMP(63);
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 0) {
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
-    }
 }
 
 // ---------------------------------------------------------------- K7 v3
@@ -1248,8 +699,6 @@ int flashmatch_forward(fnl_context* ctx, const fnl_attention_desc& d) {
         if (p % 16) return fail(FNL_EINVAL, "flashmatch: tensors must be 16 B aligned");
     if (d.heads > 65535 || d.batch > 65535) return fail(FNL_EINVAL, "flashmatch: batch/heads exceed 65535");
     if (!fm_attr_done) {
-        FNL_CUDA_TRY(cudaFuncSetAttribute(flashmatch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFm));
-        FNL_CUDA_TRY(cudaFuncSetAttribute(flashmatch2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFm2));
         FNL_CUDA_TRY(cudaFuncSetAttribute(flashmatch3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFm2));
         FNL_CUDA_TRY(cudaFuncSetAttribute(flashmatch4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFm4));
         fm_attr_done = true;
@@ -1269,11 +718,10 @@ int flashmatch_forward(fnl_context* ctx, const fnl_attention_desc& d) {
     a.scale_log2 = d.scale * 1.4426950408889634f;
     static const int trace = getenv("FNL_FM_TRACE") ? atoi(getenv("FNL_FM_TRACE")) : 0;
     a.trace = trace;
-    dim3 grid((d.nq + kBlockQ - 1) / kBlockQ, d.heads, d.batch);
     cudaStream_t s = ctx_stream(ctx);
     ProfScope prof(ctx, FNL_KCLASS_ATTN);
-    // v2 (warp-specialised, two query tiles per CTA) is the product kernel;
-    // FNL_FM_VERSION=1 selects the barrier-synchronous v1 for comparison
+    // v4 (TMA loads) is the product kernel; FNL_FM_VERSION=3 selects the
+    // cp.async-loader v3 for comparison
     static const int ver = getenv("FNL_FM_VERSION") ? atoi(getenv("FNL_FM_VERSION")) : 4;
     if (ver == 4) {
         // TMA tensor maps of Q, K, V viewed as [batch][heads][rows][64] binary16
@@ -1311,14 +759,10 @@ int flashmatch_forward(fnl_context* ctx, const fnl_attention_desc& d) {
                                                        : (tiles1 <= (uint64_t)ctx_sm_count(ctx) ? 1u : 2u);
         flashmatch4_kernel<<<dim3((d.nq + a.tiles * kBlockQ - 1) / (a.tiles * kBlockQ), d.heads, d.batch), kFm4Threads,
                              kSmemFm4, s>>>(a, tq, tk, tv);
-    } else if (ver == 1)
-        flashmatch_kernel<<<grid, kFmThreads, kSmemFm, s>>>(a);
-    else if (ver == 3)
+    } else {
         flashmatch3_kernel<<<dim3((d.nq + 2 * kBlockQ - 1) / (2 * kBlockQ), d.heads, d.batch), kFm3Threads,
                              kSmemFm2, s>>>(a);
-    else
-        flashmatch2_kernel<<<dim3((d.nq + 2 * kBlockQ - 1) / (2 * kBlockQ), d.heads, d.batch), kFm2Threads,
-                             kSmemFm2, s>>>(a);
+    }
     FNL_CUDA_TRY(cudaGetLastError());
     ctx_count_launches(ctx, 1);
     return FNL_OK;
