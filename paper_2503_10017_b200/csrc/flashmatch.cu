@@ -432,7 +432,6 @@ __global__ void __launch_bounds__(kFm3Threads, 1) flashmatch3_kernel(FmArgs a) {
 // = +32 B), V MN-major (hd contiguous, 8-key atoms 1 KB apart, K step of 16
 // keys = +2 KB).  P keeps the no-swizzle layout the softmax writes.
 constexpr uint32_t kKvStages4 = 3;
-constexpr uint32_t kFm4Threads = (16 + 1 + 1) * 32;
 constexpr uint32_t kSmemFm4 = 2 * kTileQK + 2 * kKvStages4 * kTileQK + 2 * kTileP + 1024;  // + alignment slack
 
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -448,10 +447,19 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map
         : "memory");
 }
 
-__global__ void __launch_bounds__(kFm4Threads, 1)
+// kH = threads per query row (2: 16 softmax warps, 64 key columns each, row
+// max / sum halves meet in shared memory; 1: 8 softmax warps, a whole
+// 128-column row per thread in 128 registers, no exchange).
+template <int kH>
+__global__ void __launch_bounds__((8 * kH + 2) * 32, 1)
     flashmatch4_kernel(FmArgs a, const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                        const __grid_constant__ CUtensorMap tv) {
-    __shared__ float red[2][2][kBlockQ];  // [tile][column half][row] partial maxima / sums
+    constexpr uint32_t kSoftWarps = 8 * kH;          // both tiles
+    constexpr uint32_t kTileWarps = 4 * kH;          // per tile
+    constexpr uint32_t kCols = kBlockK / kH;         // key columns per thread
+    constexpr uint32_t kSF = kCols / 32;             // 32-column S fragments per thread
+    constexpr uint32_t kOF = kHd / kH / 32;          // 32-column O fragments per thread
+    __shared__ float red[2][2][kBlockQ];  // [tile][column half][row] partial maxima / sums (kH = 2)
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint32_t tmem_slot;
     __shared__ __align__(8) uint64_t s_full[2], s_free[2], p_full[2], o_full[2];
@@ -469,8 +477,8 @@ __global__ void __launch_bounds__(kFm4Threads, 1)
     if (tid == 0) {
         for (int t = 0; t < 2; ++t) {
             mbar_init(&s_full[t], 1);
-            mbar_init(&s_free[t], 8);  // the tile's 8 softmax warps
-            mbar_init(&p_full[t], 8);
+            mbar_init(&s_free[t], kTileWarps);
+            mbar_init(&p_full[t], kTileWarps);
             mbar_init(&o_full[t], 1);
         }
         for (uint32_t st = 0; st < kKvStages4; ++st) {
@@ -478,6 +486,13 @@ __global__ void __launch_bounds__(kFm4Threads, 1)
             mbar_init(&kv_empty[st], 1);  // one tcgen05.commit after the block's last PV
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        // the first boxes go out before the CTA-wide barrier / TMEM allocation
+        const int hh = (int)h, bb = (int)b;
+        mbar_expect_tx(&kv_full[0], (ntile + 2) * kTileQK);
+        tma_load_4d(sQ, &tq, 0, (int)q0, hh, bb, &kv_full[0]);
+        if (ntile == 2) tma_load_4d(sQ + kTileQK, &tq, 0, (int)(q0 + kBlockQ), hh, bb, &kv_full[0]);
+        tma_load_4d(sK, &tk, 0, 0, hh, bb, &kv_full[0]);
+        tma_load_4d(sV, &tv, 0, 0, hh, bb, &kv_full[0]);
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_slot)),
@@ -490,16 +505,10 @@ __global__ void __launch_bounds__(kFm4Threads, 1)
     const uint32_t tmem = tmem_slot;
     FM_STAMP(34);
 
-    if (warp == 17) {
-        // ---------------- loader: one elected thread issues every TMA box
+    if (warp == kSoftWarps + 1) {
+        // ---------------- loader: one elected thread issues the remaining TMA boxes
         if (elect_one()) {
             const int hh = (int)h, bb = (int)b;
-            // Q tiles ride on K/V stage 0's barrier (the first S needs all three)
-            mbar_expect_tx(&kv_full[0], (ntile + 2) * kTileQK);
-            tma_load_4d(sQ, &tq, 0, (int)q0, hh, bb, &kv_full[0]);
-            if (ntile == 2) tma_load_4d(sQ + kTileQK, &tq, 0, (int)(q0 + kBlockQ), hh, bb, &kv_full[0]);
-            tma_load_4d(sK, &tk, 0, 0, hh, bb, &kv_full[0]);
-            tma_load_4d(sV, &tv, 0, 0, hh, bb, &kv_full[0]);
             for (uint32_t blk = 1; blk < nblk; ++blk) {
                 const uint32_t st = blk % kKvStages4;
                 mbar_wait(&kv_empty[st], ((blk / kKvStages4) & 1u) ^ 1u);
@@ -509,7 +518,7 @@ __global__ void __launch_bounds__(kFm4Threads, 1)
             }
         }
         __syncwarp();
-    } else if (warp == 16) {
+    } else if (warp == kSoftWarps) {
         // ---------------- MMA warp: S_t(j+1) as soon as S_t(j) is drained,
         // PV_t(j) as soon as P_t(j) is published
         auto kv_ready = [&](uint32_t blk) {
@@ -527,7 +536,7 @@ __global__ void __launch_bounds__(kFm4Threads, 1)
             }
             __syncwarp();
         };
-        kv_ready(0);  // also covers Q (issued before K0/V0 by the same lanes)
+        kv_ready(0);  // also covers Q (same barrier phase)
         issue_s(0, 0);
         if (ntile == 2) issue_s(1, 0);
         // a single-tile CTA never serves tile 1
@@ -558,50 +567,53 @@ __global__ void __launch_bounds__(kFm4Threads, 1)
                 }
             }
         }
-    } else if ((warp >> 3) < ntile) {
-        // ---------------- softmax warpgroup t: warps 8t..8t+7; warp w reads TMEM
-        // lane quadrant w%4 and column half hf = (w/4)%2: two threads per query
-        // row, 64 key columns and 32 O columns each
-        const uint32_t t = warp >> 3, hf = (warp >> 2) & 1u, row = ((warp & 3u) << 5) | lane;
+    } else if (warp / kTileWarps < ntile) {
+        // ---------------- softmax warpgroup t: warp w reads TMEM lane quadrant
+        // w%4 and key-column part hf = (w/4)%kH
+        const uint32_t t = warp / kTileWarps, hf = (warp >> 2) % kH, row = ((warp & 3u) << 5) | lane;
         const uint32_t lane_base = ((warp & 3u) * 32u) << 16;
-        const uint32_t tS = tmem + lane_base + t * 256u, tO = tS + 128u + 32u * hf;
+        const uint32_t tS = tmem + lane_base + t * 256u + hf * kCols, tO = tmem + lane_base + t * 256u + 128u + hf * (kHd / kH);
         uint8_t* pP = pP0 + t * kTileP;
         float m = -INFINITY, l = 0.0f;
         const float sl2 = a.scale_log2;
-        auto tile_sync = [&]() { asm volatile("bar.sync %0, 256;" ::"r"(1u + t) : "memory"); };
+        auto tile_sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1u + t), "r"(kTileWarps * 32) : "memory"); };
         for (uint32_t j = 0; j < nblk; ++j) {
             mbar_wait(&s_full[t], j & 1u);
             if (t == 0) FM_STAMP(3 + j);
             tc_fence_after();
-            Frag f0, f1;
-            frag_ld64(tS + hf * 64u, f0, f1);
-            frag_wait2(f0, f1);
+            Frag f[kSF];
+#pragma unroll
+            for (uint32_t c = 0; c < kSF; c += 2) frag_ld64(tS + c * 32u, f[c], f[c + 1]);
+#pragma unroll
+            for (uint32_t c = 0; c < kSF; c += 2) frag_wait2(f[c], f[c + 1]);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&s_free[t]);  // S_t(j) is in registers: S_t(j+1) may overwrite it
             const uint32_t kvalid = a.nkv - j * kBlockK;
             if (kvalid < kBlockK) {
 #pragma unroll
-                for (uint32_t i = 0; i < 32; ++i) {
-                    if (hf * 64u + i >= kvalid) f0.r[i] = __float_as_uint(-INFINITY);
-                    if (hf * 64u + 32u + i >= kvalid) f1.r[i] = __float_as_uint(-INFINITY);
-                }
+                for (uint32_t c = 0; c < kSF; ++c)
+#pragma unroll
+                    for (uint32_t i = 0; i < 32; ++i)
+                        if (hf * kCols + c * 32u + i >= kvalid) f[c].r[i] = __float_as_uint(-INFINITY);
             }
             float r4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-            for (uint32_t i = 0; i < 32; i += 8)
+            for (uint32_t c = 0; c < kSF; ++c)
 #pragma unroll
-                for (uint32_t u = 0; u < 4; ++u) {
-                    r4[u] = max3(r4[u], __uint_as_float(f0.r[i + 2 * u]), __uint_as_float(f0.r[i + 2 * u + 1]));
-                    r4[u] = max3(r4[u], __uint_as_float(f1.r[i + 2 * u]), __uint_as_float(f1.r[i + 2 * u + 1]));
-                }
+                for (uint32_t i = 0; i < 32; i += 8)
+#pragma unroll
+                    for (uint32_t u = 0; u < 4; ++u)
+                        r4[u] = max3(r4[u], __uint_as_float(f[c].r[i + 2 * u]), __uint_as_float(f[c].r[i + 2 * u + 1]));
             float mx = fmaxf(fmaxf(r4[0], r4[1]), fmaxf(r4[2], r4[3]));
-            red[t][hf][row] = mx;
-            tile_sync();
-            mx = fmaxf(mx, red[t][hf ^ 1u][row]);
-            tile_sync();  // both halves read before either writes the next value
+            if (kH == 2) {
+                red[t][hf][row] = mx;
+                tile_sync();
+                mx = fmaxf(mx, red[t][hf ^ 1u][row]);
+                tile_sync();  // both halves read before either writes the next value
+            }
             // lazy rescale: keep the stale max unless the row max grew by more
-            // than 2^kRescaleLog2 (both threads of a row decide identically)
+            // than 2^kRescaleLog2 (the threads of a row decide identically)
             const float mc = mx * sl2;
             const bool grow = mc > m + kRescaleLog2;
             const float m_new = grow ? mc : m;
@@ -614,14 +626,13 @@ __global__ void __launch_bounds__(kFm4Threads, 1)
             }
             float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (uint32_t c = 0; c < 2; ++c) {
-                const Frag& f = c ? f1 : f0;
-                const uint32_t col0 = hf * 64u + c * 32u;
+            for (uint32_t c = 0; c < kSF; ++c) {
+                const uint32_t col0 = hf * kCols + c * 32u;
 #pragma unroll
                 for (uint32_t q = 0; q < 4; ++q) {
                     float p[8];
 #pragma unroll
-                    for (uint32_t i = 0; i < 8; ++i) p[i] = ex2(fmaf(__uint_as_float(f.r[q * 8 + i]), sl2, -m_new));
+                    for (uint32_t i = 0; i < 8; ++i) p[i] = ex2(fmaf(__uint_as_float(f[c].r[q * 8 + i]), sl2, -m_new));
                     acc[q] += ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
                     uint4 w;
                     w.x = pack_half2_rn(p[0], p[1]);
@@ -632,12 +643,15 @@ __global__ void __launch_bounds__(kFm4Threads, 1)
                 }
             }
             if (__any_sync(0xFFFFFFFFu, alpha != 1.0f)) {  // warp-collective TMEM round trip of O
-                Frag o;
-                frag_ld(tO, o);
-                frag_wait1(o);
 #pragma unroll
-                for (uint32_t i = 0; i < 32; ++i) o.r[i] = __float_as_uint(__uint_as_float(o.r[i]) * alpha);
-                frag_st(tO, o);
+                for (uint32_t c = 0; c < kOF; ++c) {
+                    Frag o;
+                    frag_ld(tO + c * 32u, o);
+                    frag_wait1(o);
+#pragma unroll
+                    for (uint32_t i = 0; i < 32; ++i) o.r[i] = __float_as_uint(__uint_as_float(o.r[i]) * alpha);
+                    frag_st(tO + c * 32u, o);
+                }
                 tmem_st_wait();
             }
             tc_fence_before();
@@ -645,29 +659,34 @@ __global__ void __launch_bounds__(kFm4Threads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&p_full[t]);  // P_t(j) written, O_t rescaled
             if (t == 0) FM_STAMP(20 + j);
-            l = l * alpha + ((acc[0] + acc[1]) + (acc[2] + acc[3]));  // partial: this thread's columns
+            l = l * alpha + ((acc[0] + acc[1]) + (acc[2] + acc[3]));  // partial when kH = 2
             m = m_new;
         }
         mbar_wait(&o_full[t], (nblk - 1) & 1u);
         tc_fence_after();
-        Frag o;
-        frag_ld(tO, o);
-        frag_wait1(o);
-        red[t][hf][row] = l;
-        tile_sync();
-        l += red[t][hf ^ 1u][row];
+        if (kH == 2) {
+            red[t][hf][row] = l;
+            tile_sync();
+            l += red[t][hf ^ 1u][row];
+        }
         const uint32_t grow_ = q0 + t * kBlockQ + row;
-        if (grow_ < a.nq) {
-            const float inv = 1.0f / l;
-            __half* go = a.o + b * a.o_sb + h * a.o_sh + (uint64_t)grow_ * a.o_sn + hf * 32u;
+        const float inv = 1.0f / l;
 #pragma unroll
-            for (uint32_t c = 0; c < kHd / 16; ++c) {
-                uint4 w;
-                w.x = pack_half2_rn(__uint_as_float(o.r[c * 8 + 0]) * inv, __uint_as_float(o.r[c * 8 + 1]) * inv);
-                w.y = pack_half2_rn(__uint_as_float(o.r[c * 8 + 2]) * inv, __uint_as_float(o.r[c * 8 + 3]) * inv);
-                w.z = pack_half2_rn(__uint_as_float(o.r[c * 8 + 4]) * inv, __uint_as_float(o.r[c * 8 + 5]) * inv);
-                w.w = pack_half2_rn(__uint_as_float(o.r[c * 8 + 6]) * inv, __uint_as_float(o.r[c * 8 + 7]) * inv);
-                *reinterpret_cast<uint4*>(go + c * 8) = w;
+        for (uint32_t c = 0; c < kOF; ++c) {
+            Frag o;
+            frag_ld(tO + c * 32u, o);
+            frag_wait1(o);
+            if (grow_ < a.nq) {
+                __half* go = a.o + b * a.o_sb + h * a.o_sh + (uint64_t)grow_ * a.o_sn + hf * (kHd / kH) + c * 32u;
+#pragma unroll
+                for (uint32_t q = 0; q < 4; ++q) {
+                    uint4 w;
+                    w.x = pack_half2_rn(__uint_as_float(o.r[q * 8 + 0]) * inv, __uint_as_float(o.r[q * 8 + 1]) * inv);
+                    w.y = pack_half2_rn(__uint_as_float(o.r[q * 8 + 2]) * inv, __uint_as_float(o.r[q * 8 + 3]) * inv);
+                    w.z = pack_half2_rn(__uint_as_float(o.r[q * 8 + 4]) * inv, __uint_as_float(o.r[q * 8 + 5]) * inv);
+                    w.w = pack_half2_rn(__uint_as_float(o.r[q * 8 + 6]) * inv, __uint_as_float(o.r[q * 8 + 7]) * inv);
+                    *reinterpret_cast<uint4*>(go + q * 8) = w;
+                }
             }
         }
     }
@@ -700,7 +719,8 @@ int flashmatch_forward(fnl_context* ctx, const fnl_attention_desc& d) {
     if (d.heads > 65535 || d.batch > 65535) return fail(FNL_EINVAL, "flashmatch: batch/heads exceed 65535");
     if (!fm_attr_done) {
         FNL_CUDA_TRY(cudaFuncSetAttribute(flashmatch3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFm2));
-        FNL_CUDA_TRY(cudaFuncSetAttribute(flashmatch4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFm4));
+        FNL_CUDA_TRY(cudaFuncSetAttribute(flashmatch4_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFm4));
+        FNL_CUDA_TRY(cudaFuncSetAttribute(flashmatch4_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFm4));
         fm_attr_done = true;
     }
     FmArgs a{};
@@ -757,8 +777,16 @@ int flashmatch_forward(fnl_context* ctx, const fnl_attention_desc& d) {
         static const int force_tiles = getenv("FNL_FM_TILES") ? atoi(getenv("FNL_FM_TILES")) : 0;
         a.tiles = force_tiles == 1 || force_tiles == 2 ? (uint32_t)force_tiles
                                                        : (tiles1 <= (uint64_t)ctx_sm_count(ctx) ? 1u : 2u);
-        flashmatch4_kernel<<<dim3((d.nq + a.tiles * kBlockQ - 1) / (a.tiles * kBlockQ), d.heads, d.batch), kFm4Threads,
-                             kSmemFm4, s>>>(a, tq, tk, tv);
+        // threads per query row: a whole row per thread when the CTA has one
+        // tile (measured 11.2 vs 11.7 us per decoder launch), two otherwise
+        // (15.2 vs 15.9 us per encoder launch)
+        static const int force_rt = getenv("FNL_FM_ROW_THREADS") ? atoi(getenv("FNL_FM_ROW_THREADS")) : 0;
+        const int row_threads = force_rt == 1 || force_rt == 2 ? force_rt : (a.tiles == 1 ? 1 : 2);
+        const dim3 grid4((d.nq + a.tiles * kBlockQ - 1) / (a.tiles * kBlockQ), d.heads, d.batch);
+        if (row_threads == 1)
+            flashmatch4_kernel<1><<<grid4, (8 * 1 + 2) * 32, kSmemFm4, s>>>(a, tq, tk, tv);
+        else
+            flashmatch4_kernel<2><<<grid4, (8 * 2 + 2) * 32, kSmemFm4, s>>>(a, tq, tk, tv);
     } else {
         flashmatch3_kernel<<<dim3((d.nq + 2 * kBlockQ - 1) / (2 * kBlockQ), d.heads, d.batch), kFm3Threads,
                              kSmemFm2, s>>>(a);
