@@ -969,7 +969,7 @@ extern "C" int fnl_reciprocal_match_batch(fnl_context* ctx, uint32_t npairs, con
         const uint32_t n = std::min(std::min(want, max_sub), npairs - first);
         sched.push_back({first, n});
         first += n;
-        want *= 2;
+        want = std::min(2 * want, max_sub);  // capped: a doubling uint32 would wrap to 0 after 29 sub-batches
     }
     const uint32_t sub = max_sub;
     float* dbuf[2][2];

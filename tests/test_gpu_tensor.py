@@ -181,3 +181,20 @@ def test_confidence_compaction_equals_post_filter(fnl, ref, metric):
     for p in range(B):
         assert np.array_equal(kept[p], full[p][dists[p] <= np.float32(thr)])
     assert 0 < sum(len(k) for k in kept) < sum(len(f) for f in full)
+
+
+def test_batch_over_1024_pairs(fnl, ref):
+    """More pairs than one plan-kernel chunk (1024): the device-built work
+    lists (K2p) must scan across chunks; every pair equals the exact CUDA
+    `single` backend on the same binary16-rounded maps."""
+    P = 1100
+    base1 = [h16(ref.gen_random(16, 12, 24, 3000 + k)) for k in range(8)]
+    base2 = [h16(ref.gen_random(16, 12, 24, 4000 + k)) for k in range(8)]
+    D1 = np.stack([base1[k % 8] for k in range(P)])
+    D2 = np.stack([base2[(k // 8) % 8] for k in range(P)])
+    pt, ct, st = fnl.reciprocal_match_batch(D1, D2, backend="tensor", metric="dot", stride=2)
+    ps, cs, ss = fnl.reciprocal_match_batch(D1, D2, backend="single", metric="dot", stride=2)
+    assert np.array_equal(ct, cs)
+    for k in range(P):
+        assert np.array_equal(pt[k, : ct[k]], ps[k, : cs[k]])
+        assert st[k]["active_history"] == ss[k]["active_history"]
