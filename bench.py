@@ -115,24 +115,30 @@ class ClockSampler:
             self.thread.join(timeout=2)
 
     def summary(self):
-        rows = []
+        parsed = []
         for ts, line in self.lines:
-            if self.t0 is not None and ts < self.t0:
-                continue
-            if self.t1 is not None and ts > self.t1 + 0.05:
-                continue
             parts = [p.strip() for p in line.split(",")]
             if len(parts) >= 7:
                 try:
-                    rows.append((float(parts[0]), float(parts[1]), parts[3:7]))
+                    parsed.append((ts, (float(parts[0]), float(parts[1]), parts[3:7])))
                 except ValueError:
                     pass
+        rows = [r for ts, r in parsed if (self.t0 is None or ts >= self.t0) and (self.t1 is None or ts <= self.t1 + 0.05)]
+        nearest = False
+        if not rows and parsed and self.t0 is not None:
+            # timed region shorter than the sampling period: the sample nearest to it
+            mid = 0.5 * (self.t0 + (self.t1 or self.t0))
+            rows = [min(parsed, key=lambda x: abs(x[0] - mid))[1]]
+            nearest = True
         if not rows:
             return None
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v.lower() == "active"})
-        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
-                "reasons": reasons, "samples": len(rows)}
+        out = {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+               "reasons": reasons, "samples": len(rows)}
+        if nearest:
+            out["nearest_sample"] = True
+        return out
 
 
 def dist_setup():
