@@ -123,14 +123,11 @@ struct FmArgs {
     uint64_t k_sb, k_sh, k_sn;
     uint64_t v_sb, v_sh, v_sn;
     uint64_t o_sb, o_sh, o_sn;
-    float scale_log2;
-    uint32_t tiles;  // query tiles per CTA (v4: 1 or 2)  // softmax scale * log2(e)
+    float scale_log2;  // softmax scale * log2(e)
+    uint32_t tiles;    // query tiles per CTA (v4: 1 or 2)
     int trace;
 };
 
-// 128 rows x 64 hd of a [token][hd] operand into smem.  Warp lanes: row%8 and
-// 4 consecutive 16 B chunks, so global reads are 64 B runs and every quarter
-// warp writes one 128 B core matrix.
 // ---------------------------------------------------------------- shared by v3 / v4
 constexpr uint32_t kKvStages = 4;  // K/V ring depth
 constexpr uint32_t kSmemFm2 = 2 * kTileQK + 2 * kKvStages * kTileQK + 2 * kTileP + 64;

@@ -899,21 +899,6 @@ uint32_t ceil_div_u(uint32_t a, uint32_t b) { return (a + b - 1) / b; }
         if (_st != FNL_OK) return _st; \
     } while (0)
 
-__global__ void stage_kernel(uint32_t* dst, const uint32_t* src, size_t words) {
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < words; i += (size_t)gridDim.x * blockDim.x)
-        dst[i] = src[i];
-}
-
-// dst (device) <- src (pinned host, mapped), via a kernel on the context stream
-int stage_from_host(fnl_context* ctx, uint32_t* dst, const uint32_t* src, size_t words) {
-    if (words == 0) return FNL_OK;
-    const uint32_t blocks = (uint32_t)std::min<size_t>(64, (words + 255) / 256);
-    stage_kernel<<<blocks, 256, 0, ctx_stream(ctx)>>>(dst, src, words);
-    FNL_CUDA_TRY(cudaGetLastError());
-    ctx_count_launches(ctx, 1);
-    return FNL_OK;
-}
-
 bool attr_done = false;
 
 int ensure_attrs() {
