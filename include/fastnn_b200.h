@@ -194,11 +194,34 @@ int fnl_mutual_nn_tensor(fnl_context* ctx, const float* h_d1, uint32_t h1, uint3
 typedef int (*fnl_key_reduce_fn)(void* user, int64_t* d_keys, uint64_t count, void* stream);
 typedef struct fnl_shard_spec {
     uint32_t rank, count;
-    int64_t* d_keys;          /* device, >= npairs * samples entries */
+    int64_t* d_keys;          /* device, >= npairs * samples entries (peer mode: 2x, see below) */
     uint64_t keys_capacity;
     fnl_key_reduce_fn reduce; /* returns 0 on success */
     void* user;
+    /* Optional peer-memory transport (replaces `reduce` when peer_keys != NULL;
+     * count <= 8): peer_keys[r] / peer_flags[r] are rank r's key buffer
+     * (2 * npairs * samples entries: one half per NN-pass parity, all
+     * INT64_MAX when the call starts; left that way on return) and barrier
+     * counter, mapped into this process (fnl_ipc_open; entry `rank` is this
+     * rank's own d_keys / flag).  The merge and rescan epilogues push every
+     * winner key into all ranks' buffers with a system-scope atomicMin over
+     * NVLink and a peer-memory barrier replaces the all-reduce.
+     * *barrier_seq (host, in/out) counts the barriers completed on these
+     * counters by earlier calls; all ranks must pass the same value. */
+    int64_t* const* peer_keys;
+    uint32_t* const* peer_flags;
+    uint64_t* barrier_seq;
 } fnl_shard_spec;
+
+/* Peer-memory buffers for fnl_shard_spec's peer transport: device allocations
+ * of their own (so CUDA IPC handles cover exactly them), filled with INT64_MAX
+ * (fill_key_none != 0, bytes a multiple of 8) or zero. */
+int fnl_p2p_alloc(fnl_context* ctx, uint64_t bytes, int fill_key_none, void** d_ptr);
+int fnl_p2p_free(void* d_ptr);
+/* CUDA IPC: 64-byte handle of a fnl_p2p_alloc buffer; open / close a peer's. */
+int fnl_ipc_handle(const void* d_ptr, unsigned char handle[64]);
+int fnl_ipc_open(fnl_context* ctx, const unsigned char handle[64], void** d_ptr);
+int fnl_ipc_close(void* d_ptr);
 int fnl_reciprocal_match_sharded_device(fnl_context* ctx, uint32_t npairs, const float* d_d1,
                                         const float* d_d2, uint32_t h, uint32_t w, uint32_t dim,
                                         const fnl_match_config* cfg, int backend,

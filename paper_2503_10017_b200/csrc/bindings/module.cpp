@@ -495,6 +495,81 @@ PYBIND11_MODULE(_fastnn, m) {
           py::arg("convergence") = 0.99, py::arg("metric") = "dot", py::arg("block_size") = 4096,
           py::arg("stream") = py::none());
 
+    // Same, with the peer-memory transport (keys pushed into every rank's
+    // buffer by the merge epilogues, peer-memory barrier instead of NCCL).
+    // Returns (stats, barrier_seq).
+    m.def("reciprocal_match_p2p_device",
+          [](std::uintptr_t d1, std::uintptr_t d2, std::uint32_t n, std::uint32_t h, std::uint32_t w,
+             std::uint32_t d, std::uintptr_t out_pairs, std::uintptr_t out_counts, std::uint64_t keys_capacity,
+             std::uint32_t rank, const std::vector<std::uintptr_t>& peer_keys,
+             const std::vector<std::uintptr_t>& peer_flags, std::uint64_t barrier_seq, const std::string& backend,
+             std::uint32_t k, std::uint32_t stride, std::uint32_t max_iters, double convergence,
+             const std::string& metric, std::uint32_t block_size, py::object stream) {
+              void* const sh = stream_handle(stream);  // with the GIL held
+              if (peer_keys.size() != peer_flags.size() || rank >= peer_keys.size())
+                  throw std::invalid_argument("reciprocal_match_p2p_device: one key buffer and flag per rank");
+              const auto cfg = make_cfg(k, stride, max_iters, convergence, metric, "full", block_size);
+              cfg.validate();
+              const auto cc = c_cfg(cfg);
+              const int be = c_backend(fastnn::backend_from_string(backend));
+              std::vector<fnl_run_stats> st(n);
+              std::vector<std::int64_t*> pk;
+              std::vector<std::uint32_t*> pf;
+              for (auto v : peer_keys) pk.push_back(reinterpret_cast<std::int64_t*>(v));
+              for (auto v : peer_flags) pf.push_back(reinterpret_cast<std::uint32_t*>(v));
+              fnl_shard_spec spec{};
+              spec.rank = rank;
+              spec.count = std::uint32_t(pk.size());
+              spec.d_keys = pk[rank];
+              spec.keys_capacity = keys_capacity;
+              spec.peer_keys = pk.data();
+              spec.peer_flags = pf.data();
+              spec.barrier_seq = &barrier_seq;
+              int rc;
+              {
+                  py::gil_scoped_release nogil;
+                  fnl_context* ctx = fastnn::b200::context();
+                  fastnn::b200::check(fnl_context_set_stream(ctx, sh));
+                  rc = fnl_reciprocal_match_sharded_device(
+                      ctx, n, reinterpret_cast<const float*>(d1), reinterpret_cast<const float*>(d2), h, w, d,
+                      &cc, be, &spec, reinterpret_cast<std::uint32_t*>(out_pairs),
+                      reinterpret_cast<std::uint32_t*>(out_counts), st.data());
+                  fnl_context_set_stream(ctx, nullptr);
+              }
+              fastnn::b200::check(rc);
+              py::list stats;
+              for (const auto& s : st) stats.append(stats_dict(s));
+              return py::make_tuple(stats, barrier_seq);
+          },
+          py::arg("d1"), py::arg("d2"), py::arg("npairs"), py::arg("height"), py::arg("width"),
+          py::arg("dim"), py::arg("out_pairs"), py::arg("out_counts"), py::arg("keys_capacity"),
+          py::arg("shard_rank"), py::arg("peer_keys"), py::arg("peer_flags"), py::arg("barrier_seq"),
+          py::arg("backend") = "tensor", py::arg("k") = 0, py::arg("stride") = 8, py::arg("max_iters") = 10,
+          py::arg("convergence") = 0.99, py::arg("metric") = "dot", py::arg("block_size") = 4096,
+          py::arg("stream") = py::none());
+    m.def("p2p_alloc",
+          [](std::uint64_t bytes, bool fill_key_none) {
+              void* p = nullptr;
+              fastnn::b200::check(fnl_p2p_alloc(fastnn::b200::context(), bytes, fill_key_none ? 1 : 0, &p));
+              return reinterpret_cast<std::uintptr_t>(p);
+          },
+          py::arg("bytes"), py::arg("fill_key_none") = false);
+    m.def("p2p_free", [](std::uintptr_t p) { fastnn::b200::check(fnl_p2p_free(reinterpret_cast<void*>(p))); });
+    m.def("ipc_handle", [](std::uintptr_t p) {
+        unsigned char h[64];
+        fastnn::b200::check(fnl_ipc_handle(reinterpret_cast<const void*>(p), h));
+        return py::bytes(reinterpret_cast<const char*>(h), 64);
+    });
+    m.def("ipc_open", [](py::bytes handle) {
+        const std::string s = handle;
+        if (s.size() != 64) throw std::invalid_argument("ipc_open: handles are 64 bytes");
+        void* p = nullptr;
+        fastnn::b200::check(fnl_ipc_open(fastnn::b200::context(),
+                                         reinterpret_cast<const unsigned char*>(s.data()), &p));
+        return reinterpret_cast<std::uintptr_t>(p);
+    });
+    m.def("ipc_close", [](std::uintptr_t p) { fastnn::b200::check(fnl_ipc_close(reinterpret_cast<void*>(p))); });
+
     m.def("kernel_timing",
           [](bool reset) {
               double ms = 0;

@@ -665,9 +665,14 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
         if (!tensor) return fail(FNL_EINVAL, "sharded reciprocal_match: tensor backend only");
         if (shard->count == 0 || shard->rank >= shard->count)
             return fail(FNL_EINVAL, "sharded reciprocal_match: rank must be < count");
-        if (sharded && (!shard->d_keys || !shard->reduce || shard->keys_capacity < (uint64_t)npairs * cap))
+        const bool peer = sharded && shard->peer_keys;
+        if (sharded && !peer && (!shard->d_keys || !shard->reduce || shard->keys_capacity < (uint64_t)npairs * cap))
             return fail(FNL_EINVAL, "sharded reciprocal_match: key buffer (npairs * samples) and reduce callback "
                                     "required");
+        if (peer && (shard->count > (uint32_t)fnl::kMaxShardPeers || !shard->peer_flags || !shard->barrier_seq ||
+                     !shard->d_keys || shard->keys_capacity < 2ull * npairs * cap))
+            return fail(FNL_EINVAL, "sharded reciprocal_match (peer memory): at most 8 ranks, key buffers of "
+                                    "2 * npairs * samples, flags and barrier_seq required");
     }
     Prepared P1, P2;
     fnl::PackedMaps T1, T2;
@@ -717,6 +722,13 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
 
     // ---- NN pass helper: queries = rows of qmap at ids, targets = tmap
     uint32_t call = 0;
+    const bool peer = sharded && shard->peer_keys;
+    unsigned int* barrier_err = nullptr;
+    if (peer) {
+        TRY(dev_arr(ctx, "m.p2perr", 1, &barrier_err));
+        FNL_CUDA_TRY(cudaMemsetAsync(barrier_err, 0, 4, s));
+    }
+    uint32_t peer_pass = 0;
     auto nn_pass = [&](const Prepared& Q, uint32_t qrows, const uint32_t* ids, const Prepared& Tm,
                        uint32_t nt, uint32_t* out) -> int {
         if (tensor) {
@@ -731,6 +743,29 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
             const uint32_t tb = (uint32_t)(tiles * shard->rank / shard->count);
             const uint32_t te = (uint32_t)(tiles * (shard->rank + 1) / shard->count);
             const uint64_t nkeys = (uint64_t)npairs * cap;
+            if (peer) {
+                // keys go straight into every rank's buffer (half `par`) from the
+                // merge / rescan epilogues; a peer-memory barrier replaces the
+                // all-reduce; the half is reset after decoding, before this rank
+                // can take part in the next barrier (the earliest a peer pushes
+                // into it again)
+                const uint32_t par = peer_pass++ & 1u;
+                fnl::ShardPeers pp{};
+                pp.n = shard->count;
+                for (uint32_t r = 0; r < shard->count; ++r)
+                    pp.keys[r] = reinterpret_cast<long long*>(shard->peer_keys[r]) + par * nkeys;
+                long long* own = reinterpret_cast<long long*>(shard->d_keys) + par * nkeys;
+                if (te > tb)
+                    TRY(fnl::tensor_nn_pass(ctx, npairs, TQ, ids, cap, m.n_active, m.done, TT, dim, l2, out, cap,
+                                            nullptr, near_ties, tb, te, own, &pp));
+                const uint64_t seq = ++*shard->barrier_seq;
+                TRY(fnl::tensor_shard_barrier(ctx, reinterpret_cast<unsigned int* const*>(shard->peer_flags),
+                                              shard->count,
+                                              reinterpret_cast<unsigned int*>(shard->peer_flags[shard->rank]),
+                                              (unsigned int)(seq * shard->count), barrier_err));
+                TRY(fnl::tensor_shard_finalize(ctx, npairs, own, cap, m.n_active, m.done, out));
+                return fnl::tensor_shard_reset(ctx, own, nkeys);
+            }
             TRY(fnl::tensor_shard_reset(ctx, reinterpret_cast<long long*>(shard->d_keys), nkeys));
             if (te > tb)
                 TRY(fnl::tensor_nn_pass(ctx, npairs, TQ, ids, cap, m.n_active, m.done, TT, dim, l2, out, cap,
@@ -813,6 +848,13 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
         timer.begin(kPhaseForward);
         TRY(nn_pass(P1, p1, m.active_u, P2, p2, m.active_v));
         timer.end();
+    }
+
+    if (peer) {
+        unsigned int err = 0;
+        FNL_CUDA_TRY(cudaMemcpyAsync(&err, barrier_err, 4, cudaMemcpyDeviceToHost, s));
+        FNL_CUDA_TRY(cudaStreamSynchronize(s));
+        if (err) return fail(FNL_ERUNTIME, "sharded reciprocal_match: peer-memory barrier timed out (a rank stopped)");
     }
 
     // ---- stats back to host and the reference's accounting
@@ -1216,5 +1258,60 @@ extern "C" int fnl_mutual_nn(fnl_context* ctx, const float* h_d1, uint32_t h1, u
     FNL_CUDA_TRY(cudaStreamSynchronize(s));
     timing_harvest(ctx);
     if (n_pairs) *n_pairs = n;
+    return FNL_OK;
+}
+
+// ---------------------------------------------------------------- peer memory
+namespace {
+__global__ void fill_i64_kernel(long long* p, uint64_t n, long long v) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+}  // namespace
+
+extern "C" int fnl_p2p_alloc(fnl_context* ctx, uint64_t bytes, int fill_key_none, void** d_ptr) {
+    TRY(check_device(ctx));
+    if (!d_ptr || bytes == 0) return fail(FNL_EINVAL, "fnl_p2p_alloc: null output or zero size");
+    if (fill_key_none && bytes % 8) return fail(FNL_EINVAL, "fnl_p2p_alloc: key buffers are int64");
+    void* p = nullptr;
+    FNL_CUDA_TRY(cudaMalloc(&p, bytes));
+    if (fill_key_none) {
+        const uint64_t n = bytes / 8;
+        fill_i64_kernel<<<(unsigned)std::min<uint64_t>(1024, (n + 255) / 256), 256>>>(
+            static_cast<long long*>(p), n, 0x7FFFFFFFFFFFFFFFll);
+        FNL_CUDA_TRY(cudaGetLastError());
+    } else {
+        FNL_CUDA_TRY(cudaMemset(p, 0, bytes));
+    }
+    FNL_CUDA_TRY(cudaDeviceSynchronize());
+    *d_ptr = p;
+    return FNL_OK;
+}
+
+extern "C" int fnl_p2p_free(void* d_ptr) {
+    if (d_ptr) FNL_CUDA_TRY(cudaFree(d_ptr));
+    return FNL_OK;
+}
+
+extern "C" int fnl_ipc_handle(const void* d_ptr, unsigned char handle[64]) {
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "CUDA IPC handles are 64 bytes");
+    if (!d_ptr || !handle) return fail(FNL_EINVAL, "fnl_ipc_handle: null pointer");
+    cudaIpcMemHandle_t h;
+    FNL_CUDA_TRY(cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)));
+    memcpy(handle, &h, 64);
+    return FNL_OK;
+}
+
+extern "C" int fnl_ipc_open(fnl_context* ctx, const unsigned char handle[64], void** d_ptr) {
+    TRY(check_device(ctx));
+    if (!handle || !d_ptr) return fail(FNL_EINVAL, "fnl_ipc_open: null pointer");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, 64);
+    FNL_CUDA_TRY(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return FNL_OK;
+}
+
+extern "C" int fnl_ipc_close(void* d_ptr) {
+    if (d_ptr) FNL_CUDA_TRY(cudaIpcCloseMemHandle(d_ptr));
     return FNL_OK;
 }

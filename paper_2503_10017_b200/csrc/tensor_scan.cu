@@ -589,7 +589,18 @@ struct MergeArgs {
     unsigned int* rescan_count;
     unsigned long long* near_ties;  // per pair
     long long* shard_keys;      // sharded mode: signed winner keys instead of out/min_dist
+    ShardPeers peers;           // sharded mode over peer memory (peers.n > 0)
 };
+
+// sharded mode: this rank's winner key of output slot o -- a local store, or
+// a system-scope atomicMin into every rank's key buffer (peer memory)
+__device__ __forceinline__ void shard_emit(long long* local, const ShardPeers& p, uint64_t o, long long key) {
+    if (p.n == 0) {
+        local[o] = key;
+        return;
+    }
+    for (uint32_t r = 0; r < p.n; ++r) atomicMin_system(p.keys[r] + o, key);
+}
 
 template <bool kL2, int DIM>
 __device__ __forceinline__ float packed_chain(const float (&q)[kPackK], const uint8_t* map, uint32_t row,
@@ -682,7 +693,7 @@ __global__ void __launch_bounds__(kQueryTilePair) merge_kernel(MergeArgs a) {
         if (lane == 0) {
             const uint64_t o = (uint64_t)pair * a.out_stride + a.tp_qi0[tp] + row;
             if (a.shard_keys) {
-                a.shard_keys[o] = (long long)(key ^ 0x8000000000000000ull);
+                shard_emit(a.shard_keys, a.peers, o, (long long)(key ^ 0x8000000000000000ull));
                 continue;
             }
             a.out[o] = (uint32_t)(key & 0xFFFFFFFFull);
@@ -785,13 +796,13 @@ __global__ void __launch_bounds__(kRescanThreads) rescan_kernel(RescanArgs a) {
 
 __global__ void rescan_finish_kernel(const uint32_t* rescan, const unsigned int* count,
                                      unsigned long long* keys, uint32_t* out, float* min_dist,
-                                     uint32_t out_stride, bool dot, long long* shard_keys) {
+                                     uint32_t out_stride, bool dot, long long* shard_keys, ShardPeers peers) {
     const uint32_t n = *count;
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
         const uint64_t o = (uint64_t)rescan[3 * k + 1] * out_stride + rescan[3 * k + 2];
         const unsigned long long key = keys[k];
         if (shard_keys) {
-            shard_keys[o] = (long long)(key ^ 0x8000000000000000ull);
+            shard_emit(shard_keys, peers, o, (long long)(key ^ 0x8000000000000000ull));
             keys[k] = ~0ull;
             continue;
         }
@@ -814,6 +825,30 @@ __global__ void shard_finalize_kernel(const long long* keys, uint32_t stride, co
         const uint64_t o = (uint64_t)p * stride + i;
         out[o] = (uint32_t)(((unsigned long long)keys[o] ^ 0x8000000000000000ull) & 0xFFFFFFFFull);
     }
+}
+
+struct PeerFlags {
+    unsigned int* flags[kMaxShardPeers];
+    uint32_t n;
+};
+
+__global__ void shard_barrier_kernel(PeerFlags f, unsigned int* own, unsigned int target, unsigned int* err) {
+    __threadfence_system();  // this rank's key pushes (earlier kernels) before the arrivals
+    for (uint32_t r = 0; r < f.n; ++r) atomicAdd_system(f.flags[r], 1u);
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+        unsigned int v;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(own) : "memory");
+        if ((int)(v - target) >= 0) break;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 20000000000ull) {  // a peer never arrived: report instead of hanging the GPU
+            atomicExch(err, 1u);
+            break;
+        }
+        __nanosleep(256);
+    }
+    __threadfence_system();
 }
 
 __global__ void shard_reset_kernel(long long* keys, uint64_t n) {
@@ -1067,7 +1102,9 @@ int tensor_pack(fnl_context* ctx, const char* tag, const float* d_src, uint32_t 
 int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const uint32_t* ids, uint32_t cap,
                    const uint32_t* d_active, const uint8_t* d_done, const PackedMaps& T, uint32_t dim, bool l2,
                    uint32_t* out, uint32_t out_stride, float* min_dist, unsigned long long* d_near_ties,
-                   uint32_t tile_begin, uint32_t tile_end, long long* shard_keys) {
+                   uint32_t tile_begin, uint32_t tile_end, long long* shard_keys, const ShardPeers* peers) {
+    const ShardPeers no_peers{};
+    const ShardPeers& pp = peers ? *peers : no_peers;
     TRY(ensure_attrs());
     cudaStream_t s = ctx_stream(ctx);
     const uint32_t nt = T.rows;
@@ -1149,7 +1186,7 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     // ---- K3b merge + certification
     {
         MergeArgs m{partial, d_tp_pair, d_tp_row0, d_tp_qi0, d_hdr, d_active, margin, qbuf, T.data,
-                    T.pair_bytes, nt, dim, out, min_dist, out_stride, rescan, rcount, d_near_ties, shard_keys};
+                    T.pair_bytes, nt, dim, out, min_dist, out_stride, rescan, rcount, d_near_ties, shard_keys, pp};
         ProfScope prof(ctx, FNL_KCLASS_MERGE);
         if (dim == 24) {
             if (l2) merge_kernel<true, 24><<<tp_max, kQueryTilePair, 0, s>>>(m);
@@ -1174,7 +1211,7 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
             else rescan_kernel<false, 0><<<grid, kRescanThreads, 0, s>>>(r);
         }
         FNL_CUDA_TRY(cudaGetLastError());
-        rescan_finish_kernel<<<4, 256, 0, s>>>(rescan, rcount, keys, out, min_dist, out_stride, !l2, shard_keys);
+        rescan_finish_kernel<<<4, 256, 0, s>>>(rescan, rcount, keys, out, min_dist, out_stride, !l2, shard_keys, pp);
         FNL_CUDA_TRY(cudaGetLastError());
     }
     if (debug_mode_trace_dump(ctx, s)) {}
@@ -1187,6 +1224,18 @@ int tensor_shard_finalize(fnl_context* ctx, uint32_t npairs, const long long* ke
     cudaStream_t s = ctx_stream(ctx);
     ProfScope prof(ctx, FNL_KCLASS_OTHER);
     shard_finalize_kernel<<<dim3(ceil_div_u(stride, 256), npairs), 256, 0, s>>>(keys, stride, d_n_active, d_done, out);
+    FNL_CUDA_TRY(cudaGetLastError());
+    ctx_count_launches(ctx, 1);
+    return FNL_OK;
+}
+
+int tensor_shard_barrier(fnl_context* ctx, unsigned int* const* flags, uint32_t n, unsigned int* own,
+                         unsigned int target, unsigned int* d_err) {
+    if (n > (uint32_t)kMaxShardPeers) return fail(FNL_EINVAL, "shard barrier: at most 8 ranks");
+    PeerFlags f{};
+    for (uint32_t r = 0; r < n; ++r) f.flags[r] = flags[r];
+    f.n = n;
+    shard_barrier_kernel<<<1, 1, 0, ctx_stream(ctx)>>>(f, own, target, d_err);
     FNL_CUDA_TRY(cudaGetLastError());
     ctx_count_launches(ctx, 1);
     return FNL_OK;

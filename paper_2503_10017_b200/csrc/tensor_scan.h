@@ -58,16 +58,33 @@ int tensor_pack(fnl_context* ctx, const char* tag, const float* d_src, uint32_t 
 // shard_keys[p*out_stride + i] instead of out/min_dist, so a MIN all-reduce of
 // the keys over the shards (NCCL / gloo int64 MIN) yields the global winner
 // with the reference's lowest-index tie rule; tensor_shard_finalize decodes.
+// Peer-memory key exchange (config C5 without NCCL): with n > 0 the pass
+// pushes every winner key into all n ranks' key buffers (keys[r], mapped into
+// this process by CUDA IPC / NVLink peer access) with a system-scope
+// atomicMin from the merge / rescan epilogues themselves, so the "all-reduce"
+// is fused into the kernels that produce the keys.
+constexpr int kMaxShardPeers = 8;
+struct ShardPeers {
+    long long* keys[kMaxShardPeers];
+    uint32_t n;
+};
+
 int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const uint32_t* ids,
                    uint32_t cap, const uint32_t* d_active, const uint8_t* d_done,
                    const PackedMaps& T, uint32_t dim, bool l2, uint32_t* out, uint32_t out_stride,
                    float* min_dist, unsigned long long* d_near_ties, uint32_t tile_begin = 0,
-                   uint32_t tile_end = 0, long long* shard_keys = nullptr);
+                   uint32_t tile_end = 0, long long* shard_keys = nullptr, const ShardPeers* peers = nullptr);
 
 // shard keys -> nearest indices for the active queries of every pair
 int tensor_shard_finalize(fnl_context* ctx, uint32_t npairs, const long long* keys, uint32_t stride,
                           const uint32_t* d_n_active, const uint8_t* d_done, uint32_t* out);
 int tensor_shard_reset(fnl_context* ctx, long long* keys, uint64_t n);
+// Cross-GPU barrier over peer memory: increments every rank's counter
+// (flags[r], system scope, after a system fence that publishes this rank's
+// key pushes), then waits until its own counter reaches `target` (wrapping
+// compare).  Gives up after ~20 s and raises *d_err instead of hanging.
+int tensor_shard_barrier(fnl_context* ctx, unsigned int* const* flags, uint32_t n, unsigned int* own,
+                         unsigned int target, unsigned int* d_err);
 // value every shard key starts from (no candidate in this shard)
 constexpr long long kShardKeyNone = 0x7FFFFFFFFFFFFFFFll;
 constexpr uint32_t kTargetTileRows = 256;  // targets per K3 B tile (shard granularity)

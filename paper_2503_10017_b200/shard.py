@@ -16,6 +16,13 @@ run.  This is the only collective on the path: 8 B per active query per pass
 
 The device work is in libfastnn_b200.so (fnl_reciprocal_match_sharded_device);
 this module only supplies the key buffer and the all-reduce callback.
+
+``transport="p2p"`` replaces the NCCL all-reduce with peer memory: every
+rank's key buffers and barrier counter are CUDA-IPC-mapped into every other
+rank (NVLink / NVSwitch peer access), the merge and near-tie epilogues push
+each winner key straight into all ranks' buffers with a system-scope
+atomicMin, and a one-thread peer-memory barrier kernel closes the pass -- the
+collective is fused into the kernels that produce the keys.
 """
 import numpy as np
 
@@ -46,7 +53,66 @@ def decode_index(keys):
     return (np.asarray(keys, dtype=np.int64).view(np.uint64) & np.uint64(0xFFFFFFFF)).astype(np.uint32)
 
 
-def match_sharded(d1, d2, stride=8, metric="dot", group=None, backend="tensor", **kw):
+class PeerTransport:
+    """Key buffers (two NN-pass parities) and a barrier counter per rank,
+    mapped into every rank of `group` with CUDA IPC.  Reusable across calls
+    with at most `nkeys` keys per pass; close() unmaps and frees."""
+
+    def __init__(self, nkeys, group=None):
+        import torch.distributed as dist
+
+        from . import _fastnn
+        self._fnl = _fastnn
+        self.nkeys = nkeys
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.keys = _fastnn.p2p_alloc(2 * nkeys * 8, True)
+        self.flag = _fastnn.p2p_alloc(4, False)
+        mine = (_fastnn.ipc_handle(self.keys), _fastnn.ipc_handle(self.flag))
+        handles = [None] * world
+        if world > 1:
+            dist.all_gather_object(handles, mine, group=group)
+        else:
+            handles = [mine]
+        self.opened = []
+        self.peer_keys, self.peer_flags = [], []
+        ok, err = True, ""
+        try:
+            for r, (hk, hf) in enumerate(handles):
+                if r == self.rank:
+                    self.peer_keys.append(self.keys)
+                    self.peer_flags.append(self.flag)
+                    continue
+                k = _fastnn.ipc_open(hk)
+                self.opened.append(k)
+                f = _fastnn.ipc_open(hf)
+                self.opened.append(f)
+                self.peer_keys.append(k)
+                self.peer_flags.append(f)
+        except Exception as e:  # e.g. no peer access between these GPUs
+            ok, err = False, str(e)
+        # every rank learns whether every rank mapped every buffer (and no rank
+        # pushes before all have): all succeed or all raise, nobody hangs
+        verdicts = [(ok, err)]
+        if world > 1:
+            verdicts = [None] * world
+            dist.all_gather_object(verdicts, (ok, err), group=group)
+        bad = [e for good, e in verdicts if not good]
+        if bad:
+            self.close()
+            raise RuntimeError("peer-memory transport unavailable: " + bad[0])
+        self.seq = 0
+
+    def close(self):
+        for p in self.opened:
+            self._fnl.ipc_close(p)
+        self.opened = []
+        self._fnl.p2p_free(self.keys)
+        self._fnl.p2p_free(self.flag)
+
+
+def match_sharded(d1, d2, stride=8, metric="dot", group=None, backend="tensor", transport="nccl",
+                  peers=None, **kw):
     """Reciprocal matching of one pair (or a stack) with the target columns
     sharded over the ranks of `group` (torch.distributed; NCCL on GPUs).
 
@@ -66,14 +132,30 @@ def match_sharded(d1, d2, stride=8, metric="dot", group=None, backend="tensor", 
     samples = ((H + stride - 1) // stride) * ((W + stride - 1) // stride)
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     world = dist.get_world_size(group) if dist.is_initialized() else 1
-    keys = torch.empty((P * samples,), dtype=torch.int64, device=d1.device)
     pairs = torch.empty((P, samples, 3), dtype=torch.int32, device=d1.device)
     counts = torch.empty((P,), dtype=torch.int32, device=d1.device)
+    stream = torch.cuda.current_stream(d1.device).cuda_stream
+    if transport == "p2p":
+        own = peers is None
+        if own:
+            peers = PeerTransport(P * samples, group)
+        try:
+            stats, peers.seq = _fastnn.reciprocal_match_p2p_device(
+                d1.data_ptr(), d2.data_ptr(), P, H, W, D, pairs.data_ptr(), counts.data_ptr(),
+                2 * peers.nkeys, rank, peers.peer_keys, peers.peer_flags, peers.seq, backend=backend,
+                stride=stride, metric=metric, stream=stream, **kw)
+        finally:
+            if own:
+                torch.cuda.synchronize(d1.device)
+                if world > 1:
+                    dist.barrier(group=group)  # nobody unmaps while a peer may still push
+                peers.close()
+        return pairs, counts, stats
+    keys = torch.empty((P * samples,), dtype=torch.int64, device=d1.device)
 
     def reduce(count):
         dist.all_reduce(keys[:count], op=dist.ReduceOp.MIN, group=group)
 
-    stream = torch.cuda.current_stream(d1.device).cuda_stream
     stats = _fastnn.reciprocal_match_sharded_device(
         d1.data_ptr(), d2.data_ptr(), P, H, W, D, pairs.data_ptr(), counts.data_ptr(), keys.data_ptr(),
         keys.numel(), rank, world, reduce, backend=backend, stride=stride, metric=metric, stream=stream, **kw)

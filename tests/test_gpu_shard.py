@@ -19,7 +19,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, D1, D2, metric, out):
+def _worker(rank, world, port, D1, D2, metric, out, transport="nccl", calls=1):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -29,7 +29,18 @@ def _worker(rank, world, port, D1, D2, metric, out):
     from paper_2503_10017_b200.shard import match_sharded
     d1 = torch.from_numpy(D1).cuda()
     d2 = torch.from_numpy(D2).cuda()
-    pairs, counts, stats = match_sharded(d1, d2, metric=metric)
+    if transport == "p2p":
+        # one transport reused over several calls (barrier counters carry over)
+        from paper_2503_10017_b200.shard import PeerTransport
+        samples = ((D1.shape[0] + 7) // 8) * ((D1.shape[1] + 7) // 8)
+        peers = PeerTransport(samples, None)
+        for _ in range(calls):
+            pairs, counts, stats = match_sharded(d1, d2, metric=metric, transport="p2p", peers=peers)
+        torch.cuda.synchronize()
+        dist.barrier()
+        peers.close()
+    else:
+        pairs, counts, stats = match_sharded(d1, d2, metric=metric)
     torch.cuda.synchronize()
     n = int(counts[0].item())
     out[rank] = (pairs[0, :n].cpu().numpy().copy(), stats[0]["iterations"])
@@ -45,6 +56,23 @@ def test_sharded_equals_unsharded(fnl, H, W, world, metric):
     mgr = mp.Manager()
     out = mgr.dict()
     mp.spawn(_worker, args=(world, _free_port(), D1, D2, metric, out), nprocs=world, join=True)
+    for r in range(world):
+        got, _ = out[r]
+        assert np.array_equal(got.astype(np.uint32), want), f"rank {r}"
+
+
+@pytest.mark.parametrize("H,W,world,metric,calls", [(128, 96, 2, "dot", 3), (128, 96, 3, "l2", 1)])
+def test_sharded_peer_memory_equals_unsharded(fnl, H, W, world, metric, calls):
+    """The peer-memory transport (CUDA IPC mapped key buffers, system-scope
+    atomicMin pushes from the merge epilogues, peer-memory barrier) -- here
+    between processes sharing the one GPU -- gives the same MatchSet."""
+    import torch.multiprocessing as mp
+    D1 = fnl.gen_random(H, W, 24, 606)
+    D2 = fnl.gen_random(H, W, 24, 607)
+    want, _ = fnl.reciprocal_match(D1, D2, backend="tensor", metric=metric)
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), D1, D2, metric, out, "p2p", calls), nprocs=world, join=True)
     for r in range(world):
         got, _ = out[r]
         assert np.array_equal(got.astype(np.uint32), want), f"rank {r}"
