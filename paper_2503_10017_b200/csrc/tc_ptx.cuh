@@ -120,6 +120,18 @@ __device__ __forceinline__ void frag_ld(uint32_t taddr, Frag& f) {
         : "r"(taddr));
 }
 
+__device__ __forceinline__ void frag_wait1(Frag& f) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(f.r[0]), "+r"(f.r[1]), "+r"(f.r[2]), "+r"(f.r[3]), "+r"(f.r[4]), "+r"(f.r[5]),
+                   "+r"(f.r[6]), "+r"(f.r[7]), "+r"(f.r[8]), "+r"(f.r[9]), "+r"(f.r[10]), "+r"(f.r[11]),
+                   "+r"(f.r[12]), "+r"(f.r[13]), "+r"(f.r[14]), "+r"(f.r[15]), "+r"(f.r[16]), "+r"(f.r[17]),
+                   "+r"(f.r[18]), "+r"(f.r[19]), "+r"(f.r[20]), "+r"(f.r[21]), "+r"(f.r[22]), "+r"(f.r[23]),
+                   "+r"(f.r[24]), "+r"(f.r[25]), "+r"(f.r[26]), "+r"(f.r[27]), "+r"(f.r[28]), "+r"(f.r[29]),
+                   "+r"(f.r[30]), "+r"(f.r[31])
+                 :
+                 : "memory");
+}
+
 // one tcgen05.ld of 64 consecutive columns (32x32b.x64) into two fragments
 __device__ __forceinline__ void frag_ld64(uint32_t taddr, Frag& f, Frag& g) {
     asm volatile(
