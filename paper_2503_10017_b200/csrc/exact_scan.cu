@@ -83,31 +83,42 @@ __device__ __forceinline__ float reg_chain(const QueryRegs<DMAX>& q, const float
 
 // DMAX > 0: queries in registers (dim <= DMAX; kExactDim when dim == DMAX).
 // DMAX == 0: generic dim, query re-read from global memory (L1 resident).
-// Each thread scores kQB queries (q, q + kScanThreads, ...) against every
+// Each thread scores QB queries (q, q + kScanThreads, ...) against every
 // staged target, so one broadcast shared-memory read of a target channel feeds
-// kQB independent FMA chains (the scan is otherwise bound by LDS issue).
+// QB independent FMA chains (the scan is otherwise bound by LDS issue).
+// Queries per thread: 4, or 2 when a query row of up to 64 channels lives in
+// registers (4 x 64 would spill).  dim 33..64 are the DMAX = 64 kernels.
 constexpr int kQB = 4;
+// (1 for the hybrid kernels of dim 33..63, whose predicated channel loop
+// would otherwise spill inside the scan loop).
+__host__ __device__ constexpr int qb_for(int dmax, bool hyb, bool exact_dim) {
+    return dmax > 32 ? (hyb && !exact_dim ? 1 : 2) : kQB;
+}
+__host__ __device__ constexpr int qb_for_dim(uint32_t dim, bool hyb) {
+    return dim > 32 && dim <= 64 ? (hyb && dim != 64 ? 1 : 2) : kQB;
+}
 
 template <bool kL2, bool kHyb, int DMAX, bool kExactDim>
 __global__ void __launch_bounds__(kScanThreads) exact_scan_kernel(ScanArgs a, uint32_t chunk) {
+    constexpr int QB = qb_for(DMAX, kHyb, kExactDim);
     extern __shared__ float4 smem4[];
     float* tile = reinterpret_cast<float*>(smem4);
     const uint32_t pair = blockIdx.z;
     if (a.pair_done && a.pair_done[pair]) return;
     const uint32_t nq = a.qcount ? a.qcount[pair] : a.qcount_const;
-    if (blockIdx.x * kScanThreads * kQB >= nq) return;
+    if (blockIdx.x * kScanThreads * QB >= nq) return;
     const uint32_t t0 = blockIdx.y * a.split_len;
     if (t0 >= a.nt) return;
     const uint32_t t1 = min(a.nt, t0 + a.split_len);
     const uint32_t dim = a.dim;
 
-    uint32_t qi[kQB], row[kQB];
-    bool active[kQB];
-    const float* qsrc[kQB];
-    QueryRegs<(DMAX > 0 ? DMAX : 1)> qr[kQB];
+    uint32_t qi[QB], row[QB];
+    bool active[QB];
+    const float* qsrc[QB];
+    QueryRegs<(DMAX > 0 ? DMAX : 1)> qr[QB];
 #pragma unroll
-    for (int b = 0; b < kQB; ++b) {
-        qi[b] = blockIdx.x * kScanThreads * kQB + b * kScanThreads + threadIdx.x;
+    for (int b = 0; b < QB; ++b) {
+        qi[b] = blockIdx.x * kScanThreads * QB + b * kScanThreads + threadIdx.x;
         active[b] = qi[b] < nq;
         row[b] = 0;
         if (active[b]) row[b] = a.qids ? a.qids[(size_t)pair * a.qids_pair_stride + qi[b]] : qi[b];
@@ -121,10 +132,10 @@ __global__ void __launch_bounds__(kScanThreads) exact_scan_kernel(ScanArgs a, ui
     const bool any_active = active[0];
 
     const float* T = a.tmap + pair * a.tmap_pair_stride;
-    float best[kQB];
-    uint32_t bidx[kQB];
+    float best[QB];
+    uint32_t bidx[QB];
 #pragma unroll
-    for (int b = 0; b < kQB; ++b) {
+    for (int b = 0; b < QB; ++b) {
         best[b] = INFINITY;
         bidx[b] = t0;
     }
@@ -149,7 +160,7 @@ __global__ void __launch_bounds__(kScanThreads) exact_scan_kernel(ScanArgs a, ui
             for (uint32_t j = 0; j < n; ++j) {
                 const float* t = tile + (size_t)j * dim;
 #pragma unroll
-                for (int b = 0; b < kQB; ++b) {
+                for (int b = 0; b < QB; ++b) {
                     float d;
                     if constexpr (DMAX > 0) {
                         d = reg_chain<kL2, DMAX, kExactDim>(qr[b], t, dim);
@@ -170,14 +181,14 @@ __global__ void __launch_bounds__(kScanThreads) exact_scan_kernel(ScanArgs a, ui
         }
     }
 #pragma unroll
-    for (int b = 0; b < kQB; ++b)
+    for (int b = 0; b < QB; ++b)
         if (active[b]) atomicMin(a.keys + (size_t)pair * a.keys_pair_stride + qi[b], pack_key(best[b], bidx[b]));
 
     if constexpr (kHyb) {
         uint32_t qsat = 0;
         if (blockIdx.y == 0 && a.q_row_sat) {
 #pragma unroll
-            for (int b = 0; b < kQB; ++b)
+            for (int b = 0; b < QB; ++b)
                 if (active[b]) qsat += a.q_row_sat[pair * a.q_row_sat_pair_stride + row[b]];
         }
         const uint32_t ws = warp_sum(dsat), wq = warp_sum(qsat);
@@ -216,7 +227,8 @@ cudaError_t launch_exact_scan(const ScanArgs& a, uint32_t max_q, uint32_t npairs
     uint32_t chunk = 8192u / a.dim;
     chunk = chunk < 1 ? 1 : (chunk > 256 ? 256 : chunk);
     const size_t smem = (size_t)chunk * a.dim * sizeof(float);
-    const uint32_t gx = (max_q + kScanThreads * kQB - 1) / (kScanThreads * kQB);
+    const uint32_t qb = (uint32_t)qb_for_dim(a.dim, hybrid);
+    const uint32_t gx = (max_q + kScanThreads * qb - 1) / (kScanThreads * qb);
     // Split targets so that the grid covers the machine several times over.
     const uint32_t want_ctas = 148u * 8u;
     uint32_t splits = (want_ctas + gx * npairs - 1) / (gx * npairs);

@@ -23,11 +23,11 @@ constexpr float kHalfOverflow = 65520.0f;
 
 // binary16 round trip with the reference's saturation rule.
 __device__ __forceinline__ float half_round_sat(float x, uint32_t& sat) {
-    if (fabsf(x) >= kHalfOverflow) {  // false for NaN
-        ++sat;
-        return copysignf(kHalfMax, x);
-    }
-    return __half2float(__float2half_rn(x));
+    // branch-free (selects), so it stays if-converted inside unrolled scans
+    const bool over = fabsf(x) >= kHalfOverflow;  // false for NaN
+    sat += over ? 1u : 0u;
+    const float r = __half2float(__float2half_rn(x));
+    return over ? copysignf(kHalfMax, x) : r;
 }
 __device__ __forceinline__ float half_round_nosat(float x) {
     return __half2float(__float2half_rn(x));
