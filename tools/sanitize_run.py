@@ -13,6 +13,15 @@ for be in ("tensor", "single", "hybrid", "double"):
     m, _ = fnl.reciprocal_match(D1, D2, backend=be, metric="dot")
     print(be, m.shape[0])
 print("l2", fnl.reciprocal_match(D1, D2, backend="tensor", metric="l2")[0].shape[0])
+# several 256-row tile pairs (merge slices 0..3, ragged last slice) and the
+# dim-dependent exact kernels (33..64 channels: 2 / 1 queries per thread)
+E1 = fnl.gen_random(128, 96, 24, 31)
+E2 = fnl.gen_random(128, 96, 24, 131)
+print("tensor 700q", fnl.reciprocal_match(E1, E2, backend="tensor", metric="dot", stride=4)[0].shape[0])
+F1 = fnl.gen_random(32, 24, 48, 41)
+F2 = fnl.gen_random(32, 24, 48, 141)
+for be in ("single", "hybrid"):
+    print(be, "d48", fnl.reciprocal_match(F1, F2, backend=be, metric="dot", stride=4)[0].shape[0])
 r = fnl.nn_tensor(D1, D2, metric="dot")
 print("dense", len(r["nearest"]))
 print("mutual", fnl.mutual_nn_exact(D1, D2, metric="dot").shape[0])
