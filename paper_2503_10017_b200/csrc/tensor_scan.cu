@@ -680,30 +680,35 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs a) {
     __syncthreads();
     const uint32_t warp = r >> 5, lane = r & 31;
     const uint8_t* tm = a.tmap + pair * a.t_pair_bytes;
-    for (uint32_t row = warp; row < nrows; row += kMergeThreads / 32) {
-        if (!s_go[row]) continue;
-        float q[kPackK];
-        load_query(a.qbuf, row0 + row, q);
+    // two rows per warp at a time, one per 16-lane half, four targets per lane
+    const uint32_t half = lane >> 4, hl = lane & 15u;
+    for (uint32_t rb = warp; rb < nrows; rb += 2 * (kMergeThreads / 32)) {
+        const uint32_t row = rb + half * (kMergeThreads / 32);
+        const bool go = row < nrows && s_go[row];
         unsigned long long key = ~0ull;
+        if (go) {
+            float q[kPackK];
+            load_query(a.qbuf, row0 + row, q);
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            const uint32_t st = s_t[row][c];
-            if (st == 0xFFFFFFFFu) continue;
+            for (int c = 0; c < 2; ++c) {
+                const uint32_t st = s_t[row][c];
+                if (st == 0xFFFFFFFFu) continue;
 #pragma unroll
-            for (uint32_t h = 0; h < kSubTile; h += 32) {
-                const uint32_t t = st * kSubTile + h + lane;
-                if (t < a.nt) {
-                    const unsigned long long k = pack_key(packed_chain<kL2, DIM>(q, tm, t, a.dim), t);
-                    key = k < key ? k : key;
+                for (uint32_t h = 0; h < kSubTile; h += 16) {
+                    const uint32_t t = st * kSubTile + h + hl;
+                    if (t < a.nt) {
+                        const unsigned long long k = pack_key(packed_chain<kL2, DIM>(q, tm, t, a.dim), t);
+                        key = k < key ? k : key;
+                    }
                 }
             }
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
+        for (int o = 8; o > 0; o >>= 1) {  // within each 16-lane half
             const unsigned long long other = __shfl_xor_sync(0xFFFFFFFFu, key, o);
             key = other < key ? other : key;
         }
-        if (lane == 0) {
+        if (go && hl == 0) {
             const uint64_t o = (uint64_t)pair * a.out_stride + qi0 + row;
             if (a.shard_keys) {
                 shard_emit(a.shard_keys, a.peers, o, (long long)(key ^ 0x8000000000000000ull));
