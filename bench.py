@@ -356,6 +356,7 @@ def main_b200(args):
 
     # ---- CPU baseline (rank 0, N=1 only): the reference on a bounded sample
     cpu = None
+    parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import oracle
         ref = oracle.reference()
@@ -367,6 +368,22 @@ def main_b200(args):
         cpu = {"value": done / spent, "unit": "pairs/s", "cores": threads, "kind": "reference",
                "sample": f"{done} C2 pairs (512x384 d=24 stride 8, dot), reference reciprocal_match "
                          f"backend=single, {threads} threads, {spent:.1f} s; host CPU {cpu_model()}"}
+        # the same reference as the checker (untimed): the tensor backend must
+        # equal reference backend=single on binary16-rounded maps, bit for bit,
+        # for the first pairs of the last timed step's batch
+        got_pairs = out_pairs[:args.parity_pairs].cpu().numpy()
+        got_counts = out_counts[:args.parity_pairs].cpu().numpy()
+        same = 0
+        for i in range(min(args.parity_pairs, B)):
+            a, b = pair_maps(i)
+            want, _ = ref.reciprocal_match(oracle.half_round_array(pool[a]), oracle.half_round_array(pool[b]),
+                                           backend="single", metric=METRIC, stride=STRIDE,
+                                           block_size=math.ceil(samples / threads), threads=threads)
+            n = int(got_counts[i])
+            same += int(n == len(want) and np.array_equal(got_pairs[i, :n].astype(np.uint32), want))
+        parity = {"pairs_checked": min(args.parity_pairs, B), "identical": same,
+                  "checker": "oracle/_ref reciprocal_match backend=single on binary16-rounded maps "
+                             "(the tensor backend's contract), (i, j, iter) triples of the last timed step"}
 
     if rank != 0:
         return
@@ -415,6 +432,7 @@ def main_b200(args):
                      "kernel_share_of_step": (tot_score_ms / world) / max_ms / 1.0,
                      "avg_launch_ms": tot_score_ms / max(1, tot_launch)},
         "cpu_baseline": cpu,
+        "parity_sample": parity,
         "clocks": clk.summary(),
         "c5_sharded_pair": c5,
         "c3_flashmatch": c3,
@@ -495,6 +513,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--parity-pairs", type=int, default=2, help="pairs of the timed batch re-checked against the reference")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c5", action="store_true", help="skip the sharded 1536x1152 pair (config C5)")
     ap.add_argument("--no-c3", action="store_true", help="skip the FlashMatch attention section (config C3)")
