@@ -69,6 +69,18 @@ def test_nn_tensor_equals_reference_on_half_inputs(fnl, ref, metric):
         assert np.array_equal(ours["min_dist"].view(np.uint32), theirs["min_dist"].view(np.uint32))
 
 
+@pytest.mark.parametrize("nq", [1, 63, 64, 65, 127, 192, 255, 256, 257, 321, 513])
+def test_nn_tensor_merge_slice_boundaries(fnl, ref, nq):
+    """Query counts around the merge kernel's 64-row slices and 256-row tile
+    pairs (ragged last slice, empty trailing slices, multi-tile-pair)."""
+    A = ref.gen_random(1, nq, 24, 500 + nq)
+    B = ref.gen_random(48, 40, 24, 600 + nq)
+    ours = fnl.nn_tensor(A, B, "dot")
+    theirs = ref.nn_single_loop(h16(A), h16(B), metric="dot", precision="full")
+    assert np.array_equal(ours["nearest"], theirs["nearest"])
+    assert np.array_equal(ours["min_dist"].view(np.uint32), theirs["min_dist"].view(np.uint32))
+
+
 def test_nn_tensor_ties_and_duplicates(fnl, ref):
     # duplicated targets force exact ties: lowest index must win via the rescan
     rng = np.random.default_rng(3)
