@@ -40,7 +40,13 @@ enum fnl_precision { FNL_PREC_FULL = 0, FNL_PREC_HYBRID = 1 };
 /* include/fastnn/nn.hpp:20 (NnBackend) plus the tensor-core HybridCast path.
  * FNL_BACKEND_TENSOR: binary16 cast-in, tcgen05 fp32 accumulate, fp32 compare
  * (Alg. 3); near ties are re-decided by the exact FMA chain, so the
- * result equals the reference `single` backend run on binary16-rounded maps. */
+ * result equals the reference `single` backend run on binary16-rounded maps.
+ * The reference backends keep their own arithmetic bit for bit: they take the
+ * same tensor route (tcgen05 scores nominate 64-target sub-tiles, the winner is
+ * decided by the reference chain on the fp32 rows -- or, for hybrid, on the
+ * binary16 rows with the binary16 distance cast) whenever dim <= 32 (dot) /
+ * 30 (l2), the inputs are finite and nothing saturates in binary16, and run on
+ * the CUDA-core exact scan otherwise (or with FNL_EXACT_KERNEL=cuda_core). */
 enum fnl_backend {
     FNL_BACKEND_BRUTEFORCE = 0,
     FNL_BACKEND_DOUBLE = 1,
@@ -74,13 +80,19 @@ typedef struct {
     uint64_t a_block_fetches;
     uint64_t b_block_fetches;
     uint64_t half_saturation_events;
-    /* tensor backend only: rows whose tensor-core top-2 gap fell inside the
-     * certified error band and were re-decided by the exact chain */
+    /* tensor route only: rows whose first candidate sub-tile did not settle
+     * the winner (tensor-core top-2 gap inside the certified error band) */
     uint64_t near_tie_rows;
     uint64_t query_rows; /* total NN query rows issued (forward + reverse) */
     /* device time of each phase (CUDA events on the context stream), shared by
      * all pairs of one batched launch; RunReport *_us fields */
     double subsample_us, forward_nn_us, reverse_nn_us, harvest_us;
+    /* tensor route only: rows whose three candidate sub-tiles did not settle
+     * the winner and were re-decided over every target (K4' rescan) */
+    uint64_t rescan_rows;
+    /* 1 when the run took the tensor route (K1 pack + tcgen05 K3 + certified
+     * resolution), 0 when it ran on the CUDA-core exact scan K4 */
+    uint32_t tensor_route;
 } fnl_run_stats;
 
 typedef struct fnl_context fnl_context;

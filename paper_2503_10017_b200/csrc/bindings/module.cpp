@@ -98,6 +98,8 @@ py::dict stats_dict(const fnl_run_stats& s) {
     d["b_block_fetches"] = s.b_block_fetches;
     d["half_saturation_events"] = s.half_saturation_events;
     d["near_tie_rows"] = s.near_tie_rows;
+    d["rescan_rows"] = s.rescan_rows;
+    d["tensor_route"] = s.tensor_route;
     d["query_rows"] = s.query_rows;
     d["forward_nn_us"] = s.forward_nn_us;
     d["reverse_nn_us"] = s.reverse_nn_us;

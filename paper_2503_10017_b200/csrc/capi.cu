@@ -216,6 +216,13 @@ bool backend_hybrid(int backend, int precision) {
     return precision == FNL_PREC_HYBRID;
 }
 
+// FNL_EXACT_KERNEL=cuda_core keeps the reference backends on the CUDA-core
+// exact scan K4 (tests pin both kernels); read per call so a test can flip it
+bool force_cuda_core() {
+    const char* e = getenv("FNL_EXACT_KERNEL");
+    return e && strcmp(e, "cuda_core") == 0;
+}
+
 std::string nonfinite_msg(uint64_t idx) {
     return "FeatureMap: non-finite value at flat index " + std::to_string(idx);
 }
@@ -518,13 +525,23 @@ extern "C" int fnl_nn_query(fnl_context* ctx, const float* h_q, uint32_t nq, con
     FNL_CUDA_TRY(cudaMemcpyAsync(dt, h_t, (size_t)nt * dim * 4, cudaMemcpyHostToDevice, ctx->stream));
     FNL_CUDA_TRY(cudaMemsetAsync(keys, 0xFF, (size_t)nq * 8, ctx->stream));
     FNL_CUDA_TRY(cudaMemsetAsync(cnt, 0, 16, ctx->stream));
-    Prepared pq, pt;
-    TRY(prepare_maps(ctx, "nn.pq", dq, 1, nq, dim, hyb, false, &pq, bad));
-    TRY(prepare_maps(ctx, "nn.pt", dt, 1, nt, dim, hyb, false, &pt, bad));
 
-    if (backend == FNL_BACKEND_TENSOR) {
-        TRY(fnl::tensor_nn_dense(ctx, dq, nq, dt, nt, dim, l2, dnear, dmd));
-    } else {
+    // Tensor route (K1 pack + K3 tcgen05 scores + certified exact resolution
+    // in the backend's own arithmetic) whenever the inputs allow it; else the
+    // CUDA-core exact scan K4.  Both are bit-identical to the reference.
+    const int mode = backend == FNL_BACKEND_TENSOR ? fnl::kResolveRounded
+                                                   : (hyb ? fnl::kResolveHybrid : fnl::kResolveFull);
+    bool routed = false;
+    if (backend == FNL_BACKEND_TENSOR || !force_cuda_core())
+        TRY(fnl::tensor_nn_dense(ctx, dq, nq, dt, nt, dim, l2, dnear, dmd, mode, &routed));
+    unsigned long long h_cnt[2] = {0, 0}, h_ms[2] = {0, 0};
+    if (!routed) {
+        // the tensor backend's contract is ref single on binary16-rounded
+        // rows: K4 on the rounded rows, fp32 compare
+        const bool round_in = hyb || backend == FNL_BACKEND_TENSOR;
+        Prepared pq, pt;
+        TRY(prepare_maps(ctx, "nn.pq", dq, 1, nq, dim, round_in, false, &pq, bad));
+        TRY(prepare_maps(ctx, "nn.pt", dt, 1, nt, dim, round_in, false, &pt, bad));
         fnl::ScanArgs sa{};
         sa.qmap = pq.data;
         sa.qcount_const = nq;
@@ -543,15 +560,20 @@ extern "C" int fnl_nn_query(fnl_context* ctx, const float* h_q, uint32_t nq, con
         fa.nearest_pair_stride = nq;
         fa.min_dist = dmd;
         fa.dot = !l2;
+        fa.hybrid = hyb;
+        fa.qmap = pq.data;
+        fa.tmap = pt.data;
+        fa.dim = dim;
         TRY(exact_nn(ctx, sa, nq, 1, l2, hyb, fa));
+        FNL_CUDA_TRY(cudaMemcpyAsync(h_cnt, cnt, 16, cudaMemcpyDeviceToHost, ctx->stream));
+        FNL_CUDA_TRY(cudaMemcpyAsync(&h_ms[0], pq.map_sat, 8, cudaMemcpyDeviceToHost, ctx->stream));
+        FNL_CUDA_TRY(cudaMemcpyAsync(&h_ms[1], pt.map_sat, 8, cudaMemcpyDeviceToHost, ctx->stream));
     }
+    // (routed: no input or distance saturates -- tensor_route_ok -- so the
+    // reference's hybrid saturation count is 0)
     FNL_CUDA_TRY(cudaMemcpyAsync(h_nearest, dnear, (size_t)nq * 4, cudaMemcpyDeviceToHost, ctx->stream));
     if (h_min_dist)
         FNL_CUDA_TRY(cudaMemcpyAsync(h_min_dist, dmd, (size_t)nq * 4, cudaMemcpyDeviceToHost, ctx->stream));
-    unsigned long long h_cnt[2] = {0, 0}, h_ms[2] = {0, 0};
-    FNL_CUDA_TRY(cudaMemcpyAsync(h_cnt, cnt, 16, cudaMemcpyDeviceToHost, ctx->stream));
-    FNL_CUDA_TRY(cudaMemcpyAsync(&h_ms[0], pq.map_sat, 8, cudaMemcpyDeviceToHost, ctx->stream));
-    FNL_CUDA_TRY(cudaMemcpyAsync(&h_ms[1], pt.map_sat, 8, cudaMemcpyDeviceToHost, ctx->stream));
     FNL_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     timing_harvest(ctx);
 
@@ -658,11 +680,13 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
     FNL_CUDA_TRY(cudaMemsetAsync(counters, 0, (size_t)max_calls * npairs * 16, s));
     FNL_CUDA_TRY(cudaMemsetAsync(bad, 0xFF, 16, s));
 
-    // ---- K1: validate + (hybrid) round, or binary16 pack for the tensor path
+    // ---- K1: binary16 pack for the tensor route, or validate + (hybrid)
+    // round for the CUDA-core exact scan.  Every backend takes the tensor
+    // route (K3 scores + certified resolution in the backend's arithmetic,
+    // bit-identical to the reference) when the inputs allow it.
     const bool tensor = backend == FNL_BACKEND_TENSOR;
     const bool sharded = shard && shard->count > 1;
     if (shard) {
-        if (!tensor) return fail(FNL_EINVAL, "sharded reciprocal_match: tensor backend only");
         if (shard->count == 0 || shard->rank >= shard->count)
             return fail(FNL_EINVAL, "sharded reciprocal_match: rank must be < count");
         const bool peer = sharded && shard->peer_keys;
@@ -674,42 +698,64 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
             return fail(FNL_EINVAL, "sharded reciprocal_match (peer memory): at most 8 ranks, key buffers of "
                                     "2 * npairs * samples, flags and barrier_seq required");
     }
+    const int mode = tensor ? fnl::kResolveRounded : (hyb ? fnl::kResolveHybrid : fnl::kResolveFull);
+    bool tc = false;  // tensor route taken
     Prepared P1, P2;
     fnl::PackedMaps T1, T2;
     unsigned long long *near_ties = nullptr, *tsat = nullptr;
-    TRY(dev_arr(ctx, "m.neartie", npairs, &near_ties));
+    TRY(dev_arr(ctx, "m.neartie", 2 * (size_t)npairs, &near_ties));
     TRY(dev_arr(ctx, "m.tsat", 2 * (size_t)npairs, &tsat));
-    FNL_CUDA_TRY(cudaMemsetAsync(near_ties, 0, (size_t)npairs * 8, s));
+    FNL_CUDA_TRY(cudaMemsetAsync(near_ties, 0, (size_t)npairs * 16, s));
     FNL_CUDA_TRY(cudaMemsetAsync(tsat, 0, (size_t)npairs * 16, s));
-    if (tensor) {
+    const bool fits = dim + (l2 ? 2u : 0u) <= fnl::kPackK;
+    if ((tensor && fits) || (!tensor && fits && !force_cuda_core())) {
         unsigned long long* tbad;
         TRY(dev_arr(ctx, "m.tbad", 2 * (size_t)npairs, &tbad));
         FNL_CUDA_TRY(cudaMemsetAsync(tbad, 0xFF, (size_t)npairs * 16, s));
         TRY(fnl::tensor_pack(ctx, "m.t1", d_d1, npairs, p1, dim, l2, tbad, tsat, &T1));
         TRY(fnl::tensor_pack(ctx, "m.t2", d_d2, npairs, p2, dim, l2, tbad + npairs, tsat + npairs, &T2));
-        // host-buffer entry points validate finiteness like the reference
-        // FeatureMap (a host round trip); the device-resident batch API does not
-        if (validate) {
-            std::vector<unsigned long long> hb(2 * (size_t)npairs);
+        tc = true;
+        // The host reads the pack's per-pair finiteness / norms / saturations
+        // when it must: to validate like the reference FeatureMap (host-buffer
+        // entry points) and to check the route (the tensor backend on dot
+        // maps is always eligible, so the device-resident batch path of the
+        // bench has no host round trip here).
+        if (validate || !tensor || l2) {
+            std::vector<unsigned long long> hb(2 * (size_t)npairs), hs(2 * (size_t)npairs);
+            std::vector<float> hn(2 * (size_t)npairs);
             FNL_CUDA_TRY(cudaMemcpyAsync(hb.data(), tbad, hb.size() * 8, cudaMemcpyDeviceToHost, s));
+            FNL_CUDA_TRY(cudaMemcpyAsync(hs.data(), tsat, hs.size() * 8, cudaMemcpyDeviceToHost, s));
+            FNL_CUDA_TRY(cudaMemcpyAsync(hn.data(), T1.max_norm, npairs * 4, cudaMemcpyDeviceToHost, s));
+            FNL_CUDA_TRY(cudaMemcpyAsync(hn.data() + npairs, T2.max_norm, npairs * 4, cudaMemcpyDeviceToHost, s));
             FNL_CUDA_TRY(cudaStreamSynchronize(s));
-            for (uint32_t p = 0; p < npairs; ++p)
-                if (hb[p] != ~0ull) return fail(FNL_EINVAL, nonfinite_msg(hb[p]));
-            for (uint32_t p = 0; p < npairs; ++p)
-                if (hb[npairs + p] != ~0ull) return fail(FNL_EINVAL, nonfinite_msg(hb[npairs + p]));
+            if (validate) {
+                // D1 is checked before D2, as the reference converts D1 first
+                // (bindings/module.cpp:232-233); indices are flat within one map
+                for (uint32_t p = 0; p < npairs; ++p)
+                    if (hb[p] != ~0ull) return fail(FNL_EINVAL, nonfinite_msg(hb[p]));
+                for (uint32_t p = 0; p < npairs; ++p)
+                    if (hb[npairs + p] != ~0ull) return fail(FNL_EINVAL, nonfinite_msg(hb[npairs + p]));
+            }
+            for (uint32_t p = 0; p < npairs && tc; ++p)
+                tc = fnl::tensor_route_ok(mode, l2, dim, hn[p], hn[npairs + p], hs[p] + hs[npairs + p],
+                                          std::min(hb[p], hb[npairs + p]));
         }
-    } else {
-        TRY(prepare_maps(ctx, "m.p1", d_d1, npairs, p1, dim, hyb, validate, &P1, bad));
-        TRY(prepare_maps(ctx, "m.p2", d_d2, npairs, p2, dim, hyb, validate, &P2, bad + 1));
     }
-    if (validate && !tensor) {
-        // D1 is checked before D2, as the reference converts D1 first
-        // (bindings/module.cpp:232-233); indices are flat within one map.
-        unsigned long long hb[2] = {~0ull, ~0ull};
-        FNL_CUDA_TRY(cudaMemcpyAsync(hb, bad, 16, cudaMemcpyDeviceToHost, s));
-        FNL_CUDA_TRY(cudaStreamSynchronize(s));
-        if (hb[0] != ~0ull) return fail(FNL_EINVAL, nonfinite_msg(hb[0] % ((uint64_t)p1 * dim)));
-        if (hb[1] != ~0ull) return fail(FNL_EINVAL, nonfinite_msg(hb[1] % ((uint64_t)p2 * dim)));
+    if (shard && !tc)
+        return fail(FNL_EINVAL, "sharded reciprocal_match: needs the tensor route (descriptor dim <= 32 for dot, "
+                                "<= 30 for l2; finite inputs without binary16 saturation)");
+    if (!tc) {
+        // the tensor backend's contract is ref single on binary16-rounded
+        // rows: K4 on the rounded rows, fp32 compare
+        TRY(prepare_maps(ctx, "m.p1", d_d1, npairs, p1, dim, hyb || tensor, validate, &P1, bad));
+        TRY(prepare_maps(ctx, "m.p2", d_d2, npairs, p2, dim, hyb || tensor, validate, &P2, bad + 1));
+        if (validate) {
+            unsigned long long hb[2] = {~0ull, ~0ull};
+            FNL_CUDA_TRY(cudaMemcpyAsync(hb, bad, 16, cudaMemcpyDeviceToHost, s));
+            FNL_CUDA_TRY(cudaStreamSynchronize(s));
+            if (hb[0] != ~0ull) return fail(FNL_EINVAL, nonfinite_msg(hb[0] % ((uint64_t)p1 * dim)));
+            if (hb[1] != ~0ull) return fail(FNL_EINVAL, nonfinite_msg(hb[1] % ((uint64_t)p2 * dim)));
+        }
     }
     PhaseTimer timer{ctx};
     timer.enabled = h_stats != nullptr;
@@ -731,14 +777,20 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
     uint32_t peer_pass = 0;
     auto nn_pass = [&](const Prepared& Q, uint32_t qrows, const uint32_t* ids, const Prepared& Tm,
                        uint32_t nt, uint32_t* out) -> int {
-        if (tensor) {
-            const fnl::PackedMaps& TQ = (qrows == p1 && ids == m.active_u) ? T1 : T2;
-            const fnl::PackedMaps& TT = (qrows == p1 && ids == m.active_u) ? T2 : T1;
+        if (tc) {
+            const bool fwd = qrows == p1 && ids == m.active_u;
+            const fnl::PackedMaps& TQ = fwd ? T1 : T2;
+            const fnl::PackedMaps& TT = fwd ? T2 : T1;
+            fnl::ResolveSrc rs;
+            rs.mode = mode;
+            rs.q32 = fwd ? d_d1 : d_d2;
+            rs.q32_pair_stride = (uint64_t)(fwd ? p1 : p2) * dim;
+            rs.t32 = fwd ? d_d2 : d_d1;
+            rs.t32_pair_stride = (uint64_t)(fwd ? p2 : p1) * dim;
             ++call;
             if (!sharded)
                 return fnl::tensor_nn_pass(ctx, npairs, TQ, ids, cap, m.n_active, m.done, TT, dim, l2, out, cap,
-                                           nullptr, near_ties);
-            // target shard of this rank: contiguous 128-target tiles
+                                           nullptr, near_ties, 0, 0, nullptr, nullptr, &rs);            // target shard of this rank: contiguous 128-target tiles
             const uint64_t tiles = ceil_div(nt, fnl::kTargetTileRows);
             const uint32_t tb = (uint32_t)(tiles * shard->rank / shard->count);
             const uint32_t te = (uint32_t)(tiles * (shard->rank + 1) / shard->count);
@@ -757,7 +809,7 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
                 long long* own = reinterpret_cast<long long*>(shard->d_keys) + par * nkeys;
                 if (te > tb)
                     TRY(fnl::tensor_nn_pass(ctx, npairs, TQ, ids, cap, m.n_active, m.done, TT, dim, l2, out, cap,
-                                            nullptr, near_ties, tb, te, own, &pp));
+                                            nullptr, near_ties, tb, te, own, &pp, &rs));
                 const uint64_t seq = ++*shard->barrier_seq;
                 TRY(fnl::tensor_shard_barrier(ctx, reinterpret_cast<unsigned int* const*>(shard->peer_flags),
                                               shard->count,
@@ -770,7 +822,7 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
             if (te > tb)
                 TRY(fnl::tensor_nn_pass(ctx, npairs, TQ, ids, cap, m.n_active, m.done, TT, dim, l2, out, cap,
                                         nullptr, near_ties, tb, te,
-                                        reinterpret_cast<long long*>(shard->d_keys)));
+                                        reinterpret_cast<long long*>(shard->d_keys), nullptr, &rs));
             if (shard->reduce(shard->user, shard->d_keys, nkeys, ctx->stream) != 0)
                 return fail(FNL_ERUNTIME, "sharded reciprocal_match: key reduction callback failed");
             return fnl::tensor_shard_finalize(ctx, npairs, reinterpret_cast<const long long*>(shard->d_keys), cap,
@@ -806,7 +858,7 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
 
     unsigned int* lag_done = nullptr;  // pinned [2]: n_done after iterations t-1, t
     cudaEvent_t* lag_ev = nullptr;
-    if (tensor) {
+    if (tc) {
         TRY(fnl::ws_pinned(ctx, "m.lagdone", 8, (void**)&lag_done));
         TRY(lag_events(ctx, &lag_ev));
     }
@@ -826,7 +878,7 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
         }
         timer.end();
         ctx->total_launches += 1;
-        if (tensor) {
+        if (tc) {
             // Lagged convergence check: iteration t is enqueued before the
             // host looks at the done count of iteration t-1, so the GPU never
             // idles on the round trip.  Passes enqueued after the last pair
@@ -865,12 +917,12 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
         std::vector<uint32_t> npr(npairs);
         FNL_CUDA_TRY(cudaMemcpyAsync(st.data(), m.stats, st.size() * 4, cudaMemcpyDeviceToHost, s));
         FNL_CUDA_TRY(cudaMemcpyAsync(cnt.data(), counters, cnt.size() * 8, cudaMemcpyDeviceToHost, s));
-        if (!tensor) {
+        if (!tc) {
             FNL_CUDA_TRY(cudaMemcpyAsync(ms1.data(), P1.map_sat, npairs * 8, cudaMemcpyDeviceToHost, s));
             FNL_CUDA_TRY(cudaMemcpyAsync(ms2.data(), P2.map_sat, npairs * 8, cudaMemcpyDeviceToHost, s));
         }
         FNL_CUDA_TRY(cudaMemcpyAsync(npr.data(), m.n_pairs, npairs * 4, cudaMemcpyDeviceToHost, s));
-        std::vector<unsigned long long> tsat_h(2 * (size_t)npairs), ties_h(npairs);
+        std::vector<unsigned long long> tsat_h(2 * (size_t)npairs), ties_h(2 * (size_t)npairs);
         FNL_CUDA_TRY(cudaMemcpyAsync(tsat_h.data(), tsat, tsat_h.size() * 8, cudaMemcpyDeviceToHost, s));
         FNL_CUDA_TRY(cudaMemcpyAsync(ties_h.data(), near_ties, ties_h.size() * 8, cudaMemcpyDeviceToHost, s));
         FNL_CUDA_TRY(cudaStreamSynchronize(s));
@@ -921,9 +973,11 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
                     if (hyb) o.half_saturation_events += tsat + qs + ds;
                 }
             }
-            if (tensor) {
-                o.half_saturation_events = tsat_h[p] + tsat_h[npairs + p];
+            if (tensor) o.half_saturation_events = tsat_h[p] + tsat_h[npairs + p];
+            if (tc) {
                 o.near_tie_rows = ties_h[p];
+                o.rescan_rows = ties_h[npairs + p];
+                o.tensor_route = 1;
             }
         }
     }
@@ -1230,6 +1284,11 @@ extern "C" int fnl_mutual_nn(fnl_context* ctx, const float* h_d1, uint32_t h1, u
     FNL_CUDA_TRY(cudaMemsetAsync(k2, 0xFF, (size_t)p2 * 8, s));
     auto pass = [&](const float* q, uint32_t nq, const float* t, uint32_t nt,
                     unsigned long long* keys, uint32_t* out) -> int {
+        if (!force_cuda_core()) {  // tensor route, full-precision resolution
+            bool routed = false;
+            TRY(fnl::tensor_nn_dense(ctx, q, nq, t, nt, dim, l2, out, nullptr, fnl::kResolveFull, &routed));
+            if (routed) return FNL_OK;
+        }
         fnl::ScanArgs sa{};
         sa.qmap = q;
         sa.qcount_const = nq;

@@ -258,7 +258,16 @@ __global__ void finalize_kernel(FinalizeArgs a) {
     a.nearest[(size_t)pair * a.nearest_pair_stride + q] = (uint32_t)(key & 0xFFFFFFFFull);
     if (a.min_dist) {
         float d = from_orderable((uint32_t)(key >> 32));
-        if (d == 0.0f) d = a.dot ? -0.0f : 0.0f;  // canonical sign of an exact zero
+        if (d == 0.0f) {
+            if (a.hybrid && a.qmap) {  // the winner's own signed zero
+                const uint32_t idx = (uint32_t)(key & 0xFFFFFFFFull);
+                const float* qr = a.qmap + (size_t)q * a.dim;
+                const float* tr = a.tmap + (size_t)idx * a.dim;
+                d = half_round_nosat(a.dot ? chain<false>(qr, tr, a.dim) : chain<true>(qr, tr, a.dim));
+            } else {
+                d = a.dot ? -0.0f : 0.0f;  // canonical sign of an exact zero (fp32 chain)
+            }
+        }
         a.min_dist[(size_t)pair * a.nearest_pair_stride + q] = d;
     }
 }

@@ -102,6 +102,13 @@ struct FinalizeArgs {
     uint32_t nearest_pair_stride;
     float* min_dist;              // may be null
     bool dot;                     // exact zero distance is -0.0f under NegativeDot
+    // hybrid min_dist: a binary16-cast distance that rounds to zero keeps the
+    // winner's sign (h(-acc) is -0 for tiny positive acc, +0 for negative), so
+    // a zero is re-evaluated from the (rounded) rows; dense queries only
+    bool hybrid;
+    const float* qmap;
+    const float* tmap;
+    uint32_t dim;
 };
 cudaError_t launch_finalize(const FinalizeArgs& a, uint32_t max_q, uint32_t npairs, cudaStream_t s);
 

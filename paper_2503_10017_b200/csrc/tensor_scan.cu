@@ -30,6 +30,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -225,6 +226,7 @@ struct GatherArgs {
     uint32_t dim;
     bool l2;
     const uint32_t* nslots;  // device slot count (plan header), or null = gridDim.y
+    int mode;                // ResolveMode the margin is for
 };
 
 __global__ void gather_kernel(GatherArgs a) {
@@ -258,20 +260,34 @@ __global__ void gather_kernel(GatherArgs a) {
     ss += __shfl_xor_sync(0xFFFFFFFFu, ss, 2);
     *reinterpret_cast<uint4*>(a.qbuf + packed_offset(drow, chunk)) = val;
     if (chunk == 0) {
-        // Certification margin (score units), see DESIGN.md "certified argmax":
-        //   tensor-core accumulation error <= 2^-16 * sum|products| per score,
-        //   reference FMA chain error <= (d+2) 2^-24 * sum|terms| per distance,
-        //   l2 norm split / fp32 norm error <= 2^-20 |t|^2.
-        const float qn = sqrtf(ss) * 1.0001f, tn = a.tmax[pair] * 1.0001f;
-        const float d = (float)a.dim;
+        // One-sided certification margin M (score units, larger is better):
+        // for EVERY target t, the score the resolve mode's exact arithmetic
+        // gives t is <= tc_score(t) + M, so a target whose tensor-core score
+        // bound B satisfies exact_winner > B + M provably loses (DESIGN.md
+        // "certified argmax").  Terms, with |q| <= qn and |t| <= tn:
+        //   tensor-core accumulation          2^-15 (qn tn + tn^2 [l2])
+        //   reference FMA chain rounding      (d+2) 2^-24 qn tn            (dot)
+        //                                     (d+2) 2^-25 (qn + tn)^2      (l2, half a distance)
+        //   l2: -|t|^2/2 as binary16 hi + lo  2^-20 tn^2, query |q|^2 chain (d+2) 2^-25 qn^2
+        //   kResolveFull: binary16 input rounding of q and t (u = 2^-11, subnormal step 2^-24)
+        //                                     2^-10 qn tn + 2^-24 sqrt(d) (qn + tn) (+ 2^-11 tn^2 l2)
+        // The norms are of the binary16 rows; the fp32 rows differ by <= u
+        // relative plus 2^-25 per channel, covered by the 1.001 / additive
+        // inflation.
+        const float d = (float)a.dim, sd = sqrtf(d);
+        const float qn = sqrtf(ss) * 1.001f + ldexpf(sd, -24);
+        const float tn = a.tmax[pair] * 1.001f + ldexpf(sd, -24);
+        const bool full = a.mode == kResolveFull;
         float m;
         if (!a.l2) {
             const float A = qn * tn;
-            m = 2.0f * ldexpf(A, -16) + 2.0f * (d + 2.0f) * ldexpf(A, -24);
+            m = ldexpf(A, -15) + (d + 2.0f) * ldexpf(A, -24);
+            if (full) m += ldexpf(A, -10) + ldexpf(sd * (qn + tn), -24);
         } else {
             const float A = qn * tn + tn * tn;
             const float S = (qn + tn) * (qn + tn);
-            m = 2.0f * ldexpf(A, -16) + (d + 2.0f) * ldexpf(S, -24) + 2.0f * ldexpf(tn * tn, -20);
+            m = ldexpf(A, -15) + (d + 2.0f) * ldexpf(S, -25) + ldexpf(tn * tn, -20) + (d + 2.0f) * ldexpf(qn * qn, -25);
+            if (full) m += ldexpf(qn * tn, -10) + ldexpf(tn * tn, -11) + ldexpf(sd * (qn + tn), -24);
         }
         a.margin[drow] = 1.25f * m + 1e-30f;
     }
@@ -297,7 +313,7 @@ struct TcArgs {
     uint32_t nt;
     const TcItem* items;
     const uint32_t* nitems;  // device item count (plan header)
-    float4* partial;  // [item][col half][256][2] = (b1, b2, b3, t1 bits), (t2 bits, 0, 0, 0)
+    float4* partial;  // [item][col half][256][2] = (b1, b2, b3, b4), (t1, t2, t3 bits, 0)
     int debug;        // profiling only: 1 = epilogue releases buffers unread, 16 = clock trace of CTA 0
     unsigned long long* trace;  // [4][4096] clock64 stamps (debug & 16)
 };
@@ -335,14 +351,15 @@ constexpr uint32_t kSubTile = 64;  // winner granularity handed to the merge
 
 // Per query row and 64-target sub-tile: m = max of the 64 fp32 scores
 // (3-input-max tree, ~0.5 ALU op per score, no data-dependent branch), then a
-// branch-free insert of (m, sub-tile) into the row's top-3 of sub-tile maxima:
-// b1 >= b2 >= b3 with the sub-tiles t1, t2 of the first two.  The merge kernel
-// certifies b1 - b2 > margin (the reference winner lies in t1) or else
-// b1 - b3 > margin (it lies in t1 or t2) and resolves those sub-tiles with the
-// exact chain; only rows with three sub-tiles inside the margin are re-scanned.
+// branch-free insert of (m, sub-tile) into the row's top-4 of sub-tile maxima:
+// b1 >= b2 >= b3 >= b4 with the sub-tiles t1, t2, t3 of the first three.  The
+// merge resolves t1, then t2, then t3 with the exact reference chain, and
+// closes the row as soon as the exact winner beats the next bound (b2, b3 or
+// b4) by the certification margin; only rows with four sub-tiles inside the
+// margin are re-scanned.
 struct RowState {
-    float b1, b2, b3;
-    uint32_t t1, t2;
+    float b1, b2, b3, b4;
+    uint32_t t1, t2, t3;
 };
 
 __device__ __forceinline__ float tile_max64(const float* v) {
@@ -358,7 +375,9 @@ __device__ __forceinline__ float tile_max64(const float* v) {
 }
 
 __device__ __forceinline__ void tile_update(RowState& st, float m, uint32_t tile) {
-    const bool gt1 = m > st.b1, gt2 = m > st.b2;
+    const bool gt1 = m > st.b1, gt2 = m > st.b2, gt3 = m > st.b3;
+    st.b4 = fmaxf(st.b4, fminf(st.b3, m));
+    st.t3 = gt2 ? st.t2 : (gt3 ? tile : st.t3);
     st.b3 = fmaxf(st.b3, fminf(st.b2, m));
     st.t2 = gt1 ? st.t1 : (gt2 ? tile : st.t2);
     st.b2 = fmaxf(st.b2, fminf(st.b1, m));
@@ -384,7 +403,7 @@ __device__ __forceinline__ void subtile_scan(RowState& st, const Frag& f, const 
     // statistics: ~3 ln(#sub-tiles) updates per row over a whole scan), so the
     // branch-free top-3 insert runs only when some lane of the warp needs it
     const float m = tile_max64(v);
-    if (__any_sync(0xFFFFFFFFu, m > st.b3)) tile_update(st, m, sub);
+    if (__any_sync(0xFFFFFFFFu, m > st.b4)) tile_update(st, m, sub);
 }
 
 __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
@@ -510,7 +529,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
         Frag f0, f1;
         for (uint32_t u = blockIdx.x; u < nitems; u += G) {
             const TcItem item = a.items[u];
-            RowState st{-INFINITY, -INFINITY, -INFINITY, 0xFFFFFFFFu, 0xFFFFFFFFu};
+            RowState st{-INFINITY, -INFINITY, -INFINITY, -INFINITY, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
             const bool warp_real = qt * 128u + quad * 32u < item.nvalid;  // else all rows padding
             for (uint32_t t = item.tile_begin; t < item.tile_end; ++t, ++k) {
                 mbar_wait(&tfull[qt * 2 + h], k & 1u);
@@ -547,7 +566,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&accfree[qt * 2 + h]);  // this warp's 128 columns drained
                 if (tw && lane == 0) a.trace[16384 + k] = clock64();
-                if (__any_sync(0xFFFFFFFFu, m0 > st.b3)) tile_update(st, m0, sub0);
+                if (__any_sync(0xFFFFFFFFu, m0 > st.b4)) tile_update(st, m0, sub0);
                 subtile_scan(st, f0, f1, sub0 + 1, a.nt);
                 if (tw) {
                     __syncwarp();
@@ -556,8 +575,8 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
             }
             const uint32_t row = qt * 128u + quad * 32u + lane;  // 0..255 within the tile pair
             float4* po = a.partial + (((uint64_t)u * kPartialSplit + h) * kQueryTilePair + row) * 2;
-            po[0] = make_float4(st.b1, st.b2, st.b3, __uint_as_float(st.t1));
-            po[1] = make_float4(__uint_as_float(st.t2), 0.0f, 0.0f, 0.0f);
+            po[0] = make_float4(st.b1, st.b2, st.b3, st.b4);
+            po[1] = make_float4(__uint_as_float(st.t1), __uint_as_float(st.t2), __uint_as_float(st.t3), 0.0f);
         }
     }
     tc_fence_before();
@@ -587,9 +606,13 @@ struct MergeArgs {
     uint32_t out_stride;
     uint32_t* rescan;           // (gathered row, pair, qi) triples
     unsigned int* rescan_count;
-    unsigned long long* near_ties;  // per pair
+    unsigned long long* near_ties;  // [p] rows not closed by T1, [npairs + p] rows sent to the rescan
+    uint32_t npairs;
     long long* shard_keys;      // sharded mode: signed winner keys instead of out/min_dist
     ShardPeers peers;           // sharded mode over peer memory (peers.n > 0)
+    const uint32_t* ids;        // query ids of the pass (null = identity), pair stride cap
+    uint32_t cap;
+    ResolveSrc rs;              // kResolveFull: original fp32 rows
 };
 
 // sharded mode: this rank's winner key of output slot o -- a local store, or
@@ -602,130 +625,6 @@ __device__ __forceinline__ void shard_emit(long long* local, const ShardPeers& p
     for (uint32_t r = 0; r < p.n; ++r) atomicMin_system(p.keys[r] + o, key);
 }
 
-template <bool kL2, int DIM>
-__device__ __forceinline__ float packed_chain(const float (&q)[kPackK], const uint8_t* map, uint32_t row,
-                                              uint32_t dim);
-__device__ __forceinline__ void load_query(const uint8_t* qbuf, uint32_t grow, float (&q)[kPackK]);
-
-// One CTA per 64-row slice of a tile pair: phase 2 is a chain of dependent
-// L2/HBM loads per row, so the kernel is latency bound and wants many rows in
-// flight -- four slices per tile pair give each warp 8 rows instead of 32
-// (measured: 1.07 -> 0.74 ms per 128-pair step; 32-row slices: 0.84 ms).
-constexpr uint32_t kMergeRows = 64;
-constexpr uint32_t kMergeSlices = kQueryTilePair / kMergeRows;
-constexpr uint32_t kMergeThreads = 256;
-
-template <bool kL2, int DIM>
-__global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs a) {
-    // phase 1 (thread per row): certification from the split partials
-    // phase 2 (warp per row): exact resolution of the candidate sub-tiles, two
-    //   targets per lane, coalesced 16 B loads, (dist, index) key reduction
-    __shared__ uint32_t s_t[kMergeRows][2];  // candidate sub-tiles; t[1] = ~0 when one suffices
-    __shared__ uint32_t s_go[kMergeRows];    // 1 = resolve here
-    const uint32_t tp = blockIdx.x / kMergeSlices, slice = blockIdx.x % kMergeSlices;
-    if (tp >= a.hdr[1]) return;
-    const uint32_t splits = a.hdr[3];
-    const uint32_t pair = a.tp_pair[tp];
-    const uint32_t tp_rows = min(kQueryTilePair, a.n_active[pair] - a.tp_qi0[tp]);
-    if (slice * kMergeRows >= tp_rows) return;  // CTA-uniform
-    const uint32_t nrows = min(kMergeRows, tp_rows - slice * kMergeRows);
-    const uint32_t row0 = a.tp_row0[tp] + slice * kMergeRows;  // first gathered row of the slice
-    const uint32_t qi0 = a.tp_qi0[tp] + slice * kMergeRows;     // its query index within the pair
-    const uint32_t r = threadIdx.x;
-    if (r < kMergeRows) s_go[r] = 0;
-    if (r < nrows) {
-        // global top-3 of sub-tile maxima over the target splits: each split's
-        // (b1, t1), (b2, t2) are candidates, its b3 bounds every other sub-tile
-        float B1 = -INFINITY, B2 = -INFINITY, B3 = -INFINITY;
-        uint32_t T1 = 0, T2 = 0xFFFFFFFFu;
-        auto insert = [&](float v, uint32_t t) {
-            if (v > B1) {
-                B3 = fmaxf(B3, B2);
-                B2 = B1;
-                T2 = T1;
-                B1 = v;
-                T1 = t;
-            } else if (v > B2) {
-                B3 = fmaxf(B3, B2);
-                B2 = v;
-                T2 = t;
-            } else {
-                B3 = fmaxf(B3, v);
-            }
-        };
-        for (uint32_t s = 0; s < splits * kPartialSplit; ++s) {
-            const float4* pp =
-                a.partial + (((uint64_t)tp * splits * kPartialSplit + s) * kQueryTilePair + slice * kMergeRows + r) * 2;
-            const float4 p = pp[0];
-            const float4 p2 = pp[1];
-            insert(p.x, __float_as_uint(p.w));
-            insert(p.y, __float_as_uint(p2.x));
-            B3 = fmaxf(B3, p.z);
-        }
-        const float margin = a.margin[row0 + r];
-        const bool top1 = B1 - B2 > margin;
-        if (!top1) atomicAdd(a.near_ties + pair, 1ull);  // top-2 gap inside the error bound
-        if (top1 || B1 - B3 > margin) {
-            // certified: the reference winner lies in T1 (or T1 / T2)
-            s_t[r][0] = T1;
-            s_t[r][1] = top1 ? 0xFFFFFFFFu : T2;
-            s_go[r] = 1;
-        } else {
-            const uint32_t k = atomicAdd(a.rescan_count, 1u);
-            a.rescan[3 * k] = row0 + r;
-            a.rescan[3 * k + 1] = pair;
-            a.rescan[3 * k + 2] = qi0 + r;
-        }
-    }
-    __syncthreads();
-    const uint32_t warp = r >> 5, lane = r & 31;
-    const uint8_t* tm = a.tmap + pair * a.t_pair_bytes;
-    // two rows per warp at a time, one per 16-lane half, four targets per lane
-    const uint32_t half = lane >> 4, hl = lane & 15u;
-    for (uint32_t rb = warp; rb < nrows; rb += 2 * (kMergeThreads / 32)) {
-        const uint32_t row = rb + half * (kMergeThreads / 32);
-        const bool go = row < nrows && s_go[row];
-        unsigned long long key = ~0ull;
-        if (go) {
-            float q[kPackK];
-            load_query(a.qbuf, row0 + row, q);
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                const uint32_t st = s_t[row][c];
-                if (st == 0xFFFFFFFFu) continue;
-#pragma unroll
-                for (uint32_t h = 0; h < kSubTile; h += 16) {
-                    const uint32_t t = st * kSubTile + h + hl;
-                    if (t < a.nt) {
-                        const unsigned long long k = pack_key(packed_chain<kL2, DIM>(q, tm, t, a.dim), t);
-                        key = k < key ? k : key;
-                    }
-                }
-            }
-        }
-#pragma unroll
-        for (int o = 8; o > 0; o >>= 1) {  // within each 16-lane half
-            const unsigned long long other = __shfl_xor_sync(0xFFFFFFFFu, key, o);
-            key = other < key ? other : key;
-        }
-        if (go && hl == 0) {
-            const uint64_t o = (uint64_t)pair * a.out_stride + qi0 + row;
-            if (a.shard_keys) {
-                shard_emit(a.shard_keys, a.peers, o, (long long)(key ^ 0x8000000000000000ull));
-                continue;
-            }
-            a.out[o] = (uint32_t)(key & 0xFFFFFFFFull);
-            if (a.min_dist) {
-                float d = from_orderable((uint32_t)(key >> 32));
-                if (d == 0.0f) d = kL2 ? 0.0f : -0.0f;  // canonical sign of an exact zero
-                a.min_dist[o] = d;
-            }
-        }
-    }
-}
-
-// ---------------------------------------------------------------- K4' rescan
-// Reference FMA chain on binary16 values (packed layout), channels < dim only.
 // Reference FMA chain over channels < dim of binary16 values (packed layout).
 // DIM > 0: dim is the compile-time constant DIM (query fully in registers);
 // DIM == 0: runtime dim <= kPackK (all loops unrolled to kPackK, predicated).
@@ -755,6 +654,43 @@ __device__ __forceinline__ float packed_chain(const float (&q)[kPackK], const ui
     return kL2 ? acc : -acc;
 }
 
+// The same chain over an original fp32 row (kResolveFull), 16 B loads when
+// the row is a whole number of float4s.
+template <bool kL2, int DIM>
+__device__ __forceinline__ float f32_chain(const float (&q)[kPackK], const float* row, uint32_t dim) {
+    float acc = 0.0f;
+    if constexpr (DIM > 0 && DIM % 4 == 0) {
+#pragma unroll
+        for (int c0 = 0; c0 < DIM; c0 += 4) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(row + c0));
+            const float t[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if constexpr (kL2) {
+                    const float d = __fsub_rn(q[c0 + k], t[k]);
+                    acc = __fmaf_rn(d, d, acc);
+                } else {
+                    acc = __fmaf_rn(q[c0 + k], t[k], acc);
+                }
+            }
+        }
+    } else {
+#pragma unroll
+        for (uint32_t c = 0; c < kPackK; ++c) {
+            if (DIM > 0 ? c < (uint32_t)DIM : c < dim) {
+                const float t = __ldg(row + c);
+                if constexpr (kL2) {
+                    const float d = __fsub_rn(q[c], t);
+                    acc = __fmaf_rn(d, d, acc);
+                } else {
+                    acc = __fmaf_rn(q[c], t, acc);
+                }
+            }
+        }
+    }
+    return kL2 ? acc : -acc;
+}
+
 __device__ __forceinline__ void load_query(const uint8_t* qbuf, uint32_t grow, float (&q)[kPackK]) {
 #pragma unroll
     for (uint32_t c0 = 0; c0 < kPackK; c0 += 8) {
@@ -764,11 +700,204 @@ __device__ __forceinline__ void load_query(const uint8_t* qbuf, uint32_t grow, f
         for (int k = 0; k < 8; ++k) q[c0 + k] = __half2float(h[k]);
     }
 }
+__device__ __forceinline__ void load_query32(const float* row, uint32_t dim, float (&q)[kPackK]) {
+#pragma unroll
+    for (uint32_t c = 0; c < kPackK; ++c) q[c] = c < dim ? __ldg(row + c) : 0.0f;
+}
+
+// Query row in the resolve mode's arithmetic: the original fp32 row
+// (kResolveFull) or the gathered binary16 row.
+template <int MODE>
+__device__ __forceinline__ void mode_query(const uint8_t* qbuf, uint32_t grow, const ResolveSrc& rs,
+                                           const uint32_t* ids, uint32_t cap, uint32_t pair, uint32_t qi,
+                                           uint32_t dim, float (&q)[kPackK]) {
+    if constexpr (MODE == kResolveFull) {
+        const uint32_t id = ids ? ids[(uint64_t)pair * cap + qi] : qi;
+        load_query32(rs.q32 + pair * rs.q32_pair_stride + (uint64_t)id * dim, dim, q);
+    } else {
+        load_query(qbuf, grow, q);
+    }
+}
+
+// Exact reference distance of target t, and the value the reference compares
+// (hybrid: the distance cast to binary16, src/kernels.cpp:162-170; routing
+// guarantees no saturation on this path).
+template <bool kL2, int DIM, int MODE>
+__device__ __forceinline__ float mode_chain(const float (&q)[kPackK], const uint8_t* tm, const float* t32,
+                                            uint32_t t, uint32_t dim) {
+    if constexpr (MODE == kResolveFull) return f32_chain<kL2, DIM>(q, t32 + (uint64_t)t * dim, dim);
+    else return packed_chain<kL2, DIM>(q, tm, t, dim);
+}
+template <int MODE>
+__device__ __forceinline__ float mode_cmp(float d) {
+    if constexpr (MODE == kResolveHybrid) return half_round_nosat(d);
+    else return d;
+}
+
+// binary16 unit in the last place of |x| (normal binade, else the subnormal
+// step 2^-24): two values whose binary16 roundings coincide differ by less
+// than 2 ulp16 of either
+__device__ __forceinline__ float ulp16(float x) {
+    const int e = (int)((__float_as_uint(x) >> 23) & 0xFFu) - 127;
+    return ldexpf(1.0f, max(e - 10, -24));
+}
 
 __device__ __forceinline__ unsigned long long umin64(unsigned long long a, unsigned long long b) {
     return a < b ? a : b;
 }
 
+// One CTA per 64-row slice of a tile pair: phase 2 is a chain of dependent
+// L2/HBM loads per row, so the kernel is latency bound and wants many rows in
+// flight -- four slices per tile pair give each warp 8 rows instead of 32
+// (measured: 1.07 -> 0.74 ms per 128-pair step; 32-row slices: 0.84 ms).
+constexpr uint32_t kMergeRows = 64;
+constexpr uint32_t kMergeSlices = kQueryTilePair / kMergeRows;
+constexpr uint32_t kMergeThreads = 256;
+constexpr uint32_t kNoTile = 0xFFFFFFFFu;
+
+template <bool kL2, int DIM, int MODE>
+__global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs a) {
+    // phase 1 (thread per row): global top-4 of sub-tile maxima over the
+    //   target splits / column halves -> candidates T1, T2, T3 and the bounds
+    //   B2, B3, B4 on everything not yet resolved after 1, 2, 3 of them
+    // phase 2 (16 lanes per row, two rows per warp): resolve T1 with the exact
+    //   chain (four targets per lane, (cmp, index) key min), close the row if
+    //   the exact winner beats B2 by the margin, else resolve T2 against B3,
+    //   then T3 against B4; rows still open go to the full rescan
+    __shared__ uint32_t s_t[kMergeRows][3];
+    __shared__ float s_b[kMergeRows][3];
+    const uint32_t tp = blockIdx.x / kMergeSlices, slice = blockIdx.x % kMergeSlices;
+    if (tp >= a.hdr[1]) return;
+    const uint32_t splits = a.hdr[3];
+    const uint32_t pair = a.tp_pair[tp];
+    const uint32_t tp_rows = min(kQueryTilePair, a.n_active[pair] - a.tp_qi0[tp]);
+    if (slice * kMergeRows >= tp_rows) return;  // CTA-uniform
+    const uint32_t nrows = min(kMergeRows, tp_rows - slice * kMergeRows);
+    const uint32_t row0 = a.tp_row0[tp] + slice * kMergeRows;  // first gathered row of the slice
+    const uint32_t qi0 = a.tp_qi0[tp] + slice * kMergeRows;     // its query index within the pair
+    const uint32_t r = threadIdx.x;
+    if (r < nrows) {
+        float B[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        uint32_t T[3] = {kNoTile, kNoTile, kNoTile};
+        auto insert = [&](float v, uint32_t t) {
+            if (v > B[0]) {
+                B[3] = fmaxf(B[3], B[2]);
+                B[2] = B[1], T[2] = T[1];
+                B[1] = B[0], T[1] = T[0];
+                B[0] = v, T[0] = t;
+            } else if (v > B[1]) {
+                B[3] = fmaxf(B[3], B[2]);
+                B[2] = B[1], T[2] = T[1];
+                B[1] = v, T[1] = t;
+            } else if (v > B[2]) {
+                B[3] = fmaxf(B[3], B[2]);
+                B[2] = v, T[2] = t;
+            } else {
+                B[3] = fmaxf(B[3], v);
+            }
+        };
+        for (uint32_t s = 0; s < splits * kPartialSplit; ++s) {
+            const float4* pp =
+                a.partial + (((uint64_t)tp * splits * kPartialSplit + s) * kQueryTilePair + slice * kMergeRows + r) * 2;
+            const float4 p = pp[0];
+            const float4 p2 = pp[1];
+            insert(p.x, __float_as_uint(p2.x));
+            insert(p.y, __float_as_uint(p2.y));
+            insert(p.z, __float_as_uint(p2.z));
+            B[3] = fmaxf(B[3], p.w);
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            s_t[r][c] = T[c];
+            s_b[r][c] = B[c + 1];
+        }
+    }
+    __syncthreads();
+    const uint32_t warp = r >> 5, lane = r & 31;
+    const uint8_t* tm = a.tmap + pair * a.t_pair_bytes;
+    const float* t32 = MODE == kResolveFull ? a.rs.t32 + pair * a.rs.t32_pair_stride : nullptr;
+    const uint32_t half = lane >> 4, hl = lane & 15u;
+    for (uint32_t rb = warp; rb < nrows; rb += 2 * (kMergeThreads / 32)) {
+        const uint32_t row = rb + half * (kMergeThreads / 32);
+        const bool valid = row < nrows;
+        float q[kPackK];
+        float qq = 0.0f, M = 0.0f;
+        if (valid) {
+            mode_query<MODE>(a.qbuf, row0 + row, a.rs, a.ids, a.cap, pair, qi0 + row, a.dim, q);
+            M = a.margin[row0 + row];
+            if constexpr (kL2) {
+#pragma unroll
+                for (uint32_t c = 0; c < kPackK; ++c)
+                    if (DIM > 0 ? c < (uint32_t)DIM : c < a.dim) qq = __fmaf_rn(q[c], q[c], qq);
+            }
+        }
+        unsigned long long key = ~0ull;
+        float dmin = INFINITY;
+        bool done = !valid;
+#pragma unroll 1
+        for (int c = 0; c < 3; ++c) {
+            const uint32_t st = done ? kNoTile : s_t[row][c];
+            if (st != kNoTile) {
+#pragma unroll
+                for (uint32_t h = 0; h < kSubTile; h += 16) {
+                    const uint32_t t = st * kSubTile + h + hl;
+                    if (t < a.nt) {
+                        const float d = mode_chain<kL2, DIM, MODE>(q, tm, t32, t, a.dim);
+                        key = umin64(key, pack_key(mode_cmp<MODE>(d), t));
+                        dmin = fminf(dmin, d);
+                    }
+                }
+            }
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) {  // within each 16-lane half
+                key = umin64(key, __shfl_xor_sync(0xFFFFFFFFu, key, o));
+                dmin = fminf(dmin, __shfl_xor_sync(0xFFFFFFFFu, dmin, o));
+            }
+            if (!done) {
+                bool closed = true;  // no candidate left: every target resolved
+                if (st != kNoTile) {
+                    const float Bn = s_b[row][c];
+                    const float lb = kL2 ? qq - 2.0f * (Bn + M) : -(Bn + M);  // bound on every other distance
+                    const float dref = MODE == kResolveHybrid ? dmin + 2.0f * ulp16(fabsf(dmin)) : dmin;
+                    closed = dref < lb;
+                }
+                if (c == 0 && !closed && hl == 0) atomicAdd(a.near_ties + pair, 1ull);
+                if (closed) {
+                    done = true;
+                    if (hl == 0) {
+                        const uint64_t o = (uint64_t)pair * a.out_stride + qi0 + row;
+                        if (a.shard_keys) {
+                            shard_emit(a.shard_keys, a.peers, o, (long long)(key ^ 0x8000000000000000ull));
+                        } else {
+                            a.out[o] = (uint32_t)(key & 0xFFFFFFFFull);
+                            if (a.min_dist) {
+                                float d = from_orderable((uint32_t)(key >> 32));
+                                if (d == 0.0f)  // keys merge +-0: the winner's own zero (hybrid cast) or canonical
+                                    d = MODE == kResolveHybrid
+                                            ? mode_cmp<MODE>(mode_chain<kL2, DIM, MODE>(
+                                                  q, tm, t32, (uint32_t)(key & 0xFFFFFFFFull), a.dim))
+                                            : (kL2 ? 0.0f : -0.0f);
+                                a.min_dist[o] = d;
+                            }
+                        }
+                    }
+                }
+            }
+            if (!__any_sync(0xFFFFFFFFu, !done)) break;
+        }
+        if (!done && hl == 0) {
+            atomicAdd(a.near_ties + a.npairs + pair, 1ull);
+            const uint32_t k = atomicAdd(a.rescan_count, 1u);
+            a.rescan[3 * k] = row0 + row;
+            a.rescan[3 * k + 1] = pair;
+            a.rescan[3 * k + 2] = qi0 + row;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- K4' rescan
+// Rows with four sub-tiles inside the margin: the resolve mode's exact chain
+// over every target of the scanned range, lowest index on exact ties.
 struct RescanArgs {
     const uint32_t* rescan;
     const unsigned int* rescan_count;
@@ -780,25 +909,29 @@ struct RescanArgs {
     uint32_t chunk;                 // targets per work unit
     unsigned long long* keys;       // per rescan entry
     bool l2;
+    const uint32_t* ids;
+    uint32_t cap;
+    ResolveSrc rs;
 };
 
 constexpr int kRescanThreads = 256;
 
-template <bool kL2, int DIM>
+template <bool kL2, int DIM, int MODE>
 __global__ void __launch_bounds__(kRescanThreads) rescan_kernel(RescanArgs a) {
-    const uint32_t count = *a.rescan_count;
-    const uint32_t nchunks = (a.nt - a.t_begin + a.chunk - 1) / a.chunk;
+    const uint64_t count = *a.rescan_count;
+    const uint64_t nchunks = (a.nt - a.t_begin + a.chunk - 1) / a.chunk;
     __shared__ unsigned long long red[kRescanThreads / 32];
     float q[kPackK];
-    for (uint32_t unit = blockIdx.x; unit < count * nchunks; unit += gridDim.x) {
-        const uint32_t k = unit / nchunks, ch = unit % nchunks;
-        const uint32_t grow = a.rescan[3 * k], pair = a.rescan[3 * k + 1];
-        load_query(a.qbuf, grow, q);
+    for (uint64_t unit = blockIdx.x; unit < count * nchunks; unit += gridDim.x) {
+        const uint64_t k = unit / nchunks, ch = unit % nchunks;
+        const uint32_t grow = a.rescan[3 * k], pair = a.rescan[3 * k + 1], qi = a.rescan[3 * k + 2];
+        mode_query<MODE>(a.qbuf, grow, a.rs, a.ids, a.cap, pair, qi, a.dim, q);
         const uint8_t* tm = a.tmap + pair * a.t_pair_bytes;
-        const uint32_t t0 = a.t_begin + ch * a.chunk, t1 = min(a.nt, t0 + a.chunk);
+        const float* t32 = MODE == kResolveFull ? a.rs.t32 + pair * a.rs.t32_pair_stride : nullptr;
+        const uint32_t t0 = a.t_begin + (uint32_t)ch * a.chunk, t1 = min(a.nt, t0 + a.chunk);
         unsigned long long key = ~0ull;
         for (uint32_t t = t0 + threadIdx.x; t < t1; t += kRescanThreads)
-            key = umin64(key, (unsigned long long)pack_key(packed_chain<kL2, DIM>(q, tm, t, a.dim), t));
+            key = umin64(key, pack_key(mode_cmp<MODE>(mode_chain<kL2, DIM, MODE>(q, tm, t32, t, a.dim)), t));
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) key = umin64(key, __shfl_xor_sync(0xFFFFFFFFu, key, o));
         if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = key;
@@ -812,25 +945,36 @@ __global__ void __launch_bounds__(kRescanThreads) rescan_kernel(RescanArgs a) {
     }
 }
 
-__global__ void rescan_finish_kernel(const uint32_t* rescan, const unsigned int* count,
-                                     unsigned long long* keys, uint32_t* out, float* min_dist,
-                                     uint32_t out_stride, bool dot, long long* shard_keys, ShardPeers peers) {
-    const uint32_t n = *count;
+template <bool kL2, int DIM, int MODE>
+__global__ void rescan_finish_kernel(RescanArgs a, uint32_t* out, float* min_dist, uint32_t out_stride,
+                                     long long* shard_keys, ShardPeers peers) {
+    const uint32_t n = *a.rescan_count;
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-        const uint64_t o = (uint64_t)rescan[3 * k + 1] * out_stride + rescan[3 * k + 2];
-        const unsigned long long key = keys[k];
+        const uint32_t pair = a.rescan[3 * k + 1], qi = a.rescan[3 * k + 2];
+        const uint64_t o = (uint64_t)pair * out_stride + qi;
+        const unsigned long long key = a.keys[k];
         if (shard_keys) {
             shard_emit(shard_keys, peers, o, (long long)(key ^ 0x8000000000000000ull));
-            keys[k] = ~0ull;
+            a.keys[k] = ~0ull;
             continue;
         }
-        out[o] = (uint32_t)(key & 0xFFFFFFFFull);
+        const uint32_t idx = (uint32_t)(key & 0xFFFFFFFFull);
+        out[o] = idx;
         if (min_dist) {
             float d = from_orderable((uint32_t)(key >> 32));
-            if (d == 0.0f) d = dot ? -0.0f : 0.0f;  // canonical sign of an exact zero
+            if (d == 0.0f) {
+                if constexpr (MODE == kResolveHybrid) {  // the winner's own signed zero
+                    float q[kPackK];
+                    mode_query<MODE>(a.qbuf, a.rescan[3 * k], a.rs, a.ids, a.cap, pair, qi, a.dim, q);
+                    d = mode_cmp<MODE>(mode_chain<kL2, DIM, MODE>(q, a.tmap + pair * a.t_pair_bytes, nullptr, idx,
+                                                                    a.dim));
+                } else {
+                    d = kL2 ? 0.0f : -0.0f;  // canonical sign of an exact zero
+                }
+            }
             min_dist[o] = d;
         }
-        keys[k] = ~0ull;
+        a.keys[k] = ~0ull;
     }
 }
 
@@ -952,14 +1096,41 @@ uint32_t ceil_div_u(uint32_t a, uint32_t b) { return (a + b - 1) / b; }
         if (_st != FNL_OK) return _st; \
     } while (0)
 
-bool attr_done = false;
+// cudaFuncSetAttribute applies to the current device only: one flag per
+// device, set under a lock (threads may drive different GPUs)
+std::mutex attr_mu;
+bool attr_done[64] = {};
 
 int ensure_attrs() {
-    if (attr_done) return FNL_OK;
+    int dev = 0;
+    FNL_CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(attr_mu);
+    if (dev >= 0 && dev < 64 && attr_done[dev]) return FNL_OK;
     FNL_CUDA_TRY(cudaFuncSetAttribute(tc_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal));
     FNL_CUDA_TRY(cudaFuncSetAttribute(selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal));
-    attr_done = true;
+    if (dev >= 0 && dev < 64) attr_done[dev] = true;
     return FNL_OK;
+}
+
+template <bool kL2, int DIM>
+void launch_merge_mode(int mode, uint32_t grid, const MergeArgs& m, cudaStream_t s) {
+    if (mode == kResolveFull) merge_kernel<kL2, DIM, kResolveFull><<<grid, kMergeThreads, 0, s>>>(m);
+    else if (mode == kResolveHybrid) merge_kernel<kL2, DIM, kResolveHybrid><<<grid, kMergeThreads, 0, s>>>(m);
+    else merge_kernel<kL2, DIM, kResolveRounded><<<grid, kMergeThreads, 0, s>>>(m);
+}
+template <bool kL2, int DIM, int MODE>
+void launch_rescan_t(uint32_t grid, const RescanArgs& r, uint32_t* out, float* min_dist, uint32_t out_stride,
+                     long long* shard_keys, const ShardPeers& pp, cudaStream_t s) {
+    rescan_kernel<kL2, DIM, MODE><<<grid, kRescanThreads, 0, s>>>(r);
+    rescan_finish_kernel<kL2, DIM, MODE><<<4, 256, 0, s>>>(r, out, min_dist, out_stride, shard_keys, pp);
+}
+template <bool kL2, int DIM>
+void launch_rescan_mode(int mode, uint32_t grid, const RescanArgs& r, uint32_t* out, float* min_dist,
+                        uint32_t out_stride, long long* shard_keys, const ShardPeers& pp, cudaStream_t s) {
+    if (mode == kResolveFull) launch_rescan_t<kL2, DIM, kResolveFull>(grid, r, out, min_dist, out_stride, shard_keys, pp, s);
+    else if (mode == kResolveHybrid)
+        launch_rescan_t<kL2, DIM, kResolveHybrid>(grid, r, out, min_dist, out_stride, shard_keys, pp, s);
+    else launch_rescan_t<kL2, DIM, kResolveRounded>(grid, r, out, min_dist, out_stride, shard_keys, pp, s);
 }
 
 }  // namespace
@@ -1122,9 +1293,13 @@ int tensor_pack(fnl_context* ctx, const char* tag, const float* d_src, uint32_t 
 int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const uint32_t* ids, uint32_t cap,
                    const uint32_t* d_active, const uint8_t* d_done, const PackedMaps& T, uint32_t dim, bool l2,
                    uint32_t* out, uint32_t out_stride, float* min_dist, unsigned long long* d_near_ties,
-                   uint32_t tile_begin, uint32_t tile_end, long long* shard_keys, const ShardPeers* peers) {
+                   uint32_t tile_begin, uint32_t tile_end, long long* shard_keys, const ShardPeers* peers,
+                   const ResolveSrc* resolve) {
     const ShardPeers no_peers{};
     const ShardPeers& pp = peers ? *peers : no_peers;
+    const ResolveSrc rs = resolve ? *resolve : ResolveSrc{};
+    if (rs.mode == kResolveFull && (!rs.q32 || !rs.t32))
+        return fail(FNL_EINVAL, "tensor_nn_pass: full-precision resolution needs the fp32 maps");
     TRY(ensure_attrs());
     cudaStream_t s = ctx_stream(ctx);
     const uint32_t nt = T.rows;
@@ -1181,7 +1356,7 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     // ---- K2 gather
     {
         GatherArgs g{Q.data, Q.pair_bytes, ids, cap, d_active, d_slot_pair, d_slot_base, qbuf, margin,
-                     T.max_norm, dim, l2, d_hdr};
+                     T.max_norm, dim, l2, d_hdr, rs.mode};
         dim3 grid(ceil_div_u(tp_per_pair * kQueryTilePair * 4, 256), npairs);
         ProfScope prof(ctx, FNL_KCLASS_GATHER);
         gather_kernel<<<grid, 256, 0, s>>>(g);
@@ -1206,32 +1381,32 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     // ---- K3b merge + certification
     {
         MergeArgs m{partial, d_tp_pair, d_tp_row0, d_tp_qi0, d_hdr, d_active, margin, qbuf, T.data,
-                    T.pair_bytes, nt, dim, out, min_dist, out_stride, rescan, rcount, d_near_ties, shard_keys, pp};
+                    T.pair_bytes, nt, dim, out, min_dist, out_stride, rescan, rcount, d_near_ties, npairs, shard_keys,
+                    pp, ids, cap, rs};
         ProfScope prof(ctx, FNL_KCLASS_MERGE);
+        const uint32_t grid = tp_max * kMergeSlices;
         if (dim == 24) {
-            if (l2) merge_kernel<true, 24><<<tp_max * kMergeSlices, kMergeThreads, 0, s>>>(m);
-            else merge_kernel<false, 24><<<tp_max * kMergeSlices, kMergeThreads, 0, s>>>(m);
+            if (l2) launch_merge_mode<true, 24>(rs.mode, grid, m, s);
+            else launch_merge_mode<false, 24>(rs.mode, grid, m, s);
         } else {
-            if (l2) merge_kernel<true, 0><<<tp_max * kMergeSlices, kMergeThreads, 0, s>>>(m);
-            else merge_kernel<false, 0><<<tp_max * kMergeSlices, kMergeThreads, 0, s>>>(m);
+            if (l2) launch_merge_mode<true, 0>(rs.mode, grid, m, s);
+            else launch_merge_mode<false, 0>(rs.mode, grid, m, s);
         }
         FNL_CUDA_TRY(cudaGetLastError());
     }
-    // ---- K4' exact re-decision of near ties (grid-stride over a device count)
+    // ---- K4' exact re-decision of rows left open (grid-stride over a device count)
     {
         RescanArgs r{rescan, rcount, qbuf, T.data, T.pair_bytes, tile_begin * kBTileRows,
-                     std::min(nt, tile_end * kBTileRows), dim, 4096u, keys, l2};
+                     std::min(nt, tile_end * kBTileRows), dim, 4096u, keys, l2, ids, cap, rs};
         const uint32_t grid = 2 * (uint32_t)ctx_sm_count(ctx);
         ProfScope prof(ctx, FNL_KCLASS_RESCAN);
         if (dim == 24) {
-            if (l2) rescan_kernel<true, 24><<<grid, kRescanThreads, 0, s>>>(r);
-            else rescan_kernel<false, 24><<<grid, kRescanThreads, 0, s>>>(r);
+            if (l2) launch_rescan_mode<true, 24>(rs.mode, grid, r, out, min_dist, out_stride, shard_keys, pp, s);
+            else launch_rescan_mode<false, 24>(rs.mode, grid, r, out, min_dist, out_stride, shard_keys, pp, s);
         } else {
-            if (l2) rescan_kernel<true, 0><<<grid, kRescanThreads, 0, s>>>(r);
-            else rescan_kernel<false, 0><<<grid, kRescanThreads, 0, s>>>(r);
+            if (l2) launch_rescan_mode<true, 0>(rs.mode, grid, r, out, min_dist, out_stride, shard_keys, pp, s);
+            else launch_rescan_mode<false, 0>(rs.mode, grid, r, out, min_dist, out_stride, shard_keys, pp, s);
         }
-        FNL_CUDA_TRY(cudaGetLastError());
-        rescan_finish_kernel<<<4, 256, 0, s>>>(rescan, rcount, keys, out, min_dist, out_stride, !l2, shard_keys, pp);
         FNL_CUDA_TRY(cudaGetLastError());
     }
     if (debug_mode_trace_dump(ctx, s)) {}
@@ -1269,8 +1444,31 @@ int tensor_shard_reset(fnl_context* ctx, long long* keys, uint64_t n) {
     return FNL_OK;
 }
 
+bool tensor_route_ok(int mode, bool l2, uint32_t dim, float qmax_norm, float tmax_norm,
+                     unsigned long long sat, unsigned long long bad) {
+    if (dim == 0 || dim + (l2 ? 2u : 0u) > kPackK) return false;
+    if (bad != ~0ull) return false;  // non-finite input: the exact kernels decide it
+    const double q = (double)qmax_norm * 1.001, t = (double)tmax_norm * 1.001;
+    // -|t|^2/2 (both maps serve as targets) must stay a finite binary16 hi term
+    if (l2 && std::max(q, t) * std::max(q, t) / 2.0 >= 65504.0) return false;
+    if (mode == kResolveRounded) return true;  // its contract is the binary16 rows, saturated or not
+    if (sat != 0) return false;                // saturated inputs: relative rounding bound does not hold
+    if (mode == kResolveHybrid) {
+        // every distance must round to binary16 without saturating (so the
+        // reference's distance-saturation count is 0): |d| <= |q||t| (dot),
+        // (|q| + |t|)^2 (l2), with the chain's own rounding
+        const double dmax = l2 ? (q + t) * (q + t) : q * t;
+        if (dmax * 1.01 >= 65504.0) return false;
+    }
+    return true;
+}
+
 int tensor_nn_dense(fnl_context* ctx, const float* d_q, uint32_t nq, const float* d_t, uint32_t nt,
-                    uint32_t dim, bool l2, uint32_t* d_nearest, float* d_min_dist) {
+                    uint32_t dim, bool l2, uint32_t* d_nearest, float* d_min_dist, int mode, bool* routed) {
+    if (routed) {
+        *routed = false;
+        if (dim == 0 || dim + (l2 ? 2u : 0u) > kPackK) return FNL_OK;
+    }
     unsigned long long* scratch;
     TRY(ws_arr(ctx, "tc.dense.scratch", 4, &scratch));
     cudaStream_t s = ctx_stream(ctx);
@@ -1279,13 +1477,33 @@ int tensor_nn_dense(fnl_context* ctx, const float* d_q, uint32_t nq, const float
     PackedMaps Q, T;
     TRY(tensor_pack(ctx, "tc.dense.q", d_q, 1, nq, dim, l2, scratch, scratch + 2, &Q));
     TRY(tensor_pack(ctx, "tc.dense.t", d_t, 1, nt, dim, l2, scratch + 1, scratch + 3, &T));
+    if (routed) {
+        // one host round trip: the pack's norms / saturations / finiteness
+        // decide whether this call may take the tensor route
+        unsigned long long h[4];
+        float n[2];
+        FNL_CUDA_TRY(cudaMemcpyAsync(h, scratch, 32, cudaMemcpyDeviceToHost, s));
+        FNL_CUDA_TRY(cudaMemcpyAsync(&n[0], Q.max_norm, 4, cudaMemcpyDeviceToHost, s));
+        FNL_CUDA_TRY(cudaMemcpyAsync(&n[1], T.max_norm, 4, cudaMemcpyDeviceToHost, s));
+        FNL_CUDA_TRY(cudaStreamSynchronize(s));
+        const unsigned long long bad = std::min(h[0], h[1]);
+        if (!tensor_route_ok(mode, l2, dim, n[0], n[1], h[2] + h[3], bad)) return FNL_OK;
+        *routed = true;
+    }
     unsigned long long* ties;
-    TRY(ws_arr(ctx, "tc.dense.ties", 1, &ties));
-    FNL_CUDA_TRY(cudaMemsetAsync(ties, 0, 8, s));
+    TRY(ws_arr(ctx, "tc.dense.ties", 2, &ties));
+    FNL_CUDA_TRY(cudaMemsetAsync(ties, 0, 16, s));
     uint32_t* d_nq;
     TRY(ws_arr(ctx, "tc.dense.nq", 1, &d_nq));
     FNL_CUDA_TRY(cudaMemcpyAsync(d_nq, &nq, 4, cudaMemcpyHostToDevice, s));  // pageable: staged before return
-    return tensor_nn_pass(ctx, 1, Q, nullptr, nq, d_nq, nullptr, T, dim, l2, d_nearest, nq, d_min_dist, ties);
+    ResolveSrc rs;
+    rs.mode = mode;
+    rs.q32 = d_q;
+    rs.q32_pair_stride = (uint64_t)nq * dim;
+    rs.t32 = d_t;
+    rs.t32_pair_stride = (uint64_t)nt * dim;
+    return tensor_nn_pass(ctx, 1, Q, nullptr, nq, d_nq, nullptr, T, dim, l2, d_nearest, nq, d_min_dist, ties, 0, 0,
+                          nullptr, nullptr, &rs);
 }
 
 int tensor_selftest_scores(fnl_context* ctx, const float* d_q, const float* d_t, uint32_t dim, bool l2,

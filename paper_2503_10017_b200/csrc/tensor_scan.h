@@ -1,13 +1,15 @@
 // tensor_scan.h -- K1 pack, K2 gather, K3 tcgen05 HybridCast score + certified
 // argmax, K3b merge, K4' exact re-decision of near ties (tensor_scan.cu).
 //
-// Numeric contract of the tensor backend: descriptors are cast to binary16 once
-// (RNE, +-65504 saturation), scored on the 5th-gen tensor cores with fp32
-// accumulation (Alg. 3, HybridCast), and every row whose tensor-core
-// top-2 gap is not provably larger than the accumulated rounding error is
-// re-decided by the reference FMA chain on the same binary16 values.  The
-// nearest indices are therefore identical to the reference `single` backend run
-// on binary16-rounded maps (src/nn.cpp:134-164 on to_half_round(D)).
+// Numeric contract: descriptors are cast to binary16 once (RNE, +-65504
+// saturation) and scored on the 5th-gen tensor cores with fp32 accumulation
+// (Alg. 3, HybridCast).  The tensor-core scores only ever NOMINATE
+// candidates: the winner is decided by the reference FMA chain in the
+// arithmetic of the requested backend (ResolveMode), and a row is closed only
+// when every target outside the resolved 64-target sub-tiles provably loses
+// (its tensor-core score plus a rigorous error bound stays below the exact
+// winner).  So the nearest indices and min_dist are bit-identical to the
+// reference backend the mode names.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -49,7 +51,9 @@ int tensor_pack(fnl_context* ctx, const char* tag, const float* d_src, uint32_t 
 // are DEVICE arrays: the work lists are planned on the device, so consecutive
 // passes are enqueued without a host round trip.  Winner indices land in
 // out[p*out_stride + i]; if min_dist is non-null the exact reference distance of
-// the winner is written beside it.  d_near_ties[p] counts re-decided rows.
+// the winner is written beside it.  d_near_ties[p] counts rows the first
+// candidate sub-tile did not settle, d_near_ties[npairs + p] rows that needed
+// the full rescan (2 * npairs entries).
 //
 // Target sharding (config C5): only target tiles [tile_begin, tile_end) of T
 // (kTargetTileRows = 256 targets per tile; tile_end = 0 means all) are scanned, and with
@@ -64,6 +68,35 @@ int tensor_pack(fnl_context* ctx, const char* tag, const float* d_src, uint32_t 
 // atomicMin from the merge / rescan epilogues themselves, so the "all-reduce"
 // is fused into the kernels that produce the keys.
 constexpr int kMaxShardPeers = 8;
+
+// The arithmetic a pass's winner is decided in (the reference backend it is
+// bit-identical to):
+enum ResolveMode : int {
+    // tensor backend (Alg. 3): reference FMA chain on the binary16-rounded
+    // rows, fp32 compare == ref `single` on to_half_round(D)
+    kResolveRounded = 0,
+    // ref `hybrid` / HybridCast (src/kernels.cpp:117-170): chain on the
+    // binary16 rows, each distance cast to binary16, lowest index on ties
+    kResolveHybrid = 1,
+    // ref `single` / `double` / `bruteforce`, full precision
+    // (src/kernels.cpp:31-43): chain on the ORIGINAL fp32 rows
+    kResolveFull = 2,
+};
+// Where kResolveFull reads the original fp32 rows: query map rows (indexed by
+// the pass's query ids) and target map rows, npairs stacked maps each.
+struct ResolveSrc {
+    int mode = kResolveRounded;
+    const float* q32 = nullptr;
+    uint64_t q32_pair_stride = 0;  // floats
+    const float* t32 = nullptr;
+    uint64_t t32_pair_stride = 0;
+};
+// Host-side eligibility of the tensor route for one map pair (max row norm of
+// the binary16 rows, binary16 saturations, first non-finite index): the packed
+// l2 norm term -|t|^2/2 must stay inside binary16, no input may saturate
+// (kResolveFull / kResolveHybrid), and hybrid distances must not saturate.
+bool tensor_route_ok(int mode, bool l2, uint32_t dim, float qmax_norm, float tmax_norm,
+                     unsigned long long sat, unsigned long long bad);
 struct ShardPeers {
     long long* keys[kMaxShardPeers];
     uint32_t n;
@@ -73,7 +106,8 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
                    uint32_t cap, const uint32_t* d_active, const uint8_t* d_done,
                    const PackedMaps& T, uint32_t dim, bool l2, uint32_t* out, uint32_t out_stride,
                    float* min_dist, unsigned long long* d_near_ties, uint32_t tile_begin = 0,
-                   uint32_t tile_end = 0, long long* shard_keys = nullptr, const ShardPeers* peers = nullptr);
+                   uint32_t tile_end = 0, long long* shard_keys = nullptr, const ShardPeers* peers = nullptr,
+                   const ResolveSrc* resolve = nullptr);
 
 // shard keys -> nearest indices for the active queries of every pair
 int tensor_shard_finalize(fnl_context* ctx, uint32_t npairs, const long long* keys, uint32_t stride,
@@ -89,9 +123,14 @@ int tensor_shard_barrier(fnl_context* ctx, unsigned int* const* flags, uint32_t 
 constexpr long long kShardKeyNone = 0x7FFFFFFFFFFFFFFFll;
 constexpr uint32_t kTargetTileRows = 256;  // targets per K3 B tile (shard granularity)
 
-// Dense convenience (fnl_nn_query backend TENSOR): all rows of d_q against d_t.
+// Dense convenience (fnl_nn_query / mutual NN): all rows of d_q against d_t,
+// resolved in the arithmetic of `mode` (ResolveSrc::mode; the fp32 originals
+// are d_q / d_t themselves).  With `routed` non-null the pack's norms and
+// saturation counts are read back first and the pass runs only if
+// tensor_route_ok holds (*routed says whether it did).
 int tensor_nn_dense(fnl_context* ctx, const float* d_q, uint32_t nq, const float* d_t, uint32_t nt,
-                    uint32_t dim, bool l2, uint32_t* d_nearest, float* d_min_dist);
+                    uint32_t dim, bool l2, uint32_t* d_nearest, float* d_min_dist, int mode = 0,
+                    bool* routed = nullptr);
 
 // Self-test: raw tensor-core scores of a packed query tile pair (256 rows)
 // against one packed target tile (128 rows) -> out[256][128] fp32.

@@ -25,7 +25,8 @@ class RunStats(ctypes.Structure):
                 ("half_saturation_events", ctypes.c_uint64), ("near_tie_rows", ctypes.c_uint64),
                 ("query_rows", ctypes.c_uint64), ("subsample_us", ctypes.c_double),
                 ("forward_nn_us", ctypes.c_double), ("reverse_nn_us", ctypes.c_double),
-                ("harvest_us", ctypes.c_double)]
+                ("harvest_us", ctypes.c_double), ("rescan_rows", ctypes.c_uint64),
+                ("tensor_route", ctypes.c_uint32)]
 
 
 @pytest.fixture(scope="module")

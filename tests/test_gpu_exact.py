@@ -1,10 +1,14 @@
-"""GPU parity of the exact (CUDA-core, bit-faithful) backends against the
-unmodified reference compiled from /root/reference (oracle/_ref/_fastnn_ref).
+"""GPU parity of the reference backends against the unmodified reference
+compiled from /root/reference (oracle/_ref/_fastnn_ref).
 
 Bar: bit-exact nearest indices AND min_dist values, identical fetch counters,
 saturation counts, MatchSets (order included) and RunReports except the four
 *_us timing fields -- the reference's own equivalence contract
 (tests/acceptance.cpp:47-118, tests/test_reciprocal.cpp:167-178).
+
+Every test runs twice: on the default route (tcgen05 scores + certified
+resolution in the backend's arithmetic, where the inputs allow it) and with
+FNL_EXACT_KERNEL=cuda_core (the CUDA-core exact scan K4 everywhere).
 """
 import json
 import os
@@ -15,6 +19,15 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 TIMING = ("subsample_us", "forward_nn_us", "reverse_nn_us", "harvest_us")
+
+
+@pytest.fixture(autouse=True, params=["tensor_route", "cuda_core"])
+def exact_kernel(request, monkeypatch):
+    if request.param == "cuda_core":
+        monkeypatch.setenv("FNL_EXACT_KERNEL", "cuda_core")
+    else:
+        monkeypatch.delenv("FNL_EXACT_KERNEL", raising=False)
+    return request.param
 
 
 def same_f32(a, b):

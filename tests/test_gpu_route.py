@@ -1,0 +1,176 @@
+"""The tensor route of the reference backends (tcgen05 scores nominate
+64-target sub-tiles; the winner is decided by the reference chain in the
+backend's own arithmetic -- fp32 rows for single/double/bruteforce, binary16
+rows plus the binary16 distance cast for hybrid).
+
+Bar: bit-identical to the unmodified reference compiled from /root/reference
+(nearest, min_dist, counters, ordered MatchSets, RunReports minus timings),
+including inputs built to defeat the certification (exact ties spread over
+many sub-tiles, binary16 cast-out ties, subnormal and near-limit magnitudes)
+and the inputs the route must refuse (saturating values, l2 norms whose
+-|t|^2/2 term leaves binary16), where the CUDA-core scan takes over.
+"""
+import json
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TIMING = ("subsample_us", "forward_nn_us", "reverse_nn_us", "harvest_us")
+
+
+def same_f32(a, b):
+    return np.array_equal(np.asarray(a, np.float32).view(np.uint32), np.asarray(b, np.float32).view(np.uint32))
+
+
+def strip(report_json):
+    r = json.loads(report_json)
+    for k in TIMING:
+        r.pop(k)
+    return r
+
+
+def nn_all(fnl, ref, A, B, metric, bs=4096):
+    for name, kw in [("nn_single_loop", dict(block_size=bs, precision="full")),
+                     ("nn_single_loop", dict(block_size=bs, precision="hybrid")),
+                     ("nn_double_loop", dict(block_size=bs, precision="full")),
+                     ("nn_hybridcast", dict(block_size=bs)),
+                     ("nn_bruteforce", dict())]:
+        ours = getattr(fnl, name)(A, B, metric=metric, **kw)
+        theirs = getattr(ref, name)(A, B, metric=metric, **kw)
+        assert np.array_equal(ours["nearest"], theirs["nearest"]), (name, kw)
+        assert same_f32(ours["min_dist"], theirs["min_dist"]), (name, kw)
+        for k in ("a_block_fetches", "b_block_fetches", "half_saturation_events"):
+            assert ours[k] == theirs[k], (name, kw, k)
+
+
+def route_of(fnl, D1, D2, backend, metric, precision="full"):
+    _, _, stats = fnl.reciprocal_match_batch(D1[None], D2[None], backend=backend, metric=metric,
+                                             precision=precision)
+    return stats[0]
+
+
+@pytest.mark.parametrize("metric", ["l2", "dot"])
+def test_route_taken_on_descriptor_maps(fnl, ref, metric):
+    D1 = ref.gen_random(48, 64, 24, 11)
+    D2 = ref.gen_random(48, 64, 24, 12)
+    for backend, precision in [("single", "full"), ("single", "hybrid"), ("hybrid", "full"),
+                               ("double", "full"), ("bruteforce", "full"), ("tensor", "full")]:
+        st = route_of(fnl, D1, D2, backend, metric, precision)
+        assert st["tensor_route"] == 1, (backend, precision)
+
+
+@pytest.mark.parametrize("metric", ["l2", "dot"])
+def test_quantised_ties_across_subtiles(fnl, ref, metric):
+    # descriptors on a coarse grid: many targets share the exact best
+    # distance, spread over many 64-target sub-tiles, so rows go past the
+    # first candidate and into the full rescan; the lowest index must win
+    rng = np.random.default_rng(3)
+    for levels, shape in [(3, (40, 50, 24)), (5, (32, 64, 24)), (2, (20, 30, 16))]:
+        A = (rng.integers(-levels, levels + 1, shape) / levels).astype(np.float32)
+        B = (rng.integers(-levels, levels + 1, (shape[0] + 3, shape[1], shape[2])) / levels).astype(np.float32)
+        nn_all(fnl, ref, A, B, metric)
+        for backend in ("single", "hybrid"):
+            m1, r1 = fnl.reciprocal_match(A, B, backend=backend, metric=metric, stride=4)
+            m2, r2 = ref.reciprocal_match(A, B, backend=backend, metric=metric, stride=4)
+            assert np.array_equal(m1, m2) and strip(r1) == strip(r2), (levels, backend)
+    st = route_of(fnl, A, B[:A.shape[0]].copy(), "single", metric)
+    assert st["tensor_route"] == 1 and st["near_tie_rows"] > 0
+
+
+@pytest.mark.parametrize("metric", ["l2", "dot"])
+def test_duplicated_targets(fnl, ref, metric):
+    # every target appears 5 times, in different 64-target sub-tiles: the
+    # three candidate sub-tiles cannot settle it, so the rows are rescanned
+    # and the lowest of the five indices must win
+    base = ref.gen_random(1, 700, 24, 77).reshape(700, 24)
+    B = np.concatenate([base] * 5).reshape(50, 70, 24)
+    A = ref.gen_random(50, 70, 24, 78)
+    nn_all(fnl, ref, A, B, metric)
+    for backend in ("single", "hybrid", "tensor"):
+        st = route_of(fnl, A, B, backend, metric)
+        assert st["tensor_route"] == 1 and st["rescan_rows"] > 0, backend
+    m1, r1 = fnl.reciprocal_match(A, B, backend="single", metric=metric, stride=5)
+    m2, r2 = ref.reciprocal_match(A, B, backend="single", metric=metric, stride=5)
+    assert np.array_equal(m1, m2) and strip(r1) == strip(r2)
+
+
+@pytest.mark.parametrize("metric", ["l2", "dot"])
+@pytest.mark.parametrize("scale", [1e-6, 3e-3, 1.0, 40.0])
+def test_magnitudes(fnl, ref, metric, scale):
+    # binary16 subnormal inputs (1e-6), small, unit and large values: the
+    # input-rounding bound of full precision changes regime
+    A = (ref.gen_random(33, 41, 24, 5, normalize=False) * scale).astype(np.float32)
+    B = (ref.gen_random(37, 29, 24, 6, normalize=False) * scale).astype(np.float32)
+    nn_all(fnl, ref, A, B, metric)
+
+
+def test_hybrid_castout_ties(fnl, ref):
+    # distances clustered inside one binary16 ulp: the reference's fp16
+    # cast-out makes them ties decided by index, far beyond any fp32 gap
+    rng = np.random.default_rng(9)
+    q = rng.normal(size=24).astype(np.float32)
+    q /= np.linalg.norm(q)
+    T = (q[None, :] + rng.normal(scale=2e-3, size=(4096, 24))).astype(np.float32)
+    A = np.tile(q, (1, 8, 1)).reshape(1, 8, 24) + rng.normal(scale=1e-4, size=(1, 8, 24)).astype(np.float32)
+    A = A.astype(np.float32)
+    for metric in ("dot", "l2"):
+        nn_all(fnl, ref, A, T.reshape(64, 64, 24), metric)
+
+
+def test_route_refused_and_k4_takes_over(fnl, ref):
+    rng = np.random.default_rng(4)
+    A = ref.gen_random(20, 20, 24, 1)
+    B = ref.gen_random(20, 20, 24, 2)
+    # binary16 saturation (|x| >= 65520) in an input: no full / hybrid route
+    Bs = B.copy()
+    Bs[3, 4, 5] = 70000.0
+    for backend in ("single", "hybrid"):
+        assert route_of(fnl, A, Bs, backend, "dot")["tensor_route"] == 0
+    nn_all(fnl, ref, A, Bs, "dot")
+    # hybrid distances that would saturate binary16 (|q||t| ~ 1e5)
+    Ab, Bb = (A * 400).astype(np.float32), (B * 400).astype(np.float32)
+    assert route_of(fnl, Ab, Bb, "hybrid", "dot")["tensor_route"] == 0
+    assert route_of(fnl, Ab, Bb, "single", "dot")["tensor_route"] == 1
+    nn_all(fnl, ref, Ab, Bb, "dot")
+    # l2 with |t|^2/2 beyond binary16 (the packed norm term would
+    # overflow to inf and the scores to NaN): every backend refuses the route
+    Al = (ref.gen_random(20, 20, 24, 3, normalize=False) * 200).astype(np.float32)
+    Bl = (ref.gen_random(20, 20, 24, 4, normalize=False) * 200).astype(np.float32)
+    for backend in ("single", "tensor"):
+        assert route_of(fnl, Al, Bl, backend, "l2")["tensor_route"] == 0
+    nn_all(fnl, ref, Al, Bl, "l2")
+    # the tensor backend keeps its contract (ref single on binary16-rounded
+    # maps) on the CUDA-core fallback too
+    r16 = np.vectorize(ref.to_half_round, otypes=[np.float32])
+    Ar, Br = r16(Al), r16(Bl)
+    m1, _ = fnl.reciprocal_match(Al, Bl, backend="tensor", metric="l2", stride=3)
+    m2, _ = ref.reciprocal_match(Ar, Br, backend="single", metric="l2", stride=3)
+    assert np.array_equal(m1, m2)
+    ours = fnl.nn_tensor(Al, Bl, metric="l2")
+    theirs = ref.nn_single_loop(Ar, Br, metric="l2")
+    assert np.array_equal(ours["nearest"], theirs["nearest"])
+
+
+@pytest.mark.parametrize("metric", ["l2", "dot"])
+def test_mutual_nn_tensor_route(fnl, ref, metric):
+    D1 = ref.gen_random(40, 30, 24, 50)
+    D2 = ref.gen_random(30, 44, 24, 51)
+    assert np.array_equal(fnl.mutual_nn_exact(D1, D2, metric), ref.mutual_nn_exact(D1, D2, metric))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("backend", ["single", "hybrid"])
+@pytest.mark.parametrize("metric", ["dot", "l2"])
+def test_c2_tensor_route_identical(fnl, ref, backend, metric):
+    """C2 512x384 d=24 stride 8 (seeds 606/607 and the matched pair), routed."""
+    import os
+    threads = os.cpu_count() or 1
+    p = ref.gen_matched_pair(512, 384, 24, 7, 0.05)
+    for D1, D2 in [(ref.gen_random(512, 384, 24, 606), ref.gen_random(512, 384, 24, 607)), (p["d1"], p["d2"])]:
+        m1, r1 = fnl.reciprocal_match(D1, D2, backend=backend, metric=metric, block_size=384)
+        m2, r2 = ref.reciprocal_match(D1, D2, backend=backend, metric=metric, block_size=384, threads=threads)
+        assert np.array_equal(m1, m2)
+        assert strip(r1) == strip(r2)
+    assert route_of(fnl, D1, D2, backend, metric)["tensor_route"] == 1
