@@ -23,7 +23,7 @@ NVFLAGS := $(ARCH) -std=c++17 -O3 -lineinfo --fmad=false -Xcompiler -fPIC -Iincl
 CXXFLAGS:= -std=c++20 -O2 -march=x86-64-v3 -ffp-contract=off -fPIC -Wall -Iinclude -I$(CSRC)/host -I$(JSONDIR)
 
 CU_SRC  := $(CSRC)/capi.cu $(CSRC)/exact_scan.cu $(CSRC)/match_loop.cu $(CSRC)/tensor_scan.cu \
-           $(CSRC)/flashmatch.cu
+           $(CSRC)/flashmatch.cu $(CSRC)/comm.cu
 CU_OBJ  := $(patsubst $(CSRC)/%.cu,build/cu/%.o,$(CU_SRC))
 CU_HDR  := $(wildcard $(CSRC)/*.h $(CSRC)/*.cuh) include/fastnn_b200.h
 HOST_SRC:= $(wildcard $(CSRC)/host/*.cpp)
@@ -34,16 +34,21 @@ LIB_CU  := $(PKG)/libfastnn_b200.so
 LIB_CXX := $(PKG)/libfastnn.so
 PYMOD   := $(PKG)/_fastnn$(EXT)
 
-.PHONY: all product oracle clean
-all: product oracle
+.PHONY: all product oracle testbins clean
+all: product oracle testbins
 product: $(LIB_CU) $(LIB_CXX) $(PYMOD)
+
+# C++ test programs driving the drop-in library (run by tests/, -m gpu)
+testbins: tests/cpp/c5_sharded
+tests/cpp/c5_sharded: tests/cpp/c5_sharded.cpp $(LIB_CXX) $(HOST_HDR)
+	g++ $(CXXFLAGS) -o $@ $< -L$(PKG) -lfastnn -lfastnn_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
 
 build/cu/%.o: $(CSRC)/%.cu $(CU_HDR)
 	@mkdir -p $(dir $@)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
 $(LIB_CU): $(CU_OBJ)
-	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^ -Xlinker -soname=libfastnn_b200.so
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^ -Xlinker -soname=libfastnn_b200.so -ldl
 
 build/host/%.o: $(CSRC)/host/%.cpp $(HOST_HDR)
 	@mkdir -p $(dir $@)

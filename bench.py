@@ -54,6 +54,28 @@ def gen_pool(gen_random):
     return [gen_random(H, W, D, 1000 + i) for i in range(POOL)]
 
 
+def node_pool(gen_random, local_rank, local_world):
+    """The 64-map pool (1.21 GB fp32), generated ONCE per node: local rank 0
+    writes it to /dev/shm and the other ranks of the node map the same pages
+    read-only after a barrier, so 8 ranks hold one copy instead of eight."""
+    if local_world <= 1:
+        return gen_pool(gen_random)
+    path = f"/dev/shm/fnl_bench_pool_{H}x{W}x{D}_{POOL}_{os.getppid()}.npy"
+    if local_rank == 0:
+        arr = np.lib.format.open_memmap(path + ".tmp", mode="w+", dtype=np.float32, shape=(POOL, H, W, D))
+        for i in range(POOL):
+            arr[i] = gen_random(H, W, D, 1000 + i)
+        arr.flush()
+        del arr
+        os.replace(path + ".tmp", path)
+    barrier()
+    pool = np.load(path, mmap_mode="r")
+    barrier()
+    if local_rank == 0:
+        os.unlink(path)  # the mappings stay valid
+    return [pool[i] for i in range(POOL)]
+
+
 def pair_maps(k):
     """Pair k of the synthetic stream: two distinct pool maps."""
     a = k % POOL
@@ -251,7 +273,8 @@ def main_b200(args):
     fnl.set_device(local)
     B = args.pairs
     first_pair = rank * B
-    pool = gen_pool(fnl.gen_random)
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    pool = node_pool(fnl.gen_random, int(os.environ.get("LOCAL_RANK", "0")), local_world)
     samples = math.ceil(H / STRIDE) * math.ceil(W / STRIDE)
 
     # device-resident inputs (value) and pinned host copies (e2e)
@@ -299,6 +322,13 @@ def main_b200(args):
     elapsed_ms = ev0.elapsed_time(ev1)
     timing = fnl.kernel_timing(reset=True)
     matches_last = int(out_counts.sum().item())
+    # which pairs each rank matched and how many matches it found (the shards
+    # are disjoint contiguous pair ranges; no data-path collective)
+    by_rank = [(first_pair, first_pair + B, matches_last)]
+    if world > 1:
+        import torch.distributed as dist
+        by_rank = [None] * world
+        dist.all_gather_object(by_rank, (first_pair, first_pair + B, matches_last))
 
     # ---- per-kernel-class breakdown: one extra step with events around every
     # launch (outside the timed region; events add small gaps)
@@ -335,10 +365,43 @@ def main_b200(args):
     e2e_s = time.perf_counter() - t0
     barrier()
 
+    # ---- the other backends on the same batch (same stream, CUDA events):
+    # the paper's Alg. 3 as the `tensor` backend and the reference's hybrid;
+    # their last outputs feed the parity section
+    other = {}
+    other_outputs = {}
+    for bk in [x for x in ("single", "hybrid", "tensor") if x != args.backend]:
+        if args.no_other_backends:
+            break
+        op = torch.empty_like(out_pairs)
+        oc = torch.empty_like(out_counts)
+
+        def run_bk():
+            fnl.reciprocal_match_device(d1.data_ptr(), d2.data_ptr(), B, H, W, D, op.data_ptr(), oc.data_ptr(),
+                                        backend=bk, stride=STRIDE, metric=METRIC, stream=stream.cuda_stream,
+                                        with_stats=False)
+        for _ in range(2):
+            run_bk()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        nrep = max(3, args.steps // 2)
+        e0.record(stream)
+        for _ in range(nrep):
+            run_bk()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / nrep
+        ms = allreduce([ms], op=torch.distributed.ReduceOp.MAX)[0] if world > 1 else ms
+        other[bk] = {"pairs_per_s": round(B * world / (ms / 1e3), 1), "ms_per_step": round(ms, 3),
+                     "steps": nrep}
+        other_outputs[bk] = (op, oc)
+    fnl.kernel_timing(reset=True)
+
     # ---- C5: one oversized 1536x1152 pair, target columns sharded over the ranks
     c5 = None
     if not args.no_c5:
-        c5 = bench_c5(fnl, world, rank, local)
+        c5 = bench_c5(fnl, world, rank, local, args.backend)
 
     # ---- C3: FlashMatch attention at the MASt3R ViT shapes (rank 0)
     c3 = None
@@ -368,22 +431,8 @@ def main_b200(args):
         cpu = {"value": done / spent, "unit": "pairs/s", "cores": threads, "kind": "reference",
                "sample": f"{done} C2 pairs (512x384 d=24 stride 8, dot), reference reciprocal_match "
                          f"backend=single, {threads} threads, {spent:.1f} s; host CPU {cpu_model()}"}
-        # the same reference as the checker (untimed): the tensor backend must
-        # equal reference backend=single on binary16-rounded maps, bit for bit,
-        # for the first pairs of the last timed step's batch
-        got_pairs = out_pairs[:args.parity_pairs].cpu().numpy()
-        got_counts = out_counts[:args.parity_pairs].cpu().numpy()
-        same = 0
-        for i in range(min(args.parity_pairs, B)):
-            a, b = pair_maps(i)
-            want, _ = ref.reciprocal_match(oracle.half_round_array(pool[a]), oracle.half_round_array(pool[b]),
-                                           backend="single", metric=METRIC, stride=STRIDE,
-                                           block_size=math.ceil(samples / threads), threads=threads)
-            n = int(got_counts[i])
-            same += int(n == len(want) and np.array_equal(got_pairs[i, :n].astype(np.uint32), want))
-        parity = {"pairs_checked": min(args.parity_pairs, B), "identical": same,
-                  "checker": "oracle/_ref reciprocal_match backend=single on binary16-rounded maps "
-                             "(the tensor backend's contract), (i, j, iter) triples of the last timed step"}
+        parity = parity_checks(fnl, ref, oracle, pool, B, args, samples, threads, out_pairs, out_counts,
+                               other_outputs)
 
     if rank != 0:
         return
@@ -406,10 +455,14 @@ def main_b200(args):
     line = {
         "metric": METRIC_NAME, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f16", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": "f16 in / fp32 accumulate (tensor cores); fp32 reference chain for the decision",
+        "data": "synthetic",
         "config": {"workload": "C2/C4: FastNN-Lite reciprocal matching of 512x384 d=24 pairs, stride 8 "
-                               "(3072 samples), T=10, convergence 0.99, dot metric, tensor backend "
-                               "(binary16 in / fp32 accumulate, exact near-tie re-decision)",
+                               f"(3072 samples), T=10, convergence 0.99, dot metric, backend {args.backend} "
+                               "on the tcgen05 route (HybridCast: binary16 in / fp32 accumulate scores nominate "
+                               "candidate sub-tiles; the winner is decided by the reference chain in the "
+                               "backend's own arithmetic, so results are identical to the reference's)",
                    "pairs_per_gpu_per_step": B, "global_batch": B * world, "height": H, "width": W,
                    "dim": D, "stride": STRIDE, "backend": args.backend, "parallelism": f"pairs dp{world}",
                    "inputs": f"pool of {POOL} gen_random maps (seeds 1000..{1000 + POOL - 1}), pair k = "
@@ -418,6 +471,10 @@ def main_b200(args):
                    "query_rows_per_step": tot_rows / args.steps,
                    "near_tie_rows_per_step": near_ties / args.steps if world == 1 else None,
                    "matches_per_step_rank0": matches_last,
+                   "pairs_by_rank": [[int(a), int(b)] for a, b, _ in by_rank],
+                   "matches_by_rank": [int(m) for _, _, m in by_rank],
+                   "host_staging_per_rank_gb": round(2 * B * H * W * D * 4 / 1e9, 2),
+                   "pool": f"{POOL} maps, {POOL * H * W * D * 4 / 1e9:.2f} GB, one copy per node (/dev/shm)",
                    "kernel_breakdown_rank0": breakdown},
         "e2e": {"value": e2e_value, "unit": "pairs/s",
                 "h2d_bytes_per_step": int(2 * B * H * W * D * 4),
@@ -433,6 +490,7 @@ def main_b200(args):
                      "avg_launch_ms": tot_score_ms / max(1, tot_launch)},
         "cpu_baseline": cpu,
         "parity_sample": parity,
+        "other_backends": other,
         "clocks": clk.summary(),
         "c5_sharded_pair": c5,
         "c3_flashmatch": c3,
@@ -440,10 +498,105 @@ def main_b200(args):
     print(json.dumps(line), flush=True)
 
 
+def parity_checks(fnl, ref, oracle, pool, B, args, samples, threads, out_pairs, out_counts, other_outputs):
+    """Re-check outputs of the timed batch against the reference run on the
+    SAME fp32 maps (untimed, rank 0):
+      * the headline backend: ordered (i, j, iter) MatchSets identical to the
+        reference's same backend, for parity_pairs pairs spread over the batch;
+      * hybrid vs the reference's hybrid (2 pairs);
+      * the paper's Alg. 3 (`tensor`: binary16 in, fp32 compare) vs the
+        reference `single` on the unrounded maps: MatchSets, and per grid query
+        the forward NN, where a disagreement is only allowed when the fp32
+        top-2 distance gap is below eps_q, the bound on what binary16 input
+        rounding can move a distance by (both candidates)."""
+    bs = math.ceil(samples / threads)
+    idx = sorted({int(round(x)) for x in np.linspace(0, B - 1, min(args.parity_pairs, B))})
+
+    def ref_match(i, backend):
+        a, b = pair_maps(i)
+        m, _ = ref.reciprocal_match(pool[a], pool[b], backend=backend, metric=METRIC, stride=STRIDE,
+                                    block_size=bs, threads=threads)
+        return m
+
+    def same(op, oc, i, want):
+        n = int(oc[i].item())
+        return n == len(want) and np.array_equal(op[i, :n].cpu().numpy().astype(np.uint32), want)
+
+    ref_single = {}
+    head = 0
+    for i in idx:
+        want = ref_match(i, "single" if args.backend in ("single", "tensor") else args.backend)
+        ref_single[i] = want
+        head += int(same(out_pairs, out_counts, i, want))
+    out = {"pairs_checked": len(idx), "pair_indices": idx, "identical": head,
+           "checker": f"oracle/_ref (the unmodified reference compiled from /root/reference) reciprocal_match "
+                      f"backend={'single' if args.backend == 'tensor' else args.backend} on the same fp32 maps, "
+                      f"ordered (i, j, iter) triples of the last timed step"}
+    if args.backend == "tensor":
+        out["note"] = "headline is Alg. 3: identical only where no near tie flips (see same_input_alg3)"
+    if "hybrid" in other_outputs or args.backend == "hybrid":
+        op, oc = other_outputs.get("hybrid", (out_pairs, out_counts))
+        hi = idx[:2]
+        out["hybrid_vs_reference_hybrid"] = {
+            "pairs_checked": len(hi), "identical": sum(int(same(op, oc, i, ref_match(i, "hybrid"))) for i in hi)}
+    if "tensor" in other_outputs or args.backend == "tensor":
+        op, oc = other_outputs.get("tensor", (out_pairs, out_counts))
+        ti = idx[:2]
+        msets = sum(int(same(op, oc, i, ref_single[i])) for i in ti)
+        grid = np.asarray(fnl.grid_subsample(H, W, 0, STRIDE), dtype=np.int64)
+        nq = mism = above = near = 0
+        eps_max = 0.0
+        for i in ti:
+            a, b = pair_maps(i)
+            Q = pool[a].reshape(-1, D)[grid]
+            T = pool[b].reshape(-1, D)
+            ours = fnl.nn_tensor(Q[None], pool[b], metric=METRIC)["nearest"]
+            theirs = ref.nn_single_loop(Q[None], pool[b], block_size=math.ceil(len(Q) / threads), metric=METRIC,
+                                        precision="full", threads=threads)["nearest"]
+            qn = np.linalg.norm(Q.astype(np.float64), axis=1)
+            tn = float(np.linalg.norm(T.astype(np.float64), axis=1).max())
+            # distance units (dot: -q.t); binary16 rounding u = 2^-11 per input,
+            # subnormal step 2^-24, plus both fp32 chains' rounding
+            eps = 2.0 * (2.0**-10 * qn * tn + 2.0**-24 * math.sqrt(D) * (qn + tn)) + 4.0 * (D + 2) * 2.0**-24 * qn * tn
+            T64 = T.astype(np.float64)
+            gaps = np.empty(len(Q))
+            for c0 in range(0, len(Q), 256):
+                s = -(Q[c0:c0 + 256].astype(np.float64) @ T64.T)
+                p2 = np.partition(s, 1, axis=1)[:, :2]
+                gaps[c0:c0 + 256] = p2[:, 1] - p2[:, 0]
+            bad = ours != theirs
+            nq += len(Q)
+            mism += int(bad.sum())
+            above += int((bad & (gaps > eps)).sum())
+            near += int((gaps <= eps).sum())
+            eps_max = max(eps_max, float(eps.max()))
+        out["same_input_alg3"] = {
+            "backend": "tensor (PAPER.md Alg. 3: binary16 in, fp32 accumulate and compare)",
+            "vs": "reference single on the same unrounded fp32 maps",
+            "matchsets_identical": f"{msets}/{len(ti)}",
+            "grid_queries_checked": nq, "mismatched_queries": mism,
+            "mismatches_with_gap_above_eps": above, "queries_with_gap_below_eps": near,
+            "eps": "per query, distance units: 2(2^-10 |q| t_max + 2^-24 sqrt(d)(|q| + t_max)) + "
+                   "4(d+2) 2^-24 |q| t_max (binary16 rounding of both inputs moves each candidate's distance "
+                   f"by at most half of it); max over the sample {eps_max:.3g}"}
+    return out
+
+
 C5_H, C5_W = 1536, 1152
 
 
-def bench_c5(fnl, world, rank, local, reps=3):
+def c5_golden(backend):
+    """The reference's own C5 MatchSet (tests/golden/recip_c5.npz, made from
+    oracle/_ref by tests/golden/make_golden_c5.py), or None."""
+    path = os.path.join(ROOT, "tests", "golden", "recip_c5.npz")
+    key = f"matches_{backend}"
+    if not os.path.exists(path):
+        return None
+    z = np.load(path)
+    return z[key] if key in z else None
+
+
+def bench_c5(fnl, world, rank, local, backend, reps=3):
     """Config C5: one 1536x1152 d=24 pair (1,769,472 px/image, 27,648 samples),
     every NN pass scanning 1/world of the target columns per rank with one
     int64 MIN all-reduce of the per-query (dist, index) keys (NCCL).  Device
@@ -453,13 +606,13 @@ def bench_c5(fnl, world, rank, local, reps=3):
     D1 = torch.from_numpy(fnl.gen_random(C5_H, C5_W, D, 2606)).cuda()
     D2 = torch.from_numpy(fnl.gen_random(C5_H, C5_W, D, 2607)).cuda()
     stream = torch.cuda.current_stream()
-    match_sharded(D1, D2, stride=STRIDE, metric=METRIC)  # warm-up (workspace, packing)
+    match_sharded(D1, D2, stride=STRIDE, metric=METRIC, backend=backend)  # warm-up (workspace, packing)
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(reps):
-        pairs, counts, stats = match_sharded(D1, D2, stride=STRIDE, metric=METRIC)
+        pairs, counts, stats = match_sharded(D1, D2, stride=STRIDE, metric=METRIC, backend=backend)
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
@@ -474,12 +627,13 @@ def bench_c5(fnl, world, rank, local, reps=3):
         try:
             peers = PeerTransport(((C5_H + 7) // 8) * ((C5_W + 7) // 8), None)
             try:
-                match_sharded(D1, D2, stride=STRIDE, metric=METRIC, transport="p2p", peers=peers)
+                match_sharded(D1, D2, stride=STRIDE, metric=METRIC, backend=backend, transport="p2p", peers=peers)
                 barrier()
                 torch.cuda.synchronize()
                 e0.record(stream)
                 for _ in range(reps):
-                    pp, pc, _ = match_sharded(D1, D2, stride=STRIDE, metric=METRIC, transport="p2p", peers=peers)
+                    pp, pc, _ = match_sharded(D1, D2, stride=STRIDE, metric=METRIC, backend=backend,
+                                              transport="p2p", peers=peers)
                 e1.record(stream)
                 torch.cuda.synchronize()
                 pms = e0.elapsed_time(e1) / reps
@@ -494,13 +648,21 @@ def bench_c5(fnl, world, rank, local, reps=3):
                 peers.close()
         except Exception as e:  # reported, not fatal: the NCCL number above stands
             peer = {"error": str(e)[:200]}
+    gold = c5_golden(backend)
+    n = int(counts[0].item())
+    parity = None
+    if gold is not None:
+        parity = {"identical": bool(n == len(gold) and np.array_equal(pairs[0, :n].cpu().numpy().astype(np.uint32),
+                                                                         gold)),
+                  "checker": f"tests/golden/recip_c5.npz: the reference's own reciprocal_match backend={backend} "
+                             "on the same maps (generated from oracle/_ref)"}
     return {"workload": f"C5: one {C5_H}x{C5_W} d=24 pair (gen_random 2606/2607), stride 8 "
-                        f"({((C5_H + 7) // 8) * ((C5_W + 7) // 8)} samples), dot, tensor backend, target columns "
+                        f"({((C5_H + 7) // 8) * ((C5_W + 7) // 8)} samples), dot, backend {backend}, target columns "
                         f"sharded over {world} rank(s), int64 MIN all-reduce of (dist, index) keys per NN pass",
             "shards": world, "ms_per_pair": round(ms, 3), "pairs_per_s": round(1000.0 / ms, 2),
             "query_rows": int(rows), "iterations": int(stats[0]["iterations"]),
             "matches": int(counts[0].item()),
-            "aggregate_tflops": round(flops / (ms / 1e3) / 1e12, 1), "peer_memory": peer}
+            "aggregate_tflops": round(flops / (ms / 1e3) / 1e12, 1), "peer_memory": peer, "parity": parity}
 
 
 def main():
@@ -509,11 +671,15 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--pairs", type=int, default=128, help="pairs per GPU per step")
-    ap.add_argument("--backend", default="tensor")
+    ap.add_argument("--backend", default="single",
+                    help="headline backend: the reference's default `single` (full precision, bit-identical "
+                         "to the reference on the same inputs) on the tcgen05 route")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--parity-pairs", type=int, default=2, help="pairs of the timed batch re-checked against the reference")
+    ap.add_argument("--parity-pairs", type=int, default=8,
+                    help="pairs of the timed batch (first .. last) re-checked against the reference")
+    ap.add_argument("--no-other-backends", action="store_true", help="skip timing the non-headline backends")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c5", action="store_true", help="skip the sharded 1536x1152 pair (config C5)")
     ap.add_argument("--no-c3", action="store_true", help="skip the FlashMatch attention section (config C3)")

@@ -223,7 +223,34 @@ typedef struct fnl_shard_spec {
     int64_t* const* peer_keys;
     uint32_t* const* peer_flags;
     uint64_t* barrier_seq;
+    /* Optional native NCCL communicator (fnl_comm_create; used when
+     * peer_keys is NULL): the library all-reduces the keys itself with
+     * ncclAllReduce(int64, ncclMin) on the context stream and `reduce` may be
+     * NULL.  rank / count must equal the communicator's. */
+    struct fnl_comm* comm;
 } fnl_shard_spec;
+
+/* Native NCCL communicator for the C5 key reduction.  libnccl.so.2 is
+ * opened at first use (dlopen: the copy already loaded in the process, e.g.
+ * torch's, else the system one), so the library has no link-time NCCL
+ * dependency.  Rank 0 calls fnl_nccl_unique_id and hands the 128 bytes to the
+ * other ranks out of band; every rank then calls fnl_comm_create (collective,
+ * one GPU per rank: the context's device). */
+typedef struct fnl_comm fnl_comm;
+int fnl_nccl_unique_id(unsigned char id[128]);
+int fnl_comm_create(fnl_context* ctx, const unsigned char id[128], int nranks, int rank, fnl_comm** out);
+int fnl_comm_destroy(fnl_comm* comm);
+int fnl_comm_info(const fnl_comm* comm, int* nranks, int* rank, int* nccl_version);
+
+/* Config C5 from host buffers with a native communicator: every rank passes
+ * the same two maps; the target columns of each NN pass are split over the
+ * communicator's ranks and the winner keys are MIN-all-reduced with NCCL.
+ * Every rank receives the MatchSet of the unsharded run (same arguments and
+ * outputs as fnl_reciprocal_match). */
+int fnl_reciprocal_match_sharded(fnl_context* ctx, fnl_comm* comm, const float* h_d1, uint32_t h1,
+                                 uint32_t w1, const float* h_d2, uint32_t h2, uint32_t w2, uint32_t dim,
+                                 const fnl_match_config* cfg, int backend, uint32_t* h_pairs,
+                                 uint32_t* n_pairs, fnl_run_stats* stats);
 
 /* Peer-memory buffers for fnl_shard_spec's peer transport: device allocations
  * of their own (so CUDA IPC handles cover exactly them), filled with INT64_MAX

@@ -443,17 +443,20 @@ PYBIND11_MODULE(_fastnn, m) {
     m.def("reciprocal_match_sharded_device",
           [](std::uintptr_t d1, std::uintptr_t d2, std::uint32_t n, std::uint32_t h, std::uint32_t w,
              std::uint32_t d, std::uintptr_t out_pairs, std::uintptr_t out_counts, std::uintptr_t keys,
-             std::uint64_t keys_capacity, std::uint32_t rank, std::uint32_t count, py::function reduce,
+             std::uint64_t keys_capacity, std::uint32_t rank, std::uint32_t count, py::object reduce,
              const std::string& backend, std::uint32_t k, std::uint32_t stride, std::uint32_t max_iters,
-             double convergence, const std::string& metric, std::uint32_t block_size, py::object stream) {
+             double convergence, const std::string& metric, std::uint32_t block_size, py::object stream,
+             std::uintptr_t comm) {
               void* const sh = stream_handle(stream);  // with the GIL held
               const auto cfg = make_cfg(k, stride, max_iters, convergence, metric, "full", block_size);
               cfg.validate();
               const auto cc = c_cfg(cfg);
               const int be = c_backend(fastnn::backend_from_string(backend));
               std::vector<fnl_run_stats> st(n);
+              if (reduce.is_none() && !comm)
+                  throw std::invalid_argument("reciprocal_match_sharded_device: a reduce callback or comm is required");
               struct Ctx {
-                  py::function fn;
+                  py::object fn;
                   std::string err;
               } cb{reduce, {}};
               fnl_shard_spec spec{};
@@ -462,7 +465,8 @@ PYBIND11_MODULE(_fastnn, m) {
               spec.d_keys = reinterpret_cast<std::int64_t*>(keys);
               spec.keys_capacity = keys_capacity;
               spec.user = &cb;
-              spec.reduce = [](void* user, std::int64_t*, std::uint64_t cnt, void*) -> int {
+              spec.comm = reinterpret_cast<fnl_comm*>(comm);  // native NCCL: the library reduces itself
+              if (!spec.comm) spec.reduce = [](void* user, std::int64_t*, std::uint64_t cnt, void*) -> int {
                   auto* c = static_cast<Ctx*>(user);
                   py::gil_scoped_acquire gil;
                   try {
@@ -495,7 +499,35 @@ PYBIND11_MODULE(_fastnn, m) {
           py::arg("keys_capacity"), py::arg("shard_rank"), py::arg("shard_count"), py::arg("reduce"),
           py::arg("backend") = "tensor", py::arg("k") = 0, py::arg("stride") = 8, py::arg("max_iters") = 10,
           py::arg("convergence") = 0.99, py::arg("metric") = "dot", py::arg("block_size") = 4096,
-          py::arg("stream") = py::none());
+          py::arg("stream") = py::none(), py::arg("comm") = 0);
+
+    // Native NCCL communicator for the C5 key reduction (fnl_comm_*): rank 0
+    // makes the id, every rank creates its communicator (collective).
+    m.def("nccl_unique_id", [] {
+        unsigned char id[128];
+        fastnn::b200::check(fnl_nccl_unique_id(id));
+        return py::bytes(reinterpret_cast<const char*>(id), 128);
+    });
+    m.def("comm_create",
+          [](py::bytes id, int nranks, int rank) {
+              const std::string s = id;
+              if (s.size() != 128) throw std::invalid_argument("comm_create: the NCCL id is 128 bytes");
+              fnl_comm* c = nullptr;
+              {
+                  py::gil_scoped_release nogil;
+                  fastnn::b200::check(fnl_comm_create(fastnn::b200::context(),
+                                                      reinterpret_cast<const unsigned char*>(s.data()), nranks,
+                                                      rank, &c));
+              }
+              return reinterpret_cast<std::uintptr_t>(c);
+          },
+          py::arg("id"), py::arg("nranks"), py::arg("rank"));
+    m.def("comm_destroy", [](std::uintptr_t c) { fastnn::b200::check(fnl_comm_destroy(reinterpret_cast<fnl_comm*>(c))); });
+    m.def("comm_info", [](std::uintptr_t c) {
+        int n = 0, r = 0, v = 0;
+        fastnn::b200::check(fnl_comm_info(reinterpret_cast<const fnl_comm*>(c), &n, &r, &v));
+        return py::make_tuple(n, r, v);
+    });
 
     // Same, with the peer-memory transport (keys pushed into every rank's
     // buffer by the merge epilogues, peer-memory barrier instead of NCCL).

@@ -685,14 +685,23 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
     // route (K3 scores + certified resolution in the backend's arithmetic,
     // bit-identical to the reference) when the inputs allow it.
     const bool tensor = backend == FNL_BACKEND_TENSOR;
-    const bool sharded = shard && shard->count > 1;
+    // (a native communicator takes the key path even with one rank, so the
+    // NCCL reduction is exercised wherever the run happens)
+    const bool sharded = shard && (shard->count > 1 || (shard->comm && !shard->peer_keys));
     if (shard) {
         if (shard->count == 0 || shard->rank >= shard->count)
             return fail(FNL_EINVAL, "sharded reciprocal_match: rank must be < count");
         const bool peer = sharded && shard->peer_keys;
-        if (sharded && !peer && (!shard->d_keys || !shard->reduce || shard->keys_capacity < (uint64_t)npairs * cap))
-            return fail(FNL_EINVAL, "sharded reciprocal_match: key buffer (npairs * samples) and reduce callback "
-                                    "required");
+        if (sharded && !peer &&
+            (!shard->d_keys || (!shard->reduce && !shard->comm) || shard->keys_capacity < (uint64_t)npairs * cap))
+            return fail(FNL_EINVAL, "sharded reciprocal_match: key buffer (npairs * samples) and a reduce callback "
+                                    "or NCCL communicator required");
+        if (shard->comm && !peer) {
+            int nr = 0, rk = 0;
+            fnl::comm_size(shard->comm, &nr, &rk);
+            if ((uint32_t)nr != shard->count || (uint32_t)rk != shard->rank)
+                return fail(FNL_EINVAL, "sharded reciprocal_match: rank / count differ from the communicator's");
+        }
         if (peer && (shard->count > (uint32_t)fnl::kMaxShardPeers || !shard->peer_flags || !shard->barrier_seq ||
                      !shard->d_keys || shard->keys_capacity < 2ull * npairs * cap))
             return fail(FNL_EINVAL, "sharded reciprocal_match (peer memory): at most 8 ranks, key buffers of "
@@ -823,8 +832,12 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
                 TRY(fnl::tensor_nn_pass(ctx, npairs, TQ, ids, cap, m.n_active, m.done, TT, dim, l2, out, cap,
                                         nullptr, near_ties, tb, te,
                                         reinterpret_cast<long long*>(shard->d_keys), nullptr, &rs));
-            if (shard->reduce(shard->user, shard->d_keys, nkeys, ctx->stream) != 0)
+            if (shard->comm) {
+                TRY(fnl::comm_allreduce_min_i64(shard->comm, reinterpret_cast<long long*>(shard->d_keys), nkeys,
+                                                ctx->stream));
+            } else if (shard->reduce(shard->user, shard->d_keys, nkeys, ctx->stream) != 0) {
                 return fail(FNL_ERUNTIME, "sharded reciprocal_match: key reduction callback failed");
+            }
             return fnl::tensor_shard_finalize(ctx, npairs, reinterpret_cast<const long long*>(shard->d_keys), cap,
                                               m.n_active, m.done, out);
         }
@@ -1007,6 +1020,47 @@ extern "C" int fnl_reciprocal_match(fnl_context* ctx, const float* h_d1, uint32_
     fnl_run_stats local;
     TRY(run_match(ctx, 1, d1, h1, w1, d2, h2, w2, dim, cfg, backend, dp, dn,
                   stats ? stats : &local, true));
+    uint32_t n = 0;
+    FNL_CUDA_TRY(cudaMemcpyAsync(&n, dn, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    FNL_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (n && h_pairs)
+        FNL_CUDA_TRY(cudaMemcpyAsync(h_pairs, dp, (size_t)n * 12, cudaMemcpyDeviceToHost, ctx->stream));
+    FNL_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (n_pairs) *n_pairs = n;
+    return FNL_OK;
+}
+
+extern "C" int fnl_reciprocal_match_sharded(fnl_context* ctx, fnl_comm* comm, const float* h_d1, uint32_t h1,
+                                            uint32_t w1, const float* h_d2, uint32_t h2, uint32_t w2, uint32_t dim,
+                                            const fnl_match_config* cfg, int backend, uint32_t* h_pairs,
+                                            uint32_t* n_pairs, fnl_run_stats* stats) {
+    TRY(check_device(ctx));
+    TRY(check_cfg(cfg));
+    if (!comm) return fail(FNL_EINVAL, "fnl_reciprocal_match_sharded: null communicator");
+    int nranks = 0, rank = 0;
+    fnl::comm_size(comm, &nranks, &rank);
+    const uint64_t n1 = (uint64_t)h1 * w1 * dim, n2 = (uint64_t)h2 * w2 * dim;
+    float *d1, *d2;
+    TRY(dev_arr(ctx, "rms.d1", n1, &d1));
+    TRY(dev_arr(ctx, "rms.d2", n2, &d2));
+    FNL_CUDA_TRY(cudaMemcpyAsync(d1, h_d1, n1 * 4, cudaMemcpyHostToDevice, ctx->stream));
+    FNL_CUDA_TRY(cudaMemcpyAsync(d2, h_d2, n2 * 4, cudaMemcpyHostToDevice, ctx->stream));
+    const uint32_t stride = derived_stride(h1, w1, cfg->k, cfg->grid_stride);
+    const uint32_t samples = ((h1 + stride - 1) / stride) * ((w1 + stride - 1) / stride);
+    const uint32_t cap = std::max<uint32_t>(samples, 1);
+    uint32_t *dp, *dn;
+    long long* keys;
+    TRY(dev_arr(ctx, "rms.pairs", (size_t)3 * cap, &dp));
+    TRY(dev_arr(ctx, "rms.np", 1, &dn));
+    TRY(dev_arr(ctx, "rms.keys", cap, &keys));
+    fnl_shard_spec spec{};
+    spec.rank = (uint32_t)rank;
+    spec.count = (uint32_t)nranks;
+    spec.d_keys = reinterpret_cast<int64_t*>(keys);
+    spec.keys_capacity = cap;
+    spec.comm = comm;
+    fnl_run_stats local;
+    TRY(run_match(ctx, 1, d1, h1, w1, d2, h2, w2, dim, cfg, backend, dp, dn, stats ? stats : &local, true, &spec));
     uint32_t n = 0;
     FNL_CUDA_TRY(cudaMemcpyAsync(&n, dn, 4, cudaMemcpyDeviceToHost, ctx->stream));
     FNL_CUDA_TRY(cudaStreamSynchronize(ctx->stream));

@@ -33,6 +33,7 @@
 
 #include <stdlib.h>
 
+#include <mutex>
 #include <string>
 
 #include "fastnn_b200.h"
@@ -684,7 +685,9 @@ __global__ void __launch_bounds__((8 * kH + 2) * 32, 1)
     }
 }
 
-bool fm_attr_done = false;
+// cudaFuncSetAttribute applies to the current device only: one flag per device
+std::mutex fm_attr_mu;
+bool fm_attr_done[64] = {};
 
 }  // namespace
 
@@ -702,11 +705,16 @@ int flashmatch_forward(fnl_context* ctx, const fnl_attention_desc& d) {
     for (uintptr_t p : ptrs)
         if (p % 16) return fail(FNL_EINVAL, "flashmatch: tensors must be 16 B aligned");
     if (d.heads > 65535 || d.batch > 65535) return fail(FNL_EINVAL, "flashmatch: batch/heads exceed 65535");
-    if (!fm_attr_done) {
-        FNL_CUDA_TRY(cudaFuncSetAttribute(flashmatch3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFm2));
-        FNL_CUDA_TRY(cudaFuncSetAttribute(flashmatch4_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFm4));
-        FNL_CUDA_TRY(cudaFuncSetAttribute(flashmatch4_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFm4));
-        fm_attr_done = true;
+    {
+        int dev = 0;
+        FNL_CUDA_TRY(cudaGetDevice(&dev));
+        std::lock_guard<std::mutex> lk(fm_attr_mu);
+        if (dev < 0 || dev >= 64 || !fm_attr_done[dev]) {
+            FNL_CUDA_TRY(cudaFuncSetAttribute(flashmatch3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFm2));
+            FNL_CUDA_TRY(cudaFuncSetAttribute(flashmatch4_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFm4));
+            FNL_CUDA_TRY(cudaFuncSetAttribute(flashmatch4_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFm4));
+            if (dev >= 0 && dev < 64) fm_attr_done[dev] = true;
+        }
     }
     FmArgs a{};
     a.q = static_cast<const __half*>(d.q);

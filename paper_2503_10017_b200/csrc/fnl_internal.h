@@ -46,6 +46,9 @@ struct ProfScope {
 
 // ---------------------------------------------------------------- K7 FlashMatch
 int flashmatch_forward(fnl_context* ctx, const struct fnl_attention_desc& d);
+// native NCCL (comm.cu)
+int comm_allreduce_min_i64(struct fnl_comm* comm, long long* d_keys, uint64_t count, cudaStream_t stream);
+int comm_size(const struct fnl_comm* comm, int* nranks, int* rank);
 int flashmatch_trace(unsigned long long* host64);  // profiling aid (FNL_FM_TRACE=1)
 
 // ---------------------------------------------------------------- K1 prepare

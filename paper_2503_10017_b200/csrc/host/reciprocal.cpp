@@ -5,6 +5,9 @@
 #include "fastnn/reciprocal.hpp"
 
 #include <cmath>
+#include <cstring>
+
+#include "fastnn/sharded.hpp"
 #include <stdexcept>
 
 #include "runtime.hpp"
@@ -70,33 +73,17 @@ MatchOutcome reciprocal_match(const FeatureMap& D1, const FeatureMap& D2, const 
                                       D2.width, D1.dim, D2.dim, cfg, backend);
 }
 
-MatchOutcome b200::reciprocal_match_raw(const float* d1, std::uint32_t h1, std::uint32_t w1,
-                                        const float* d2, std::uint32_t h2, std::uint32_t w2,
-                                        std::uint32_t dim1, std::uint32_t dim2, const MatchConfig& cfg,
-                                        NnBackend backend) {
-    cfg.validate();
-    if (dim1 != dim2)
-        throw std::invalid_argument("reciprocal_match: descriptor dim mismatch (" + std::to_string(dim1) +
-                                    " vs " + std::to_string(dim2) + ")");
-    const std::uint32_t dim = dim1;
-    const FeatureMap D1shape(h1, w1, 1);
-    const int code = backend_code(backend);
-    const fnl_match_config c{cfg.k, cfg.grid_stride, cfg.max_iters, cfg.convergence_fraction,
-                             metric_code(cfg.metric),
-                             cfg.precision == PrecisionMode::Hybrid ? FNL_PREC_HYBRID : FNL_PREC_FULL,
-                             cfg.block_size};
-    const std::size_t samples = grid_subsample(D1shape, cfg.k, cfg.grid_stride).size();
-    std::vector<std::uint32_t> flat(3 * std::max<std::size_t>(samples, 1));
-    std::uint32_t n = 0;
-    fnl_run_stats st{};
-    b200::check(fnl_reciprocal_match(b200::context(), d1, h1, w1, d2, h2, w2, dim, &c, code,
-                                     flat.data(), &n, &st));
+namespace {
+
+// MatchOutcome from the C-ABI outputs: the MatchSet in harvest order and the
+// RunReport, field for field as src/reciprocal.cpp:105-111, :195-205 fill it
+MatchOutcome make_outcome(const std::vector<std::uint32_t>& flat, std::uint32_t n, const fnl_run_stats& st,
+                          std::uint32_t h1, std::uint32_t w1, std::uint32_t h2, std::uint32_t w2,
+                          std::uint32_t dim, const MatchConfig& cfg, NnBackend backend) {
     MatchOutcome out;
     out.matches.pairs.reserve(n);
     for (std::uint32_t k = 0; k < n; ++k)
         out.matches.pairs.push_back({flat[3 * k], flat[3 * k + 1], flat[3 * k + 2]});
-
-    // RunReport, field for field as src/reciprocal.cpp:105-111, :195-205 fill it
     RunReport& r = out.report;
     const bool hybrid = backend == NnBackend::HybridCast || backend == NnBackend::Tensor ||
                         (backend != NnBackend::Bruteforce && cfg.precision == PrecisionMode::Hybrid);
@@ -129,6 +116,65 @@ MatchOutcome b200::reciprocal_match_raw(const float* d1, std::uint32_t h1, std::
     r.duplicates_dropped = st.duplicates_dropped;
     r.active_history.assign(st.active_history, st.active_history + st.history_len);
     return out;
+}
+
+fnl_match_config c_config(const MatchConfig& cfg) {
+    return fnl_match_config{cfg.k, cfg.grid_stride, cfg.max_iters, cfg.convergence_fraction,
+                            metric_code(cfg.metric),
+                            cfg.precision == PrecisionMode::Hybrid ? FNL_PREC_HYBRID : FNL_PREC_FULL,
+                            cfg.block_size};
+}
+
+}  // namespace
+
+MatchOutcome b200::reciprocal_match_raw(const float* d1, std::uint32_t h1, std::uint32_t w1,
+                                        const float* d2, std::uint32_t h2, std::uint32_t w2,
+                                        std::uint32_t dim1, std::uint32_t dim2, const MatchConfig& cfg,
+                                        NnBackend backend) {
+    cfg.validate();
+    if (dim1 != dim2)
+        throw std::invalid_argument("reciprocal_match: descriptor dim mismatch (" + std::to_string(dim1) +
+                                    " vs " + std::to_string(dim2) + ")");
+    const std::uint32_t dim = dim1;
+    const FeatureMap D1shape(h1, w1, 1);
+    const fnl_match_config c = c_config(cfg);
+    const std::size_t samples = grid_subsample(D1shape, cfg.k, cfg.grid_stride).size();
+    std::vector<std::uint32_t> flat(3 * std::max<std::size_t>(samples, 1));
+    std::uint32_t n = 0;
+    fnl_run_stats st{};
+    b200::check(fnl_reciprocal_match(b200::context(), d1, h1, w1, d2, h2, w2, dim, &c, backend_code(backend),
+                                     flat.data(), &n, &st));
+    return make_outcome(flat, n, st, h1, w1, h2, w2, dim, cfg, backend);
+}
+
+// ---------------------------------------------------------------- C5 extension
+NcclCommunicator::Id NcclCommunicator::unique_id() {
+    Id id{};
+    b200::check(fnl_nccl_unique_id(id.data()));
+    return id;
+}
+
+NcclCommunicator::NcclCommunicator(const Id& id, int nranks, int rank) : nranks_(nranks), rank_(rank) {
+    b200::check(fnl_comm_create(b200::context(), id.data(), nranks, rank, &comm_));
+}
+
+NcclCommunicator::~NcclCommunicator() { fnl_comm_destroy(comm_); }
+
+MatchOutcome reciprocal_match_sharded(const FeatureMap& D1, const FeatureMap& D2, const MatchConfig& cfg,
+                                      NnBackend backend, const NcclCommunicator& comm) {
+    cfg.validate();
+    if (D1.dim != D2.dim)
+        throw std::invalid_argument("reciprocal_match: descriptor dim mismatch (" + std::to_string(D1.dim) +
+                                    " vs " + std::to_string(D2.dim) + ")");
+    const fnl_match_config c = c_config(cfg);
+    const std::size_t samples = grid_subsample(D1, cfg.k, cfg.grid_stride).size();
+    std::vector<std::uint32_t> flat(3 * std::max<std::size_t>(samples, 1));
+    std::uint32_t n = 0;
+    fnl_run_stats st{};
+    b200::check(fnl_reciprocal_match_sharded(b200::context(), comm.handle(), D1.data.data(), D1.height, D1.width,
+                                             D2.data.data(), D2.height, D2.width, D1.dim, &c,
+                                             backend_code(backend), flat.data(), &n, &st));
+    return make_outcome(flat, n, st, D1.height, D1.width, D2.height, D2.width, D1.dim, cfg, backend);
 }
 
 }  // namespace fastnn

@@ -997,6 +997,9 @@ struct PeerFlags {
 __global__ void shard_barrier_kernel(PeerFlags f, unsigned int* own, unsigned int target, unsigned int* err) {
     __threadfence_system();  // this rank's key pushes (earlier kernels) before the arrivals
     for (uint32_t r = 0; r < f.n; ++r) atomicAdd_system(f.flags[r], 1u);
+    // an earlier barrier of this run already timed out: the run fails anyway,
+    // so do not stall another 20 s here (the arrivals above still let peers on)
+    if (*reinterpret_cast<volatile unsigned int*>(err)) return;
     unsigned long long t0, t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     for (;;) {

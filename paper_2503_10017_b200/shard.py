@@ -17,6 +17,10 @@ run.  This is the only collective on the path: 8 B per active query per pass
 The device work is in libfastnn_b200.so (fnl_reciprocal_match_sharded_device);
 this module only supplies the key buffer and the all-reduce callback.
 
+``transport="nccl-native"`` keeps NCCL but drops the Python callback: the
+library owns an NCCL communicator (fnl_comm_create, NativeComm) and issues
+ncclAllReduce(int64, MIN) on the matcher's stream itself.
+
 ``transport="p2p"`` replaces the NCCL all-reduce with peer memory: every
 rank's key buffers and barrier counter are CUDA-IPC-mapped into every other
 rank (NVLink / NVSwitch peer access), the merge and near-tie epilogues push
@@ -102,6 +106,7 @@ class PeerTransport:
             self.close()
             raise RuntimeError("peer-memory transport unavailable: " + bad[0])
         self.seq = 0
+        self.broken = None
 
     def close(self):
         for p in self.opened:
@@ -111,8 +116,36 @@ class PeerTransport:
         self._fnl.p2p_free(self.flag)
 
 
+class NativeComm:
+    """A native NCCL communicator inside libfastnn_b200 (fnl_comm_create) over
+    the ranks of `group`: the library runs ncclAllReduce(int64, MIN) on the
+    keys itself, on the matcher's stream -- no Python callback per pass.
+    Rank 0's NCCL id reaches the others through torch.distributed."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        from . import _fastnn
+        self._fnl = _fastnn
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        ids = [_fastnn.nccl_unique_id() if self.rank == 0 else None]
+        if self.world > 1:
+            dist.broadcast_object_list(ids, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                       group=group)
+        self.handle = _fastnn.comm_create(ids[0], self.world, self.rank)
+
+    def info(self):
+        return self._fnl.comm_info(self.handle)
+
+    def close(self):
+        if self.handle:
+            self._fnl.comm_destroy(self.handle)
+            self.handle = 0
+
+
 def match_sharded(d1, d2, stride=8, metric="dot", group=None, backend="tensor", transport="nccl",
-                  peers=None, **kw):
+                  peers=None, comm=None, **kw):
     """Reciprocal matching of one pair (or a stack) with the target columns
     sharded over the ranks of `group` (torch.distributed; NCCL on GPUs).
 
@@ -139,11 +172,19 @@ def match_sharded(d1, d2, stride=8, metric="dot", group=None, backend="tensor", 
         own = peers is None
         if own:
             peers = PeerTransport(P * samples, group)
+        if peers.broken:
+            raise RuntimeError("PeerTransport unusable after a failed call (" + peers.broken +
+                               "); its barrier counters are out of step: create a new one")
         try:
             stats, peers.seq = _fastnn.reciprocal_match_p2p_device(
                 d1.data_ptr(), d2.data_ptr(), P, H, W, D, pairs.data_ptr(), counts.data_ptr(),
                 2 * peers.nkeys, rank, peers.peer_keys, peers.peer_flags, peers.seq, backend=backend,
                 stride=stride, metric=metric, stream=stream, **kw)
+        except Exception as e:
+            # the device counters advanced but barrier_seq did not come back:
+            # a reused transport would compute stale barrier targets
+            peers.broken = str(e)[:200]
+            raise
         finally:
             if own:
                 torch.cuda.synchronize(d1.device)
@@ -152,6 +193,21 @@ def match_sharded(d1, d2, stride=8, metric="dot", group=None, backend="tensor", 
                 peers.close()
         return pairs, counts, stats
     keys = torch.empty((P * samples,), dtype=torch.int64, device=d1.device)
+    if transport == "nccl-native":
+        # the library all-reduces with its own NCCL communicator
+        own = comm is None
+        if own:
+            comm = NativeComm(group)
+        try:
+            stats = _fastnn.reciprocal_match_sharded_device(
+                d1.data_ptr(), d2.data_ptr(), P, H, W, D, pairs.data_ptr(), counts.data_ptr(), keys.data_ptr(),
+                keys.numel(), comm.rank, comm.world, None, backend=backend, stride=stride, metric=metric,
+                stream=stream, comm=comm.handle, **kw)
+        finally:
+            if own:
+                torch.cuda.synchronize(d1.device)
+                comm.close()
+        return pairs, counts, stats
 
     def reduce(count):
         dist.all_reduce(keys[:count], op=dist.ReduceOp.MIN, group=group)

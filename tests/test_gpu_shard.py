@@ -19,7 +19,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, D1, D2, metric, out, transport="nccl", calls=1):
+def _worker(rank, world, port, D1, D2, metric, out, transport="nccl", calls=1, backend="tensor"):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -35,12 +35,13 @@ def _worker(rank, world, port, D1, D2, metric, out, transport="nccl", calls=1):
         samples = ((D1.shape[0] + 7) // 8) * ((D1.shape[1] + 7) // 8)
         peers = PeerTransport(samples, None)
         for _ in range(calls):
-            pairs, counts, stats = match_sharded(d1, d2, metric=metric, transport="p2p", peers=peers)
+            pairs, counts, stats = match_sharded(d1, d2, metric=metric, transport="p2p", peers=peers,
+                                                 backend=backend)
         torch.cuda.synchronize()
         dist.barrier()
         peers.close()
     else:
-        pairs, counts, stats = match_sharded(d1, d2, metric=metric)
+        pairs, counts, stats = match_sharded(d1, d2, metric=metric, backend=backend)
     torch.cuda.synchronize()
     n = int(counts[0].item())
     out[rank] = (pairs[0, :n].cpu().numpy().copy(), stats[0]["iterations"])
@@ -74,5 +75,21 @@ def test_sharded_peer_memory_equals_unsharded(fnl, H, W, world, metric, calls):
     out = mgr.dict()
     mp.spawn(_worker, args=(world, _free_port(), D1, D2, metric, out, "p2p", calls), nprocs=world, join=True)
     for r in range(world):
+        got, _ = out[r]
+        assert np.array_equal(got.astype(np.uint32), want), f"rank {r}"
+
+
+@pytest.mark.parametrize("backend,metric", [("single", "dot"), ("single", "l2"), ("hybrid", "dot")])
+def test_sharded_reference_backends_equal_reference(fnl, ref, backend, metric):
+    """The reference backends shard too (tensor route, winner keys in the
+    backend's own arithmetic): 2 ranks == the reference on the same maps."""
+    import torch.multiprocessing as mp
+    D1 = fnl.gen_random(128, 96, 24, 606)
+    D2 = fnl.gen_random(128, 96, 24, 607)
+    want, _ = ref.reciprocal_match(D1, D2, backend=backend, metric=metric, stride=8)
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(2, _free_port(), D1, D2, metric, out, "nccl", 1, backend), nprocs=2, join=True)
+    for r in range(2):
         got, _ = out[r]
         assert np.array_equal(got.astype(np.uint32), want), f"rank {r}"
