@@ -190,7 +190,7 @@ int fnl_mutual_nn_tensor(fnl_context* ctx, const float* h_d1, uint32_t h1, uint3
 
 /* ---- target-sharded matching (config C5: one oversized pair over N GPUs) -----
  * Every process holds both maps; for each NN pass, shard `rank` of `count`
- * scans only its contiguous range of 128-target tiles of the target map (image
+ * scans only its contiguous range of 256-target tiles of the target map (image
  * B's pixels in the forward pass, image A's in the reverse pass) and writes
  * each query's exact winner in that range as a signed 64-bit key
  *   ((orderable(dist) << 32) | index) ^ 2^63     (INT64_MAX = no candidate)
@@ -200,7 +200,9 @@ int fnl_mutual_nn_tensor(fnl_context* ctx, const float* h_d1, uint32_t h1, uint3
  * ordered on `stream` (e.g. torch.distributed.all_reduce(op=MIN) on NCCL).
  * The reduced key is the global reference winner (lowest index on exact
  * ties), so every process continues with identical state and the MatchSet is
- * bit-identical to the unsharded run.  Tensor backend only.  Replaces nothing
+ * bit-identical to the unsharded run.  Any backend on the tensor route (the
+ * winner keys carry the backend's own distances; inputs the route refuses are
+ * rejected with FNL_EINVAL).  Replaces nothing
  * in the reference (it has no distributed code); the entry point mirrors
  * fnl_reciprocal_match_batch_device. */
 typedef int (*fnl_key_reduce_fn)(void* user, int64_t* d_keys, uint64_t count, void* stream);

@@ -799,7 +799,7 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
             ++call;
             if (!sharded)
                 return fnl::tensor_nn_pass(ctx, npairs, TQ, ids, cap, m.n_active, m.done, TT, dim, l2, out, cap,
-                                           nullptr, near_ties, 0, 0, nullptr, nullptr, &rs);            // target shard of this rank: contiguous 128-target tiles
+                                           nullptr, near_ties, 0, 0, nullptr, nullptr, &rs);            // target shard of this rank: contiguous 256-target tiles
             const uint64_t tiles = ceil_div(nt, fnl::kTargetTileRows);
             const uint32_t tb = (uint32_t)(tiles * shard->rank / shard->count);
             const uint32_t te = (uint32_t)(tiles * (shard->rank + 1) / shard->count);

@@ -22,8 +22,7 @@
 // binary16 P = 2^(s*scale*log2e - m) to shared memory (UMMA K-major layout)
 // and rescales O in TMEM only when the row max grew by more than 2^8 (lazy
 // rescale; O and l carry the same stale max).  The N x N score matrix never
-// leaves the SM.  flashmatch3_kernel (v3) is the same pipeline fed by
-// cp.async loader warps, kept for comparison (FNL_FM_VERSION=3).
+// leaves the SM.
 // Measurements and the variants that lost: DESIGN.md section 7.
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -61,24 +60,13 @@ __device__ __forceinline__ uint64_t fm_desc(uint32_t saddr, uint32_t lbo, uint32
 constexpr uint32_t kIdescS = (1u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
 constexpr uint32_t kIdescPV = (1u << 4) | (1u << 16) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
 
-// Layouts (bytes; all core matrices are 8 rows x 16 B = 128 B contiguous):
-//   Q, K  [row][hd]   K-major:  (row/8)*1024 + (hd/8)*128 + (row%8)*16   LBO 128, SBO 1024
-//   V     [key][hd]   MN-major: (hd/8)*2048 + (key/8)*128 + (key%8)*16   LBO 128 (key groups), SBO 2048 (hd groups)
-//   P     [row][key]  K-major:  (row/8)*2048 + (key/8)*128 + (row%8)*16  LBO 128, SBO 2048
-__device__ __forceinline__ uint32_t off_qk(uint32_t row, uint32_t chunk) {
-    return (row >> 3) * 1024u + chunk * 128u + (row & 7u) * 16u;
-}
-__device__ __forceinline__ uint32_t off_v(uint32_t key, uint32_t chunk) {
-    return chunk * 2048u + (key >> 3) * 128u + (key & 7u) * 16u;
-}
+// P [row][key] (written by the softmax threads), K-major, no swizzle, core
+// matrices of 8 rows x 16 B: (row/8)*2048 + (key/8)*128 + (row%8)*16, LBO 128,
+// SBO 2048.  Q, K and V arrive as TMA SWIZZLE_128B boxes (see K7 v4 below).
 __device__ __forceinline__ uint32_t off_p(uint32_t row, uint32_t chunk) {
     return (row >> 3) * 2048u + chunk * 128u + (row & 7u) * 16u;
 }
 
-__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g, bool valid) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "r"(valid ? 16u : 0u)
-                 : "memory");
-}
 __device__ __forceinline__ void fence_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -129,9 +117,7 @@ struct FmArgs {
     int trace;
 };
 
-// ---------------------------------------------------------------- shared by v3 / v4
-constexpr uint32_t kKvStages = 4;  // K/V ring depth
-constexpr uint32_t kSmemFm2 = 2 * kTileQK + 2 * kKvStages * kTileQK + 2 * kTileP + 64;
+// ---------------------------------------------------------------- K7 shared
 
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
     uint32_t done;
@@ -143,271 +129,19 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
     return done != 0;
 }
 
-// one 128 x 64 tile loaded by ONE warp (32 x 16 B per step, 32 steps)
-template <bool kV>
-__device__ __forceinline__ void load_tile_warp(uint32_t sbase, const __half* g, uint64_t sn, uint32_t nvalid,
-                                               uint32_t part = 0, uint32_t parts = 1) {
-    const uint32_t lane = threadIdx.x & 31u;
-#pragma unroll 8
-    for (uint32_t combo = part; combo < 32u; combo += parts) {
-        const uint32_t chunk = (lane >> 3) + 4u * (combo & 1u);
-        const uint32_t row = (combo >> 1) * 8u + (lane & 7u);
-        const bool valid = row < nvalid;
-        const __half* src = g + (valid ? (uint64_t)row * sn + chunk * 8u : 0);
-        cp_async16(sbase + (kV ? off_v(row, chunk) : off_qk(row, chunk)), src, valid);
-    }
-}
-
-// ---------------------------------------------------------------- K7 v3
-// v2's critical path per (tile, block) was S_j ready -> row-max pass (TMEM
-// read 1) -> exp2 pass (TMEM read 2) -> P published -> only THEN S_{j+1}
-// issued (S has one TMEM buffer per tile), plus a per-block drain of the PV
-// partial into registers.  v3 reads S_j once (tcgen05.ld.x64 into 64
-// registers per thread, two threads per row), hands the S buffer back at
-// once (s_free) so S_{j+1} runs on the tensor core under this block's
-// exponentials, and keeps O in TMEM: PV_j accumulates into it, and the
-// softmax rescales O (tcgen05.ld / st of its 32 columns) only when a row max
-// grows by more than kRescaleLog2 (the P entries stay <= 2^kRescaleLog2, well
-// inside binary16; l and O carry the same stale max, so O/l is exact).
-// TMEM per tile t: S [256t, 256t+128), O [256t+128, 256t+192).
-constexpr uint32_t kLoadWarps3 = 3;  // 20 warps -> 5 per SM sub-partition -> 96 registers per thread
-constexpr uint32_t kFm3Threads = (16 + 1 + kLoadWarps3) * 32;
+// ---------------------------------------------------------------- K7 helpers
+// The softmax reads S_j once (tcgen05.ld.x64 into registers), hands the S
+// buffer back at once so S_{j+1} runs on the tensor core under this block's
+// exponentials, and keeps O in TMEM: PV_j accumulates into it, and O is
+// rescaled (tcgen05.ld / st) only when a row max grows by more than
+// kRescaleLog2 (P entries stay <= 2^kRescaleLog2, well inside binary16; l and O
+// carry the same stale max, so O/l is exact).
 constexpr float kRescaleLog2 = 8.0f;
 
 __device__ __forceinline__ void frag_st(uint32_t taddr, const Frag& f) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr), "r"(f.r[0]),"r"(f.r[1]),"r"(f.r[2]),"r"(f.r[3]),"r"(f.r[4]),"r"(f.r[5]),"r"(f.r[6]),"r"(f.r[7]),"r"(f.r[8]),"r"(f.r[9]),"r"(f.r[10]),"r"(f.r[11]),"r"(f.r[12]),"r"(f.r[13]),"r"(f.r[14]),"r"(f.r[15]),"r"(f.r[16]),"r"(f.r[17]),"r"(f.r[18]),"r"(f.r[19]),"r"(f.r[20]),"r"(f.r[21]),"r"(f.r[22]),"r"(f.r[23]),"r"(f.r[24]),"r"(f.r[25]),"r"(f.r[26]),"r"(f.r[27]),"r"(f.r[28]),"r"(f.r[29]),"r"(f.r[30]),"r"(f.r[31]) : "memory");
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-
-__global__ void __launch_bounds__(kFm3Threads, 1) flashmatch3_kernel(FmArgs a) {
-    __shared__ float red[2][2][kBlockQ];  // [tile][column half][row] partial maxima / sums
-    extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ uint32_t tmem_slot;
-    __shared__ __align__(8) uint64_t s_full[2], s_free[2], p_full[2], o_full[2];
-    __shared__ __align__(8) uint64_t kv_full[kKvStages], kv_empty[kKvStages];
-    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
-    const uint32_t q0 = blockIdx.x * 2 * kBlockQ, h = blockIdx.y, b = blockIdx.z;
-    FM_STAMP(0);
-    const uint32_t sQ = smem_addr(smem);
-    const uint32_t sK = sQ + 2 * kTileQK, sV = sK + kKvStages * kTileQK, sP = sV + kKvStages * kTileQK;
-    uint8_t* pP0 = smem + (2 + 2 * kKvStages) * kTileQK;
-    const uint32_t nblk = (a.nkv + kBlockK - 1) / kBlockK;
-
-    if (tid == 0) {
-        for (int t = 0; t < 2; ++t) {
-            mbar_init(&s_full[t], 1);
-            mbar_init(&s_free[t], 8);  // the tile's 8 softmax warps
-            mbar_init(&p_full[t], 8);
-            mbar_init(&o_full[t], 1);
-        }
-        for (uint32_t st = 0; st < kKvStages; ++st) {
-            mbar_init(&kv_full[st], 32 * kLoadWarps3);  // one cp.async.mbarrier.arrive.noinc per loader lane
-            mbar_init(&kv_empty[st], 1);  // one tcgen05.commit after the block's last PV
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_slot)),
-                     "r"(512u));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = tmem_slot;
-    FM_STAMP(34);
-
-    if (warp >= 17) {
-        // ---------------- loader (as v2)
-        const __half* gq = a.q + b * a.q_sb + h * a.q_sh + (uint64_t)q0 * a.q_sn;
-        const __half* gk = a.k + b * a.k_sb + h * a.k_sh;
-        const __half* gv = a.v + b * a.v_sb + h * a.v_sh;
-        const uint32_t qvalid = a.nq - q0;
-        const uint32_t part = warp - 17;
-        load_tile_warp<false>(sQ, gq, a.q_sn, qvalid, part, kLoadWarps3);
-        if (qvalid > kBlockQ)
-            load_tile_warp<false>(sQ + kTileQK, gq + (uint64_t)kBlockQ * a.q_sn, a.q_sn, qvalid - kBlockQ, part,
-                                  kLoadWarps3);
-        for (uint32_t blk = 0; blk < nblk; ++blk) {
-            const uint32_t st = blk % kKvStages;
-            mbar_wait(&kv_empty[st], ((blk / kKvStages) & 1u) ^ 1u);
-            load_tile_warp<false>(sK + st * kTileQK, gk + (uint64_t)blk * kBlockK * a.k_sn, a.k_sn,
-                                  a.nkv - blk * kBlockK, part, kLoadWarps3);
-            load_tile_warp<true>(sV + st * kTileQK, gv + (uint64_t)blk * kBlockK * a.v_sn, a.v_sn,
-                                 a.nkv - blk * kBlockK, part, kLoadWarps3);
-            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(&kv_full[st]))
-                         : "memory");
-        }
-    } else if (warp == 16) {
-        // ---------------- MMA warp: S_t(j+1) as soon as S_t(j) is drained,
-        // PV_t(j) as soon as P_t(j) is published
-        auto kv_ready = [&](uint32_t blk) {
-            mbar_wait(&kv_full[blk % kKvStages], (blk / kKvStages) & 1u);
-            fence_async_smem();
-        };
-        auto issue_s = [&](uint32_t t, uint32_t blk) {
-            tc_fence_after();
-            if (elect_one()) {
-                const uint32_t kb = sK + (blk % kKvStages) * kTileQK, qb = sQ + t * kTileQK;
-#pragma unroll
-                for (uint32_t ks = 0; ks < kHd / 16; ++ks)
-                    tc_mma_f16(tmem + t * 256u, fm_desc(qb + ks * 256u, 128u, 1024u),
-                               fm_desc(kb + ks * 256u, 128u, 1024u), kIdescS, ks > 0 ? 1u : 0u);
-                tc_commit(&s_full[t]);
-            }
-            __syncwarp();
-        };
-        kv_ready(0);  // also covers Q (issued before K0/V0 by the same lanes)
-        issue_s(0, 0);
-        issue_s(1, 0);
-        uint32_t js[2] = {1u, 1u}, jp[2] = {0u, 0u};
-        while (jp[0] < nblk || jp[1] < nblk) {
-#pragma unroll
-            for (uint32_t t = 0; t < 2; ++t) {
-                if (js[t] < nblk && mbar_test(&s_free[t], (js[t] - 1u) & 1u)) {
-                    kv_ready(js[t]);  // the stage cannot have been refilled: its PVs are not issued yet
-                    issue_s(t, js[t]);
-                    ++js[t];
-                }
-                const uint32_t j = jp[t];
-                if (j < nblk && mbar_test(&p_full[t], j & 1u)) {
-                    tc_fence_after();
-                    const bool last_reader = jp[t ^ 1u] > j;  // the other tile's PV_j is already issued
-                    if (elect_one()) {
-                        const uint32_t vb = sV + (j % kKvStages) * kTileQK, pb = sP + t * kTileP;
-#pragma unroll
-                        for (uint32_t ks = 0; ks < kBlockK / 16; ++ks)
-                            tc_mma_f16(tmem + t * 256u + 128u, fm_desc(pb + ks * 256u, 128u, 2048u),
-                                       fm_desc(vb + ks * 256u, 128u, 2048u), kIdescPV, (ks | j) > 0 ? 1u : 0u);
-                        tc_commit(&o_full[t]);
-                        if (last_reader) tc_commit(&kv_empty[j % kKvStages]);
-                    }
-                    __syncwarp();
-                    jp[t] = j + 1;
-                }
-            }
-        }
-    } else {
-        // ---------------- softmax warpgroup t: warps 8t..8t+7; warp w reads TMEM
-        // lane quadrant w%4 and column half hf = (w/4)%2: two threads per query
-        // row, 64 key columns and 32 O columns each
-        const uint32_t t = warp >> 3, hf = (warp >> 2) & 1u, row = ((warp & 3u) << 5) | lane;
-        const uint32_t lane_base = ((warp & 3u) * 32u) << 16;
-        const uint32_t tS = tmem + lane_base + t * 256u, tO = tS + 128u + 32u * hf;
-        uint8_t* pP = pP0 + t * kTileP;
-        float m = -INFINITY, l = 0.0f;
-        const float sl2 = a.scale_log2;
-        auto tile_sync = [&]() { asm volatile("bar.sync %0, 256;" ::"r"(1u + t) : "memory"); };
-        for (uint32_t j = 0; j < nblk; ++j) {
-            mbar_wait(&s_full[t], j & 1u);
-            if (t == 0) FM_STAMP(3 + j);
-            tc_fence_after();
-            Frag f0, f1;
-            frag_ld64(tS + hf * 64u, f0, f1);
-            frag_wait2(f0, f1);
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&s_free[t]);  // S_t(j) is in registers: S_t(j+1) may overwrite it
-            const uint32_t kvalid = a.nkv - j * kBlockK;
-            if (kvalid < kBlockK) {
-#pragma unroll
-                for (uint32_t i = 0; i < 32; ++i) {
-                    if (hf * 64u + i >= kvalid) f0.r[i] = __float_as_uint(-INFINITY);
-                    if (hf * 64u + 32u + i >= kvalid) f1.r[i] = __float_as_uint(-INFINITY);
-                }
-            }
-            float r4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-            for (uint32_t i = 0; i < 32; i += 8)
-#pragma unroll
-                for (uint32_t u = 0; u < 4; ++u) {
-                    r4[u] = max3(r4[u], __uint_as_float(f0.r[i + 2 * u]), __uint_as_float(f0.r[i + 2 * u + 1]));
-                    r4[u] = max3(r4[u], __uint_as_float(f1.r[i + 2 * u]), __uint_as_float(f1.r[i + 2 * u + 1]));
-                }
-            float mx = fmaxf(fmaxf(r4[0], r4[1]), fmaxf(r4[2], r4[3]));
-            red[t][hf][row] = mx;
-            tile_sync();
-            mx = fmaxf(mx, red[t][hf ^ 1u][row]);
-            tile_sync();  // both halves read before either writes the next value
-            // lazy rescale: keep the stale max unless the row max grew by more
-            // than 2^kRescaleLog2 (both threads of a row decide identically)
-            const float mc = mx * sl2;
-            const bool grow = mc > m + kRescaleLog2;
-            const float m_new = grow ? mc : m;
-            const float alpha = (grow && j > 0) ? ex2(m - m_new) : 1.0f;
-            if (t == 0 && j < 8) FM_STAMP(10 + j);
-            // PV_t(j-1) must have retired before P is overwritten or O rescaled
-            if (j > 0) {
-                mbar_wait(&o_full[t], (j - 1) & 1u);
-                tc_fence_after();
-            }
-            float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-            for (uint32_t c = 0; c < 2; ++c) {
-                const Frag& f = c ? f1 : f0;
-                const uint32_t col0 = hf * 64u + c * 32u;
-#pragma unroll
-                for (uint32_t q = 0; q < 4; ++q) {
-                    float p[8];
-#pragma unroll
-                    for (uint32_t i = 0; i < 8; ++i) p[i] = ex2(fmaf(__uint_as_float(f.r[q * 8 + i]), sl2, -m_new));
-                    acc[q] += ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
-                    uint4 w;
-                    w.x = pack_half2_rn(p[0], p[1]);
-                    w.y = pack_half2_rn(p[2], p[3]);
-                    w.z = pack_half2_rn(p[4], p[5]);
-                    w.w = pack_half2_rn(p[6], p[7]);
-                    *reinterpret_cast<uint4*>(pP + off_p(row, col0 / 8u + q)) = w;
-                }
-            }
-            if (__any_sync(0xFFFFFFFFu, alpha != 1.0f)) {  // warp-collective TMEM round trip of O
-                Frag o;
-                frag_ld(tO, o);
-                frag_wait1(o);
-#pragma unroll
-                for (uint32_t i = 0; i < 32; ++i) o.r[i] = __float_as_uint(__uint_as_float(o.r[i]) * alpha);
-                frag_st(tO, o);
-                tmem_st_wait();
-            }
-            tc_fence_before();
-            fence_async_smem();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&p_full[t]);  // P_t(j) written, O_t rescaled
-            if (t == 0) FM_STAMP(20 + j);
-            l = l * alpha + ((acc[0] + acc[1]) + (acc[2] + acc[3]));  // partial: this thread's columns
-            m = m_new;
-        }
-        mbar_wait(&o_full[t], (nblk - 1) & 1u);
-        tc_fence_after();
-        Frag o;
-        frag_ld(tO, o);
-        frag_wait1(o);
-        red[t][hf][row] = l;
-        tile_sync();
-        l += red[t][hf ^ 1u][row];
-        const uint32_t grow_ = q0 + t * kBlockQ + row;
-        if (grow_ < a.nq) {
-            const float inv = 1.0f / l;
-            __half* go = a.o + b * a.o_sb + h * a.o_sh + (uint64_t)grow_ * a.o_sn + hf * 32u;
-#pragma unroll
-            for (uint32_t c = 0; c < kHd / 16; ++c) {
-                uint4 w;
-                w.x = pack_half2_rn(__uint_as_float(o.r[c * 8 + 0]) * inv, __uint_as_float(o.r[c * 8 + 1]) * inv);
-                w.y = pack_half2_rn(__uint_as_float(o.r[c * 8 + 2]) * inv, __uint_as_float(o.r[c * 8 + 3]) * inv);
-                w.z = pack_half2_rn(__uint_as_float(o.r[c * 8 + 4]) * inv, __uint_as_float(o.r[c * 8 + 5]) * inv);
-                w.w = pack_half2_rn(__uint_as_float(o.r[c * 8 + 6]) * inv, __uint_as_float(o.r[c * 8 + 7]) * inv);
-                *reinterpret_cast<uint4*>(go + c * 8) = w;
-            }
-        }
-    }
-    FM_STAMP(63);
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 0) {
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
-    }
-}
 
 // ---------------------------------------------------------------- K7 v4
 // v3 with TMA: Q, K_j and V_j arrive by cp.async.bulk.tensor (one elected
@@ -710,7 +444,6 @@ int flashmatch_forward(fnl_context* ctx, const fnl_attention_desc& d) {
         FNL_CUDA_TRY(cudaGetDevice(&dev));
         std::lock_guard<std::mutex> lk(fm_attr_mu);
         if (dev < 0 || dev >= 64 || !fm_attr_done[dev]) {
-            FNL_CUDA_TRY(cudaFuncSetAttribute(flashmatch3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFm2));
             FNL_CUDA_TRY(cudaFuncSetAttribute(flashmatch4_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFm4));
             FNL_CUDA_TRY(cudaFuncSetAttribute(flashmatch4_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFm4));
             if (dev >= 0 && dev < 64) fm_attr_done[dev] = true;
@@ -733,10 +466,7 @@ int flashmatch_forward(fnl_context* ctx, const fnl_attention_desc& d) {
     a.trace = trace;
     cudaStream_t s = ctx_stream(ctx);
     ProfScope prof(ctx, FNL_KCLASS_ATTN);
-    // v4 (TMA loads) is the product kernel; FNL_FM_VERSION=3 selects the
-    // cp.async-loader v3 for comparison
-    static const int ver = getenv("FNL_FM_VERSION") ? atoi(getenv("FNL_FM_VERSION")) : 4;
-    if (ver == 4) {
+    {
         // TMA tensor maps of Q, K, V viewed as [batch][heads][rows][64] binary16
         static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
         if (!encode) {
@@ -780,9 +510,6 @@ int flashmatch_forward(fnl_context* ctx, const fnl_attention_desc& d) {
             flashmatch4_kernel<1><<<grid4, (8 * 1 + 2) * 32, kSmemFm4, s>>>(a, tq, tk, tv);
         else
             flashmatch4_kernel<2><<<grid4, (8 * 2 + 2) * 32, kSmemFm4, s>>>(a, tq, tk, tv);
-    } else {
-        flashmatch3_kernel<<<dim3((d.nq + 2 * kBlockQ - 1) / (2 * kBlockQ), d.heads, d.batch), kFm3Threads,
-                             kSmemFm2, s>>>(a);
     }
     FNL_CUDA_TRY(cudaGetLastError());
     ctx_count_launches(ctx, 1);

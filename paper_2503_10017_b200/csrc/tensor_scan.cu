@@ -2,22 +2,25 @@
 //
 //   K1 pack     fp32 map -> binary16 rows (RNE + saturation, counted) in the UMMA
 //               canonical K-major layout, row norms, per-map max norm.
+//   K2p plan    per-pass work lists from the device state (no host round trip).
 //   K2 gather   active query rows -> contiguous 256-row query tile pairs, plus the
-//               per-row certification margin.
-//   K3 scan     one CTA = 256 queries x a range of 128-target tiles.  Warp 0
-//               streams target tiles global->smem with cp.async.bulk through an
-//               8-deep mbarrier ring; warp 1 (one thread) issues
-//               tcgen05.mma.cta_group::1.kind::f16 (M=128, N=128, K=16, two
-//               query tiles x two K steps per target tile) into a double-buffered
-//               fp32 TMEM accumulator (4 x 128 columns = all 512); warps 2-9
-//               drain TMEM with tcgen05.ld, free the buffer at once, and keep a
-//               running (best, index, second) per query row in registers.  The
-//               score matrix never leaves the SM.
-//   K3b merge   per row over target splits; a row is certified when
-//               best - second > margin, i.e. the fp32 tensor-core winner is
-//               provably the reference FMA-chain winner.
-//   K4' rescan  the uncertified rows (near ties, ~0.1%) re-run the reference FMA
-//               chain over every target; lowest index on exact ties.
+//               per-row one-sided certification margin of the resolve mode.
+//   K3 scan     persistent, one CTA per SM: 256 queries x a range of 256-target
+//               tiles.  Warp 0 streams target tiles global->smem with
+//               cp.async.bulk through a 4-deep mbarrier ring; warps 1-2 (one
+//               per query tile) issue tcgen05.mma.cta_group::1.kind::f16 (M128
+//               N128 K16, two K steps) into four 128-column fp32 TMEM
+//               accumulator chains (query tile x 128-target half = all 512
+//               columns); 16 epilogue warps drain TMEM with tcgen05.ld and keep,
+//               per query row, the top-4 maxima of 64-target sub-tiles (with the
+//               first three sub-tile ids) in registers.  The score matrix never
+//               leaves the SM.
+//   K3b merge   per row over target splits: resolve the best sub-tile with the
+//               reference FMA chain in the mode's arithmetic, close the row when
+//               the exact winner beats the next bound by the margin, else the
+//               second and third sub-tiles.
+//   K4' rescan  rows still open (four sub-tiles inside the margin) re-run the
+//               exact chain over every target; lowest index on exact ties.
 //
 // Score convention: larger is better.  dot: s = q.t (dist = -s).  l2: the
 // packed target carries -|t|^2/2 as two binary16 terms (hi + lo) in channels
@@ -295,7 +298,7 @@ __global__ void gather_kernel(GatherArgs a) {
 
 // ---------------------------------------------------------------- K3 scan
 // A work unit = one query tile pair (256 gathered rows) x a contiguous range of
-// 128-target tiles.  The kernel is persistent: CTA b runs units b, b+G, b+2G...
+// 256-target tiles.  The kernel is persistent: CTA b runs units b, b+G, b+2G...
 // (static round robin over equal-sized units), so TMEM allocation, barrier
 // setup and the pipeline prologue are paid once per SM, and the query tile of
 // the next unit is fetched into the second A buffer while the current unit is
@@ -318,17 +321,18 @@ struct TcArgs {
     unsigned long long* trace;  // [4][4096] clock64 stamps (debug & 16)
 };
 
-// K3 structure (v8; measured on this B200 with the clock traces of
-// FNL_TC_DEBUG=16, see DESIGN.md):
-//  * a target tile is 256 targets (16 KB, one cp.async.bulk); each query tile
-//    qt (128 rows) owns one TMEM accumulator buffer of 256 fp32 columns
-//    (columns 256*qt), filled by two tcgen05.mma M128 N256 K16 (the 24
-//    channels + norm terms padded to K=32) issued by its own issuer warp
-//    (warp 1 + qt), so each barrier has exactly one producer and one consumer
-//    chain and an issuer only ever waits on "B landed" + "my buffer drained";
-//  * all 16 epilogue warps drain every buffer: warp = (64-column quarter,
-//    TMEM lane quadrant w%4); two tcgen05.ld.x32, release, then compare, and
-//    the other query tile's buffer is refilled while they compare.
+// K3 structure (v11; measured on this B200 with the clock traces of
+// FNL_TC_DEBUG=16, see DESIGN.md section 4):
+//  * a target tile is 256 targets (16 KB, one cp.async.bulk) in a 4-stage ring;
+//  * query tile qt (128 rows) owns TMEM columns [256 qt, 256 qt + 256), split
+//    into two 128-target halves that are independent accumulator chains; its
+//    issuer warp (1 + qt) waits "B landed" and "this half drained", then issues
+//    two M128 N128 K16 MMAs (the 24 channels + norm terms padded to K = 32)
+//    and one commit per half, so every mbarrier has one producer chain and one
+//    consumer chain;
+//  * 16 epilogue warps = (query tile, half, TMEM lane quadrant w%4): warps 3-10
+//    drain query tile 0, warps 11-18 query tile 1, so one tile's TMEM loads
+//    overlap the other tile's compares.
 constexpr uint32_t kBTileRows = kTargetTileRows;                // 256 targets per B tile
 constexpr uint32_t kBTileBytes = kBTileRows * kPackRowBytes;  // 16 KB
 constexpr int kStages = 4;
