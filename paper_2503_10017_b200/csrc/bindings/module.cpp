@@ -259,21 +259,32 @@ PYBIND11_MODULE(_fastnn, m) {
           },
           py::arg("height"), py::arg("width"), py::arg("k") = 0, py::arg("stride") = 8);
 
+    // The maps go straight from the numpy buffers to the device (no FeatureMap
+    // copy); finiteness is validated on the GPU with the reference's message.
     m.def("mutual_nn_exact",
           [](const F32& D1, const F32& D2, const std::string& metric) {
-              const auto a = to_map(D1), b = to_map(D2);
+              check_shape3(D1, "mutual_nn_exact");
+              check_shape3(D2, "mutual_nn_exact");
+              if (D1.shape(2) != D2.shape(2)) {
+                  (void)to_map(D1);  // the reference validates both maps before the dims
+                  (void)to_map(D2);
+                  throw std::invalid_argument("mutual_nn_exact: descriptor dim mismatch (" +
+                                              std::to_string(D1.shape(2)) + " vs " + std::to_string(D2.shape(2)) +
+                                              ")");
+              }
               const auto mt = fastnn::metric_from_string(metric);
-              fastnn::MatchSet s;
+              const std::uint32_t h1 = std::uint32_t(D1.shape(0)), w1 = std::uint32_t(D1.shape(1));
+              std::vector<std::uint32_t> pairs(2 * std::size_t(h1) * w1 + 2);
+              std::uint32_t n = 0;
               {
                   py::gil_scoped_release nogil;
-                  s = fastnn::mutual_nn_exact(a, b, mt);
+                  fastnn::b200::check(fnl_mutual_nn(
+                      fastnn::b200::context(), D1.data(), h1, w1, D2.data(), std::uint32_t(D2.shape(0)),
+                      std::uint32_t(D2.shape(1)), std::uint32_t(D1.shape(2)),
+                      mt == fastnn::DistanceMetric::SquaredL2 ? FNL_METRIC_L2 : FNL_METRIC_DOT, pairs.data(), &n));
               }
-              U32Array out({py::ssize_t(s.pairs.size()), py::ssize_t(2)});
-              auto v = out.mutable_unchecked<2>();
-              for (py::ssize_t r = 0; r < py::ssize_t(s.pairs.size()); ++r) {
-                  v(r, 0) = s.pairs[r].i;
-                  v(r, 1) = s.pairs[r].j;
-              }
+              U32Array out({py::ssize_t(n), py::ssize_t(2)});
+              std::memcpy(out.mutable_data(), pairs.data(), std::size_t(n) * 8);
               return out;
           },
           py::arg("D1"), py::arg("D2"), py::arg("metric") = "l2");

@@ -1235,41 +1235,6 @@ extern "C" int fnl_reciprocal_match_batch(fnl_context* ctx, uint32_t npairs, con
     return st;
 }
 
-// Dense mutual NN on the tensor backend: the K3 scan
-// in both directions plus the mutual filter.  The result equals
-// mutual_nn_exact (src/reciprocal.cpp:82-95) run on binary16-rounded maps.
-extern "C" int fnl_mutual_nn_tensor(fnl_context* ctx, const float* h_d1, uint32_t h1, uint32_t w1,
-                                    const float* h_d2, uint32_t h2, uint32_t w2, uint32_t dim, int metric,
-                                    uint32_t* h_pairs, uint32_t* n_pairs) {
-    TRY(check_device(ctx));
-    if (!valid_metric(metric)) return fail(FNL_EINVAL, "mutual_nn_tensor: bad metric");
-    const uint32_t p1 = h1 * w1, p2 = h2 * w2;
-    if (p1 == 0 || p2 == 0 || dim == 0) return fail(FNL_EINVAL, "mutual_nn_tensor: empty map");
-    const bool l2 = metric == FNL_METRIC_L2;
-    float *d1, *d2;
-    uint32_t *fwd, *bwd, *pairs, *cnt;
-    TRY(dev_arr(ctx, "mt.d1", (size_t)p1 * dim, &d1));
-    TRY(dev_arr(ctx, "mt.d2", (size_t)p2 * dim, &d2));
-    TRY(dev_arr(ctx, "mt.fwd", p1, &fwd));
-    TRY(dev_arr(ctx, "mt.bwd", p2, &bwd));
-    TRY(dev_arr(ctx, "mt.pairs", (size_t)2 * p1 + 2, &pairs));
-    TRY(dev_arr(ctx, "mt.cnt", 1, &cnt));
-    cudaStream_t s = ctx->stream;
-    FNL_CUDA_TRY(cudaMemcpyAsync(d1, h_d1, (size_t)p1 * dim * 4, cudaMemcpyHostToDevice, s));
-    FNL_CUDA_TRY(cudaMemcpyAsync(d2, h_d2, (size_t)p2 * dim * 4, cudaMemcpyHostToDevice, s));
-    TRY(fnl::tensor_nn_dense(ctx, d1, p1, d2, p2, dim, l2, fwd, nullptr));
-    TRY(fnl::tensor_nn_dense(ctx, d2, p2, d1, p1, dim, l2, bwd, nullptr));
-    FNL_CUDA_TRY(fnl::launch_mutual_filter(fwd, bwd, p1, pairs, cnt, s));
-    uint32_t n = 0;
-    FNL_CUDA_TRY(cudaMemcpyAsync(&n, cnt, 4, cudaMemcpyDeviceToHost, s));
-    FNL_CUDA_TRY(cudaStreamSynchronize(s));
-    if (n && h_pairs) FNL_CUDA_TRY(cudaMemcpyAsync(h_pairs, pairs, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
-    FNL_CUDA_TRY(cudaStreamSynchronize(s));
-    timing_harvest(ctx);
-    if (n_pairs) *n_pairs = n;
-    return FNL_OK;
-}
-
 extern "C" int fnl_confidence_compact_device(fnl_context* ctx, uint32_t npairs, const float* d_d1,
                                              const float* d_d2, uint32_t h, uint32_t w, uint32_t dim, int metric,
                                              float max_distance, uint32_t* d_pairs, uint32_t* d_n_pairs,
@@ -1312,66 +1277,112 @@ extern "C" int fnl_tensor_selftest(fnl_context* ctx, const float* h_q, const flo
 }
 
 // ============================================================== mutual NN
-extern "C" int fnl_mutual_nn(fnl_context* ctx, const float* h_d1, uint32_t h1, uint32_t w1,
-                             const float* h_d2, uint32_t h2, uint32_t w2, uint32_t dim, int metric,
-                             uint32_t* h_pairs, uint32_t* n_pairs) {
+namespace {
+
+// Dense mutual NN (src/reciprocal.cpp:82-95): NN of every D1 pixel in D2 and
+// of every D2 pixel in D1, then the pairs that agree.  Tensor route: both maps
+// packed once, both directions back to back on the device (tensor_mutual_dense),
+// resolved in full precision (mutual_nn_exact) or on the binary16-rounded rows
+// (mutual_nn_tensor); else the CUDA-core exact scan K4.
+int mutual_nn_run(fnl_context* ctx, const char* who, const float* h_d1, uint32_t h1, uint32_t w1,
+                  const float* h_d2, uint32_t h2, uint32_t w2, uint32_t dim, int metric, bool rounded,
+                  uint32_t* h_pairs, uint32_t* n_pairs) {
     TRY(check_device(ctx));
-    if (!valid_metric(metric)) return fail(FNL_EINVAL, "mutual_nn_exact: bad metric");
+    if (!valid_metric(metric)) return fail(FNL_EINVAL, std::string(who) + ": bad metric");
     const uint32_t p1 = h1 * w1, p2 = h2 * w2;
-    if (p1 == 0 || p2 == 0 || dim == 0) return fail(FNL_EINVAL, "mutual_nn_exact: empty map");
+    if (p1 == 0 || p2 == 0 || dim == 0) return fail(FNL_EINVAL, std::string(who) + ": empty map");
     const bool l2 = metric == FNL_METRIC_L2;
     float *d1, *d2;
     uint32_t *fwd, *bwd, *pairs, *cnt;
-    unsigned long long *k1, *k2;
     TRY(dev_arr(ctx, "mu.d1", (size_t)p1 * dim, &d1));
     TRY(dev_arr(ctx, "mu.d2", (size_t)p2 * dim, &d2));
     TRY(dev_arr(ctx, "mu.fwd", p1, &fwd));
     TRY(dev_arr(ctx, "mu.bwd", p2, &bwd));
-    TRY(dev_arr(ctx, "mu.k1", p1, &k1));
-    TRY(dev_arr(ctx, "mu.k2", p2, &k2));
     TRY(dev_arr(ctx, "mu.pairs", (size_t)2 * p1 + 2, &pairs));
     TRY(dev_arr(ctx, "mu.cnt", 1, &cnt));
     cudaStream_t s = ctx->stream;
     FNL_CUDA_TRY(cudaMemcpyAsync(d1, h_d1, (size_t)p1 * dim * 4, cudaMemcpyHostToDevice, s));
     FNL_CUDA_TRY(cudaMemcpyAsync(d2, h_d2, (size_t)p2 * dim * 4, cudaMemcpyHostToDevice, s));
-    FNL_CUDA_TRY(cudaMemsetAsync(k1, 0xFF, (size_t)p1 * 8, s));
-    FNL_CUDA_TRY(cudaMemsetAsync(k2, 0xFF, (size_t)p2 * 8, s));
-    auto pass = [&](const float* q, uint32_t nq, const float* t, uint32_t nt,
-                    unsigned long long* keys, uint32_t* out) -> int {
-        if (!force_cuda_core()) {  // tensor route, full-precision resolution
-            bool routed = false;
-            TRY(fnl::tensor_nn_dense(ctx, q, nq, t, nt, dim, l2, out, nullptr, fnl::kResolveFull, &routed));
-            if (routed) return FNL_OK;
+    bool routed = false, checked = false;
+    if (rounded || !force_cuda_core()) {
+        // (the pack also finds non-finite inputs: validated like the
+        // reference FeatureMap, D1 first)
+        unsigned long long hb[2] = {~0ull, ~0ull};
+        TRY(fnl::tensor_mutual_dense(ctx, d1, p1, d2, p2, dim, l2, rounded ? fnl::kResolveRounded : fnl::kResolveFull,
+                                     fwd, bwd, &routed, hb));
+        if (hb[0] != ~0ull) return fail(FNL_EINVAL, nonfinite_msg(hb[0]));
+        if (hb[1] != ~0ull) return fail(FNL_EINVAL, nonfinite_msg(hb[1]));
+        checked = dim + (l2 ? 2u : 0u) <= fnl::kPackK;
+    }
+    if (!routed) {
+        unsigned long long *k1, *k2, *bad;
+        TRY(dev_arr(ctx, "mu.k1", p1, &k1));
+        TRY(dev_arr(ctx, "mu.k2", p2, &k2));
+        TRY(dev_arr(ctx, "mu.bad", 1, &bad));
+        FNL_CUDA_TRY(cudaMemsetAsync(k1, 0xFF, (size_t)p1 * 8, s));
+        FNL_CUDA_TRY(cudaMemsetAsync(k2, 0xFF, (size_t)p2 * 8, s));
+        FNL_CUDA_TRY(cudaMemsetAsync(bad, 0xFF, 8, s));
+        Prepared P1, P2;
+        TRY(prepare_maps(ctx, "mu.p1", d1, 1, p1, dim, rounded, !checked, &P1, bad));
+        if (!checked) {
+            unsigned long long hb = ~0ull;
+            FNL_CUDA_TRY(cudaMemcpyAsync(&hb, bad, 8, cudaMemcpyDeviceToHost, s));
+            FNL_CUDA_TRY(cudaStreamSynchronize(s));
+            if (hb != ~0ull) return fail(FNL_EINVAL, nonfinite_msg(hb));
         }
-        fnl::ScanArgs sa{};
-        sa.qmap = q;
-        sa.qcount_const = nq;
-        sa.tmap = t;
-        sa.nt = nt;
-        sa.dim = dim;
-        sa.keys = keys;
-        sa.keys_pair_stride = nq;
-        fnl::FinalizeArgs fa{};
-        fa.keys = keys;
-        fa.keys_pair_stride = nq;
-        fa.qcount_const = nq;
-        fa.nearest = out;
-        fa.nearest_pair_stride = nq;
-        fa.dot = !l2;
-        return exact_nn(ctx, sa, nq, 1, l2, false, fa);
-    };
-    TRY(pass(d1, p1, d2, p2, k1, fwd));
-    TRY(pass(d2, p2, d1, p1, k2, bwd));
+        TRY(prepare_maps(ctx, "mu.p2", d2, 1, p2, dim, rounded, !checked, &P2, bad));
+        if (!checked) {
+            unsigned long long hb = ~0ull;
+            FNL_CUDA_TRY(cudaMemcpyAsync(&hb, bad, 8, cudaMemcpyDeviceToHost, s));
+            FNL_CUDA_TRY(cudaStreamSynchronize(s));
+            if (hb != ~0ull) return fail(FNL_EINVAL, nonfinite_msg(hb));
+        }
+        auto pass = [&](const float* q, uint32_t nq, const float* t, uint32_t nt, unsigned long long* keys,
+                        uint32_t* out) -> int {
+            fnl::ScanArgs sa{};
+            sa.qmap = q;
+            sa.qcount_const = nq;
+            sa.tmap = t;
+            sa.nt = nt;
+            sa.dim = dim;
+            sa.keys = keys;
+            sa.keys_pair_stride = nq;
+            fnl::FinalizeArgs fa{};
+            fa.keys = keys;
+            fa.keys_pair_stride = nq;
+            fa.qcount_const = nq;
+            fa.nearest = out;
+            fa.nearest_pair_stride = nq;
+            fa.dot = !l2;
+            return exact_nn(ctx, sa, nq, 1, l2, false, fa);
+        };
+        TRY(pass(P1.data, p1, P2.data, p2, k1, fwd));
+        TRY(pass(P2.data, p2, P1.data, p1, k2, bwd));
+    }
     FNL_CUDA_TRY(fnl::launch_mutual_filter(fwd, bwd, p1, pairs, cnt, s));
     uint32_t n = 0;
     FNL_CUDA_TRY(cudaMemcpyAsync(&n, cnt, 4, cudaMemcpyDeviceToHost, s));
     FNL_CUDA_TRY(cudaStreamSynchronize(s));
-    if (n && h_pairs)
-        FNL_CUDA_TRY(cudaMemcpyAsync(h_pairs, pairs, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+    if (n && h_pairs) FNL_CUDA_TRY(cudaMemcpyAsync(h_pairs, pairs, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
     FNL_CUDA_TRY(cudaStreamSynchronize(s));
     timing_harvest(ctx);
     if (n_pairs) *n_pairs = n;
     return FNL_OK;
+}
+
+}  // namespace
+
+extern "C" int fnl_mutual_nn(fnl_context* ctx, const float* h_d1, uint32_t h1, uint32_t w1,
+                             const float* h_d2, uint32_t h2, uint32_t w2, uint32_t dim, int metric,
+                             uint32_t* h_pairs, uint32_t* n_pairs) {
+    return mutual_nn_run(ctx, "mutual_nn_exact", h_d1, h1, w1, h_d2, h2, w2, dim, metric, false, h_pairs, n_pairs);
+}
+
+// Dense mutual NN on the binary16-rounded maps (the tensor backend's contract).
+extern "C" int fnl_mutual_nn_tensor(fnl_context* ctx, const float* h_d1, uint32_t h1, uint32_t w1,
+                                    const float* h_d2, uint32_t h2, uint32_t w2, uint32_t dim, int metric,
+                                    uint32_t* h_pairs, uint32_t* n_pairs) {
+    return mutual_nn_run(ctx, "mutual_nn_tensor", h_d1, h1, w1, h_d2, h2, w2, dim, metric, true, h_pairs, n_pairs);
 }
 
 // ---------------------------------------------------------------- peer memory

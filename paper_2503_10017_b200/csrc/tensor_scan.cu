@@ -1513,6 +1513,55 @@ int tensor_nn_dense(fnl_context* ctx, const float* d_q, uint32_t nq, const float
                           nullptr, nullptr, &rs);
 }
 
+int tensor_mutual_dense(fnl_context* ctx, const float* d1, uint32_t p1, const float* d2, uint32_t p2, uint32_t dim,
+                        bool l2, int mode, uint32_t* d_fwd, uint32_t* d_bwd, bool* routed,
+                        unsigned long long* bad_out) {
+    *routed = false;
+    if (dim == 0 || dim + (l2 ? 2u : 0u) > kPackK) return FNL_OK;
+    unsigned long long* scratch;
+    TRY(ws_arr(ctx, "tc.mu.scratch", 4, &scratch));
+    cudaStream_t s = ctx_stream(ctx);
+    FNL_CUDA_TRY(cudaMemsetAsync(scratch, 0xFF, 16, s));
+    FNL_CUDA_TRY(cudaMemsetAsync(scratch + 2, 0, 16, s));
+    // each map is packed ONCE and serves as query side in one direction and
+    // target side in the other (the gather rewrites the norm channels)
+    PackedMaps M1, M2;
+    TRY(tensor_pack(ctx, "tc.mu.1", d1, 1, p1, dim, l2, scratch, scratch + 2, &M1));
+    TRY(tensor_pack(ctx, "tc.mu.2", d2, 1, p2, dim, l2, scratch + 1, scratch + 3, &M2));
+    unsigned long long h[4];
+    float n[2];
+    FNL_CUDA_TRY(cudaMemcpyAsync(h, scratch, 32, cudaMemcpyDeviceToHost, s));
+    FNL_CUDA_TRY(cudaMemcpyAsync(&n[0], M1.max_norm, 4, cudaMemcpyDeviceToHost, s));
+    FNL_CUDA_TRY(cudaMemcpyAsync(&n[1], M2.max_norm, 4, cudaMemcpyDeviceToHost, s));
+    FNL_CUDA_TRY(cudaStreamSynchronize(s));
+    if (bad_out) bad_out[0] = h[0], bad_out[1] = h[1];
+    if (!tensor_route_ok(mode, l2, dim, n[0], n[1], h[2] + h[3], std::min(h[0], h[1]))) return FNL_OK;
+    *routed = true;
+    unsigned long long* ties;
+    uint32_t* d_n;
+    TRY(ws_arr(ctx, "tc.mu.ties", 2, &ties));
+    TRY(ws_arr(ctx, "tc.mu.n", 2, &d_n));
+    FNL_CUDA_TRY(cudaMemsetAsync(ties, 0, 16, s));
+    const uint32_t hn[2] = {p1, p2};
+    FNL_CUDA_TRY(cudaMemcpyAsync(d_n, hn, 8, cudaMemcpyHostToDevice, s));
+    FNL_CUDA_TRY(cudaStreamSynchronize(s));  // hn is pageable stack memory
+    ResolveSrc f;
+    f.mode = mode;
+    f.q32 = d1;
+    f.q32_pair_stride = (uint64_t)p1 * dim;
+    f.t32 = d2;
+    f.t32_pair_stride = (uint64_t)p2 * dim;
+    ResolveSrc b = f;
+    b.q32 = d2;
+    b.q32_pair_stride = (uint64_t)p2 * dim;
+    b.t32 = d1;
+    b.t32_pair_stride = (uint64_t)p1 * dim;
+    TRY(tensor_nn_pass(ctx, 1, M1, nullptr, p1, d_n, nullptr, M2, dim, l2, d_fwd, p1, nullptr, ties, 0, 0, nullptr,
+                       nullptr, &f));
+    return tensor_nn_pass(ctx, 1, M2, nullptr, p2, d_n + 1, nullptr, M1, dim, l2, d_bwd, p2, nullptr, ties, 0, 0,
+                          nullptr, nullptr, &b);
+}
+
 int tensor_selftest_scores(fnl_context* ctx, const float* d_q, const float* d_t, uint32_t dim, bool l2,
                            int mode, float* d_out) {
     TRY(ensure_attrs());

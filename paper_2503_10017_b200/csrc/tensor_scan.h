@@ -132,6 +132,15 @@ int tensor_nn_dense(fnl_context* ctx, const float* d_q, uint32_t nq, const float
                     uint32_t dim, bool l2, uint32_t* d_nearest, float* d_min_dist, int mode = 0,
                     bool* routed = nullptr);
 
+// Dense mutual NN on the device: each map packed once,
+// NN of every D1 pixel in D2 (d_fwd) and of every D2 pixel in D1 (d_bwd),
+// back to back with no host round trip, resolved in `mode`'s arithmetic.
+// *routed = false (nothing computed) when tensor_route_ok refuses the maps.
+// bad_out (optional, 2 entries): first non-finite flat index of D1 / D2 (~0 = none).
+int tensor_mutual_dense(fnl_context* ctx, const float* d1, uint32_t p1, const float* d2, uint32_t p2, uint32_t dim,
+                        bool l2, int mode, uint32_t* d_fwd, uint32_t* d_bwd, bool* routed,
+                        unsigned long long* bad_out = nullptr);
+
 // Self-test: raw tensor-core scores of a packed query tile pair (256 rows)
 // against one packed target tile (128 rows) -> out[256][128] fp32.
 // mode 0: both operands from shared memory; mode 1: query tiles copied to TMEM

@@ -174,3 +174,18 @@ def test_c2_tensor_route_identical(fnl, ref, backend, metric):
         assert np.array_equal(m1, m2)
         assert strip(r1) == strip(r2)
     assert route_of(fnl, D1, D2, backend, metric)["tensor_route"] == 1
+
+
+def test_mutual_nn_errors_match_reference(fnl, ref):
+    A = ref.gen_random(6, 7, 8, 1)
+    B = ref.gen_random(7, 6, 8, 2)
+    bad = B.copy()
+    bad[2, 3, 4] = np.inf
+    for args in [(A, bad), (bad, A), (A, ref.gen_random(6, 7, 5, 3)), (bad, ref.gen_random(6, 7, 5, 3))]:
+        with pytest.raises(ValueError) as ours:
+            fnl.mutual_nn_exact(*args)
+        with pytest.raises(ValueError) as theirs:
+            ref.mutual_nn_exact(*args)
+        assert str(ours.value) == str(theirs.value)
+    with pytest.raises(ValueError, match="non-finite"):
+        fnl.mutual_nn_tensor(A, bad)
