@@ -485,14 +485,30 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
         const uint32_t qt = warp - 1;
         const uint32_t b_addr = smem_addr(sB);
         const uint32_t d = tmem + qt * 256u;
-        uint32_t k = 0, i = 0;
+        uint32_t k = 0, i = 0, kq = 0;  // kq: tiles this query tile's chains were issued for
         for (uint32_t u = blockIdx.x; u < nitems; u += G, ++i) {
-            const uint32_t nt_unit = a.items[u].tile_end - a.items[u].tile_begin;
+            const TcItem item = a.items[u];
+            const uint32_t nt_unit = item.tile_end - item.tile_begin;
             const uint32_t ab = i & 1u;
             mbar_wait(&afull[ab], (i >> 1) & 1u);
             tc_fence_after();
+            if (qt * 128u >= item.nvalid) {
+                // an all-padding query tile (the last tile pair of a pass with
+                // n % 256 <= 128 live rows): no MMAs, so its chains do not
+                // compete for the tensor pipe; the B slots and the query buffer
+                // are handed back as soon as they are this unit's
+                for (uint32_t t = 0; t < nt_unit; ++t, ++k) {
+                    const uint32_t s = k % kStages;
+                    mbar_wait(&full[s], (k / kStages) & 1u);
+                    if (elect_one()) mbar_arrive(&empty[s]);
+                    __syncwarp();
+                }
+                if (elect_one()) mbar_arrive(&afree[ab]);
+                __syncwarp();
+                continue;
+            }
             const uint64_t ad = umma_desc(smem_addr(sA + ab * kSmemA + qt * kTileBytes));
-            for (uint32_t t = 0; t < nt_unit; ++t, ++k) {
+            for (uint32_t t = 0; t < nt_unit; ++t, ++k, ++kq) {
                 const uint32_t s = k % kStages;
                 if (trace && qt == 0 && lane == 0 && k < 4096) a.trace[4096 + k] = clock64();
                 mbar_wait(&full[s], (k / kStages) & 1u);
@@ -501,7 +517,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
                 for (uint32_t h = 0; h < 2; ++h) {
                     // each 128-target half of the tile is its own accumulator chain,
                     // refilled as soon as its four epilogue warps drained it
-                    mbar_wait(&accfree[qt * 2 + h], (k & 1u) ^ 1u);
+                    mbar_wait(&accfree[qt * 2 + h], (kq & 1u) ^ 1u);
                     if (trace && qt == 0 && h == 0 && lane == 0 && k < 4096) a.trace[8192 + k] = clock64();
                     tc_fence_after();
                     if (elect_one()) {
@@ -529,13 +545,14 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
         const uint32_t e = warp - kFirstEpiWarp, quad = warp & 3u;
         const uint32_t qt = e >> 3, h = (e >> 2) & 1u;
         const uint32_t lane_base = (quad * 32u) << 16;
-        uint32_t k = 0;
+        uint32_t k = 0;  // tiles of this query tile's chains (all-padding units skipped, as the issuer)
         Frag f0, f1;
         for (uint32_t u = blockIdx.x; u < nitems; u += G) {
             const TcItem item = a.items[u];
             RowState st{-INFINITY, -INFINITY, -INFINITY, -INFINITY, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
             const bool warp_real = qt * 128u + quad * 32u < item.nvalid;  // else all rows padding
-            for (uint32_t t = item.tile_begin; t < item.tile_end; ++t, ++k) {
+            const bool tile_live = qt * 128u < item.nvalid;                // else no MMAs were issued
+            for (uint32_t t = item.tile_begin; t < item.tile_end && tile_live; ++t, ++k) {
                 mbar_wait(&tfull[qt * 2 + h], k & 1u);
                 const bool tw = trace && warp == kFirstEpiWarp && k < 4096;
                 if (tw && lane == 0) a.trace[12288 + k] = clock64();
