@@ -156,7 +156,10 @@ int fnl_reciprocal_match_batch(fnl_context* ctx, uint32_t npairs, const float* h
 /* Same, with the maps already resident in device memory (d_d1/d_d2: npairs
  * contiguous H x W x dim fp32 maps).  Outputs stay on the device:
  * d_pairs npairs * 3 * samples u32, d_n_pairs npairs u32.  Asynchronous on the
- * context stream except for one small convergence read per iteration. */
+ * context stream except for one small convergence read per iteration.  For
+ * speed, non-finite inputs are not rejected here (the host-buffer entry points
+ * validate like the reference); they still take the route that keeps the
+ * results identical to the reference's arithmetic on those values. */
 int fnl_reciprocal_match_batch_device(fnl_context* ctx, uint32_t npairs, const float* d_d1,
                                       const float* d_d2, uint32_t h, uint32_t w, uint32_t dim,
                                       const fnl_match_config* cfg, int backend,
