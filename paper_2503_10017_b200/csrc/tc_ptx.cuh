@@ -139,6 +139,14 @@ __device__ __forceinline__ void frag_ld64(uint32_t taddr, Frag& f, Frag& g) {
         : "=r"(f.r[0]), "=r"(f.r[1]), "=r"(f.r[2]), "=r"(f.r[3]), "=r"(f.r[4]), "=r"(f.r[5]), "=r"(f.r[6]), "=r"(f.r[7]), "=r"(f.r[8]), "=r"(f.r[9]), "=r"(f.r[10]), "=r"(f.r[11]), "=r"(f.r[12]), "=r"(f.r[13]), "=r"(f.r[14]), "=r"(f.r[15]), "=r"(f.r[16]), "=r"(f.r[17]), "=r"(f.r[18]), "=r"(f.r[19]), "=r"(f.r[20]), "=r"(f.r[21]), "=r"(f.r[22]), "=r"(f.r[23]), "=r"(f.r[24]), "=r"(f.r[25]), "=r"(f.r[26]), "=r"(f.r[27]), "=r"(f.r[28]), "=r"(f.r[29]), "=r"(f.r[30]), "=r"(f.r[31]), "=r"(g.r[0]), "=r"(g.r[1]), "=r"(g.r[2]), "=r"(g.r[3]), "=r"(g.r[4]), "=r"(g.r[5]), "=r"(g.r[6]), "=r"(g.r[7]), "=r"(g.r[8]), "=r"(g.r[9]), "=r"(g.r[10]), "=r"(g.r[11]), "=r"(g.r[12]), "=r"(g.r[13]), "=r"(g.r[14]), "=r"(g.r[15]), "=r"(g.r[16]), "=r"(g.r[17]), "=r"(g.r[18]), "=r"(g.r[19]), "=r"(g.r[20]), "=r"(g.r[21]), "=r"(g.r[22]), "=r"(g.r[23]), "=r"(g.r[24]), "=r"(g.r[25]), "=r"(g.r[26]), "=r"(g.r[27]), "=r"(g.r[28]), "=r"(g.r[29]), "=r"(g.r[30]), "=r"(g.r[31])
         : "r"(taddr));
 }
+// one tcgen05.ld of 128 consecutive 16-bit-accumulator columns (32x32b.x64
+// with .pack::16b: two adjacent columns per register) into two fragments
+__device__ __forceinline__ void frag_ld128_p16(uint32_t taddr, Frag& f, Frag& g) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x64.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+        : "=r"(f.r[0]), "=r"(f.r[1]), "=r"(f.r[2]), "=r"(f.r[3]), "=r"(f.r[4]), "=r"(f.r[5]), "=r"(f.r[6]), "=r"(f.r[7]), "=r"(f.r[8]), "=r"(f.r[9]), "=r"(f.r[10]), "=r"(f.r[11]), "=r"(f.r[12]), "=r"(f.r[13]), "=r"(f.r[14]), "=r"(f.r[15]), "=r"(f.r[16]), "=r"(f.r[17]), "=r"(f.r[18]), "=r"(f.r[19]), "=r"(f.r[20]), "=r"(f.r[21]), "=r"(f.r[22]), "=r"(f.r[23]), "=r"(f.r[24]), "=r"(f.r[25]), "=r"(f.r[26]), "=r"(f.r[27]), "=r"(f.r[28]), "=r"(f.r[29]), "=r"(f.r[30]), "=r"(f.r[31]), "=r"(g.r[0]), "=r"(g.r[1]), "=r"(g.r[2]), "=r"(g.r[3]), "=r"(g.r[4]), "=r"(g.r[5]), "=r"(g.r[6]), "=r"(g.r[7]), "=r"(g.r[8]), "=r"(g.r[9]), "=r"(g.r[10]), "=r"(g.r[11]), "=r"(g.r[12]), "=r"(g.r[13]), "=r"(g.r[14]), "=r"(g.r[15]), "=r"(g.r[16]), "=r"(g.r[17]), "=r"(g.r[18]), "=r"(g.r[19]), "=r"(g.r[20]), "=r"(g.r[21]), "=r"(g.r[22]), "=r"(g.r[23]), "=r"(g.r[24]), "=r"(g.r[25]), "=r"(g.r[26]), "=r"(g.r[27]), "=r"(g.r[28]), "=r"(g.r[29]), "=r"(g.r[30]), "=r"(g.r[31])
+        : "r"(taddr));
+}
 __device__ __forceinline__ void frag_wait2(Frag& f, Frag& g) {
     asm volatile("tcgen05.wait::ld.sync.aligned;"
                  : "+r"(f.r[0]), "+r"(f.r[1]), "+r"(f.r[2]), "+r"(f.r[3]), "+r"(f.r[4]), "+r"(f.r[5]),

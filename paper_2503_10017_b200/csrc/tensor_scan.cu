@@ -230,6 +230,13 @@ struct GatherArgs {
     bool l2;
     const uint32_t* nslots;  // device slot count (plan header), or null = gridDim.y
     int mode;                // ResolveMode the margin is for
+    // the original fp32 query-side maps (pair stride in floats), or null: a
+    // query row is then read as dim contiguous floats (96 B at d = 24) and
+    // rounded like K1, instead of as four 16-byte chunks spread over four
+    // 128-byte lines of the packed layout (3.9x DRAM over-fetch, round 1)
+    const float* q32;
+    uint64_t q32_pair_stride;
+    bool acc16;  // K3 accumulates in binary16 (dot only): add its rounding to the margin
 };
 
 __global__ void gather_kernel(GatherArgs a) {
@@ -246,10 +253,27 @@ __global__ void gather_kernel(GatherArgs a) {
     float ss = 0.0f;
     if (i < n) {
         const uint32_t src_row = a.ids ? a.ids[(uint64_t)pair * a.cap + i] : i;
-        val = *reinterpret_cast<const uint4*>(a.qmap + pair * a.qmap_pair_bytes + packed_offset(src_row, chunk));
-        // query role: channels dim, dim+1 become 1.0 (l2) / 0 (dot)
         __half h[8];
-        *reinterpret_cast<uint4*>(h) = val;
+        if (a.q32) {
+            const float* row = a.q32 + pair * a.q32_pair_stride + (uint64_t)src_row * a.dim;
+            float v[8];
+            if ((a.dim & 3u) == 0 && chunk * 8 + 8 <= a.dim) {
+                const float4 lo = __ldg(reinterpret_cast<const float4*>(row + chunk * 8));
+                const float4 hi = __ldg(reinterpret_cast<const float4*>(row + chunk * 8 + 4));
+                v[0] = lo.x; v[1] = lo.y; v[2] = lo.z; v[3] = lo.w;
+                v[4] = hi.x; v[5] = hi.y; v[6] = hi.z; v[7] = hi.w;
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) v[k] = chunk * 8 + k < a.dim ? __ldg(row + chunk * 8 + k) : 0.0f;
+            }
+            uint32_t sat = 0;  // counted by K1
+#pragma unroll
+            for (int k = 0; k < 8; ++k) h[k] = __float2half_rn(half_round_sat(v[k], sat));
+        } else {
+            val = *reinterpret_cast<const uint4*>(a.qmap + pair * a.qmap_pair_bytes + packed_offset(src_row, chunk));
+            *reinterpret_cast<uint4*>(h) = val;
+        }
+        // query role: channels dim, dim+1 become 1.0 (l2) / 0 (dot)
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             const uint32_t c = chunk * 8 + k;
@@ -286,6 +310,10 @@ __global__ void gather_kernel(GatherArgs a) {
             const float A = qn * tn;
             m = ldexpf(A, -15) + (d + 2.0f) * ldexpf(A, -24);
             if (full) m += ldexpf(A, -10) + ldexpf(sd * (qn + tn), -24);
+            // binary16 accumulator: each of the two K-step partial sums (|.| <= A
+            // by Cauchy-Schwarz) is rounded to binary16 once (2^-11 relative,
+            // 2^-25 absolute below the normal range)
+            if (a.acc16) m += 1.001f * ldexpf(A, -10) + ldexpf(1.0f, -23);
         } else {
             const float A = qn * tn + tn * tn;
             const float S = (qn + tn) * (qn + tn);
@@ -410,7 +438,42 @@ __device__ __forceinline__ void subtile_scan(RowState& st, const Frag& f, const 
     if (__any_sync(0xFFFFFFFFu, m > st.b4)) tile_update(st, m, sub);
 }
 
+// binary16 accumulator variant: 64 scores of one row as 32 packed f16x2
+// registers (tcgen05.ld .pack::16b) -> their max (max.f16x2 tree), padding
+// columns past nt masked to -inf
+__device__ __forceinline__ uint32_t hmax2(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("max.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+__device__ __forceinline__ float tile_max64_h(const Frag& f, uint32_t sub, uint32_t nt) {
+    uint32_t v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = f.r[j];
+    if ((sub + 1) * kSubTile > nt) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const uint32_t c = sub * kSubTile + 2u * j;
+            if (c >= nt) v[j] = (v[j] & 0xFFFF0000u) | 0xFC00u;
+            if (c + 1 >= nt) v[j] = (v[j] & 0x0000FFFFu) | 0xFC000000u;
+        }
+    }
+#pragma unroll
+    for (int w = 16; w >= 1; w >>= 1)
+#pragma unroll
+        for (int j = 0; j < w; ++j) v[j] = hmax2(v[j], v[j + w]);
+    const float lo = __half2float(__ushort_as_half((unsigned short)(v[0] & 0xFFFFu)));
+    const float hi = __half2float(__ushort_as_half((unsigned short)(v[0] >> 16)));
+    return fmaxf(lo, hi);
+}
+
+// kF16: the accumulators are binary16 (instruction descriptor D format f16,
+// dot metric only, margin widened in K2): a warp reads its 128 columns with
+// ONE packed tcgen05.ld (64 registers), releases the accumulator at once and
+// reduces afterwards with max.f16x2 trees.
+template <bool kF16>
 __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
+    constexpr uint32_t kIdesc = kF16 ? (kIdescF16M128N128 & ~(1u << 4)) : kIdescF16M128N128;
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint32_t tmem_slot;
     uint8_t* sA = smem;                  // [2][16 KB]
@@ -524,8 +587,8 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
                         // half h starts 16 row groups (8 KB) further; K-step 1 starts 256 B
                         // (two 8-channel chunks) further: +16 in descriptor units
                         const uint64_t bh = bd + (uint64_t)h * (8192u >> 4);
-                        tc_mma_f16(d + h * 128u, ad, bh, kIdescF16M128N128, 0u);
-                        tc_mma_f16(d + h * 128u, ad + 16u, bh + 16u, kIdescF16M128N128, 1u);
+                        tc_mma_f16(d + h * 128u, ad, bh, kIdesc, 0u);
+                        tc_mma_f16(d + h * 128u, ad + 16u, bh + 16u, kIdesc, 1u);
                         tc_commit(&tfull[qt * 2 + h]);
                         if (h == 1) tc_commit(&empty[s]);
                     }
@@ -564,6 +627,19 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
                 tc_fence_after();
                 const uint32_t taddr = tmem + lane_base + qt * 256u + h * 128u;
                 const uint32_t sub0 = t * kSubPerTile + 2u * h;
+                if constexpr (kF16) {
+                    frag_ld128_p16(taddr, f0, f1);
+                    frag_wait2(f0, f1);
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&accfree[qt * 2 + h]);  // all 128 columns read
+                    const float m0 = tile_max64_h(f0, sub0, a.nt), m1 = tile_max64_h(f1, sub0 + 1, a.nt);
+                    if (__any_sync(0xFFFFFFFFu, fmaxf(m0, m1) > st.b4)) {
+                        tile_update(st, m0, sub0);
+                        tile_update(st, m1, sub0 + 1);
+                    }
+                    continue;
+                }
                 frag_ld64(taddr, f0, f1);
                 frag_wait2(f0, f1);
                 float m0;
@@ -1130,7 +1206,8 @@ int ensure_attrs() {
     FNL_CUDA_TRY(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lk(attr_mu);
     if (dev >= 0 && dev < 64 && attr_done[dev]) return FNL_OK;
-    FNL_CUDA_TRY(cudaFuncSetAttribute(tc_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal));
+    FNL_CUDA_TRY(cudaFuncSetAttribute(tc_scan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal));
+    FNL_CUDA_TRY(cudaFuncSetAttribute(tc_scan_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal));
     FNL_CUDA_TRY(cudaFuncSetAttribute(selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal));
     if (dev >= 0 && dev < 64) attr_done[dev] = true;
     return FNL_OK;
@@ -1377,10 +1454,13 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
         plan_kernel<<<1, kPlanThreads, 0, s>>>(pa);
         FNL_CUDA_TRY(cudaGetLastError());
     }
+    // binary16 accumulators in K3 (experimental, FNL_TC_F16ACC=1; dot only)
+    static const bool f16acc_env = getenv("FNL_TC_F16ACC") && atoi(getenv("FNL_TC_F16ACC")) != 0;
+    const bool acc16 = f16acc_env && !l2;
     // ---- K2 gather
     {
         GatherArgs g{Q.data, Q.pair_bytes, ids, cap, d_active, d_slot_pair, d_slot_base, qbuf, margin,
-                     T.max_norm, dim, l2, d_hdr, rs.mode};
+                     T.max_norm, dim, l2, d_hdr, rs.mode, rs.q32, rs.q32_pair_stride, acc16};
         dim3 grid(ceil_div_u(tp_per_pair * kQueryTilePair * 4, 256), npairs);
         ProfScope prof(ctx, FNL_KCLASS_GATHER);
         gather_kernel<<<grid, 256, 0, s>>>(g);
@@ -1398,7 +1478,8 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
         const uint32_t grid = std::min<uint32_t>(nitems_cap, sms);
         cudaEvent_t end_ev;
         ctx_score_begin(ctx, &end_ev);
-        tc_scan_kernel<<<grid, kScanThreads, kSmemTotal, s>>>(t);
+        if (acc16) tc_scan_kernel<true><<<grid, kScanThreads, kSmemTotal, s>>>(t);
+        else tc_scan_kernel<false><<<grid, kScanThreads, kSmemTotal, s>>>(t);
         ctx_score_end(ctx, end_ev);
         FNL_CUDA_TRY(cudaGetLastError());
     }
