@@ -709,6 +709,7 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
     }
     const int mode = tensor ? fnl::kResolveRounded : (hyb ? fnl::kResolveHybrid : fnl::kResolveFull);
     bool tc = false;  // tensor route taken
+    bool acc16 = false;  // K3 may accumulate in binary16 (every pair's norms allow it)
     Prepared P1, P2;
     fnl::PackedMaps T1, T2;
     unsigned long long *near_ties = nullptr, *tsat = nullptr;
@@ -725,11 +726,10 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
         TRY(fnl::tensor_pack(ctx, "m.t2", d_d2, npairs, p2, dim, l2, tbad + npairs, tsat + npairs, &T2));
         tc = true;
         // The host reads the pack's per-pair finiteness / norms / saturations
-        // when it must: to validate like the reference FeatureMap (host-buffer
-        // entry points) and to check the route (the tensor backend on dot
-        // maps is always eligible, so the device-resident batch path of the
-        // bench has no host round trip here).
-        if (validate || !tensor || l2) {
+        // (one small round trip): to validate like the reference FeatureMap
+        // (host-buffer entry points), to check the route, and to choose the
+        // K3 accumulator (binary16 when every pair's norms allow it).
+        {
             std::vector<unsigned long long> hb(2 * (size_t)npairs), hs(2 * (size_t)npairs);
             std::vector<float> hn(2 * (size_t)npairs);
             FNL_CUDA_TRY(cudaMemcpyAsync(hb.data(), tbad, hb.size() * 8, cudaMemcpyDeviceToHost, s));
@@ -748,6 +748,8 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
             for (uint32_t p = 0; p < npairs && tc; ++p)
                 tc = fnl::tensor_route_ok(mode, l2, dim, hn[p], hn[npairs + p], hs[p] + hs[npairs + p],
                                           std::min(hb[p], hb[npairs + p]));
+            acc16 = tc;
+            for (uint32_t p = 0; p < npairs && acc16; ++p) acc16 = fnl::acc16_ok(l2, hn[p], hn[npairs + p]);
         }
     }
     if (shard && !tc)
@@ -792,6 +794,7 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
             const fnl::PackedMaps& TT = fwd ? T2 : T1;
             fnl::ResolveSrc rs;
             rs.mode = mode;
+            rs.acc16 = acc16;
             rs.q32 = fwd ? d_d1 : d_d2;
             rs.q32_pair_stride = (uint64_t)(fwd ? p1 : p2) * dim;
             rs.t32 = fwd ? d_d2 : d_d1;

@@ -90,6 +90,7 @@ struct PackArgs {
     float* max_norm;                 // per pair, as non-negative float bits
     unsigned long long* bad;         // per pair first non-finite flat index
     unsigned long long* sat;         // per pair saturation count
+    float* max_norm_hi;              // per pair: max norm over packed channels 16..31
 };
 
 constexpr int kPackThreads = 256;
@@ -112,9 +113,9 @@ __device__ __forceinline__ void pack_load(const PackArgs& a, const float* src, u
     }
 }
 
-// rounds one row chunk, writes it, returns the row's norm (0 for padding rows)
+// rounds one row chunk, writes it, returns the row's squared norm (0 for padding rows)
 __device__ __forceinline__ float pack_store(const PackArgs& a, uint8_t* dst, uint32_t pair, uint32_t row,
-                                            uint32_t chunk, float (&v)[8], uint32_t& sat) {
+                                            uint32_t chunk, float (&v)[8], uint32_t& sat, float& nmax_hi) {
     const bool real = row < a.rows;
     float ss = 0.0f;
 #pragma unroll
@@ -125,8 +126,11 @@ __device__ __forceinline__ float pack_store(const PackArgs& a, uint8_t* dst, uin
         v[i] = x;
         ss = __fmaf_rn(x, x, ss);
     }
-    // row norm^2 over the 4 chunk lanes (fixed order -> deterministic)
+    // row norm^2 over the 4 chunk lanes (fixed order -> deterministic); after
+    // the first step lanes 2-3 hold the norm^2 of channels 16..31.  Maxima are
+    // kept squared (one sqrt per flush)
     ss += __shfl_xor_sync(0xFFFFFFFFu, ss, 1);
+    if (real && chunk >= 2) nmax_hi = fmaxf(nmax_hi, ss);
     ss += __shfl_xor_sync(0xFFFFFFFFu, ss, 2);
     if (a.l2 && real) {
         // -|t|^2/2 as hi + lo binary16 terms in channels dim, dim+1
@@ -146,20 +150,29 @@ __device__ __forceinline__ float pack_store(const PackArgs& a, uint8_t* dst, uin
     out.z = pack_half2(v[4], v[5]);
     out.w = pack_half2(v[6], v[7]);
     *reinterpret_cast<uint4*>(dst + packed_offset(row, chunk)) = out;
-    return real ? sqrtf(ss) : 0.0f;
+    return real ? ss : 0.0f;
 }
 
-__device__ __forceinline__ void pack_flush(const PackArgs& a, uint32_t pair, uint32_t& sat, float& nmax) {
+__device__ __forceinline__ void pack_flush(const PackArgs& a, uint32_t pair, uint32_t& sat, float& nmax,
+                                           float& nmax_hi) {
     sat = warp_sum(sat);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) nmax = fmaxf(nmax, __shfl_xor_sync(0xFFFFFFFFu, nmax, o));
+    for (int o = 16; o > 0; o >>= 1) {
+        nmax = fmaxf(nmax, __shfl_xor_sync(0xFFFFFFFFu, nmax, o));
+        nmax_hi = fmaxf(nmax_hi, __shfl_xor_sync(0xFFFFFFFFu, nmax_hi, o));
+    }
     if ((threadIdx.x & 31u) == 0) {
         if (sat) atomicAdd(a.sat + pair, (unsigned long long)sat);
-        // non-negative floats order like their bits
+        // non-negative floats order like their bits (maxima of squared norms)
+        nmax = sqrtf(nmax);
+        nmax_hi = sqrtf(nmax_hi);
         if (nmax > 0.0f) atomicMax(reinterpret_cast<unsigned int*>(a.max_norm) + pair, __float_as_uint(nmax));
+        if (nmax_hi > 0.0f)
+            atomicMax(reinterpret_cast<unsigned int*>(a.max_norm_hi) + pair, __float_as_uint(nmax_hi));
     }
     sat = 0;
     nmax = 0.0f;
+    nmax_hi = 0.0f;
 }
 
 // Flat over (pair, 8-row group): warp w owns a contiguous range of groups of
@@ -177,7 +190,7 @@ __global__ void __launch_bounds__(kPackThreads) pack_kernel(PackArgs a, uint32_t
     if (g >= end) return;
     uint32_t pair = (uint32_t)(g / groups);
     uint32_t sat = 0;
-    float nmax = 0.0f;
+    float nmax = 0.0f, nmax_hi = 0.0f;
     while (g < end) {
         const uint32_t gi = (uint32_t)(g - (uint64_t)pair * groups);
         const float* src = a.src + (uint64_t)pair * a.rows * a.dim;
@@ -192,23 +205,23 @@ __global__ void __launch_bounds__(kPackThreads) pack_kernel(PackArgs a, uint32_t
 #pragma unroll
             for (int q = 0; q < 4; ++q) pack_load(a, src, r0 + 8 * q, chunk, v[q]);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) nmax = fmaxf(nmax, pack_store(a, dst, pair, r0 + 8 * q, chunk, v[q], sat));
+            for (int q = 0; q < 4; ++q) nmax = fmaxf(nmax, pack_store(a, dst, pair, r0 + 8 * q, chunk, v[q], sat, nmax_hi));
         }
         for (; j + 1 < n; j += 2) {
             float v0[8], v1[8];
             const uint32_t r0 = (gi + j) * 8 + sub, r1 = r0 + 8;
             pack_load(a, src, r0, chunk, v0);
             pack_load(a, src, r1, chunk, v1);
-            nmax = fmaxf(nmax, pack_store(a, dst, pair, r0, chunk, v0, sat));
-            nmax = fmaxf(nmax, pack_store(a, dst, pair, r1, chunk, v1, sat));
+            nmax = fmaxf(nmax, pack_store(a, dst, pair, r0, chunk, v0, sat, nmax_hi));
+            nmax = fmaxf(nmax, pack_store(a, dst, pair, r1, chunk, v1, sat, nmax_hi));
         }
         if (j < n) {
             float v0[8];
             const uint32_t r0 = (gi + j) * 8 + sub;
             pack_load(a, src, r0, chunk, v0);
-            nmax = fmaxf(nmax, pack_store(a, dst, pair, r0, chunk, v0, sat));
+            nmax = fmaxf(nmax, pack_store(a, dst, pair, r0, chunk, v0, sat, nmax_hi));
         }
-        pack_flush(a, pair, sat, nmax);
+        pack_flush(a, pair, sat, nmax, nmax_hi);
         g += n;
         ++pair;
     }
@@ -237,6 +250,7 @@ struct GatherArgs {
     const float* q32;
     uint64_t q32_pair_stride;
     bool acc16;  // K3 accumulates in binary16 (dot only): add its rounding to the margin
+    const float* tmax_hi;  // per pair max target norm over channels 16..31 (acc16)
 };
 
 __global__ void gather_kernel(GatherArgs a) {
@@ -283,8 +297,11 @@ __global__ void gather_kernel(GatherArgs a) {
         }
         val = *reinterpret_cast<uint4*>(h);
     }
+    float sh = chunk >= 2 ? ss : 0.0f;  // channels 16..31: the binary16 accumulator's first K step
     ss += __shfl_xor_sync(0xFFFFFFFFu, ss, 1);
     ss += __shfl_xor_sync(0xFFFFFFFFu, ss, 2);
+    sh += __shfl_xor_sync(0xFFFFFFFFu, sh, 1);
+    sh += __shfl_xor_sync(0xFFFFFFFFu, sh, 2);
     *reinterpret_cast<uint4*>(a.qbuf + packed_offset(drow, chunk)) = val;
     if (chunk == 0) {
         // One-sided certification margin M (score units, larger is better):
@@ -310,10 +327,16 @@ __global__ void gather_kernel(GatherArgs a) {
             const float A = qn * tn;
             m = ldexpf(A, -15) + (d + 2.0f) * ldexpf(A, -24);
             if (full) m += ldexpf(A, -10) + ldexpf(sd * (qn + tn), -24);
-            // binary16 accumulator: each of the two K-step partial sums (|.| <= A
-            // by Cauchy-Schwarz) is rounded to binary16 once (2^-11 relative,
-            // 2^-25 absolute below the normal range)
-            if (a.acc16) m += 1.001f * ldexpf(A, -10) + ldexpf(1.0f, -23);
+            // binary16 accumulator (K3 issues channels 16..31 first): the first
+            // K step's partial sum, |.| <= |q_hi| |t_hi| by Cauchy-Schwarz, is
+            // rounded to binary16 once (2^-11 relative, 2^-25 absolute below the
+            // normal range); the final rounding, 2^-11 of the score itself, is
+            // added by the merge from the bound it compares against
+            if (a.acc16) {
+                const float qh = sqrtf(sh) * 1.001f + ldexpf(sd, -24);
+                const float th = a.tmax_hi[pair] * 1.001f + ldexpf(sd, -24);
+                m += 1.001f * ldexpf(qh * th, -11) + ldexpf(1.0f, -23);
+            }
         } else {
             const float A = qn * tn + tn * tn;
             const float S = (qn + tn) * (qn + tn);
@@ -587,8 +610,13 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
                         // half h starts 16 row groups (8 KB) further; K-step 1 starts 256 B
                         // (two 8-channel chunks) further: +16 in descriptor units
                         const uint64_t bh = bd + (uint64_t)h * (8192u >> 4);
-                        tc_mma_f16(d + h * 128u, ad, bh, kIdesc, 0u);
-                        tc_mma_f16(d + h * 128u, ad + 16u, bh + 16u, kIdesc, 1u);
+                        if (kF16) {  // channels 16..31 first: the rounded partial sum is the smaller one
+                            tc_mma_f16(d + h * 128u, ad + 16u, bh + 16u, kIdesc, 0u);
+                            tc_mma_f16(d + h * 128u, ad, bh, kIdesc, 1u);
+                        } else {
+                            tc_mma_f16(d + h * 128u, ad, bh, kIdesc, 0u);
+                            tc_mma_f16(d + h * 128u, ad + 16u, bh + 16u, kIdesc, 1u);
+                        }
                         tc_commit(&tfull[qt * 2 + h]);
                         if (h == 1) tc_commit(&empty[s]);
                     }
@@ -710,6 +738,7 @@ struct MergeArgs {
     const uint32_t* ids;        // query ids of the pass (null = identity), pair stride cap
     uint32_t cap;
     ResolveSrc rs;              // kResolveFull: original fp32 rows
+    bool acc16;                 // K3 scores are binary16 accumulations: + 2^-11 |bound|
 };
 
 // sharded mode: this rank's winner key of output slot o -- a local store, or
@@ -954,7 +983,10 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs a) {
                 bool closed = true;  // no candidate left: every target resolved
                 if (st != kNoTile) {
                     const float Bn = s_b[row][c];
-                    const float lb = kL2 ? qq - 2.0f * (Bn + M) : -(Bn + M);  // bound on every other distance
+                    // binary16 accumulator: its final rounding moves a score by at most
+                    // 2^-11 of itself, and score + 2^-11 |score| grows with the score
+                    const float Mf = a.acc16 ? M + 1.001f * ldexpf(fabsf(Bn), -11) : M;
+                    const float lb = kL2 ? qq - 2.0f * (Bn + Mf) : -(Bn + Mf);  // bound on every other distance
                     const float dref = MODE == kResolveHybrid ? dmin + 2.0f * ulp16(fabsf(dmin)) : dmin;
                     closed = dref < lb;
                 }
@@ -1373,13 +1405,14 @@ int tensor_pack(fnl_context* ctx, const char* tag, const float* d_src, uint32_t 
     const uint64_t pair_bytes = (uint64_t)rows_pad * kPackRowBytes;
     std::string t(tag);
     TRY(ws_arr(ctx, (t + ".packed").c_str(), (size_t)npairs * pair_bytes, &out->data));
-    TRY(ws_arr(ctx, (t + ".maxnorm").c_str(), npairs, &out->max_norm));
+    TRY(ws_arr(ctx, (t + ".maxnorm").c_str(), 2 * (size_t)npairs, &out->max_norm));
+    out->max_norm_hi = out->max_norm + npairs;
     cudaStream_t s = ctx_stream(ctx);
-    FNL_CUDA_TRY(cudaMemsetAsync(out->max_norm, 0, npairs * sizeof(float), s));
+    FNL_CUDA_TRY(cudaMemsetAsync(out->max_norm, 0, 2 * (size_t)npairs * sizeof(float), s));
     out->pair_bytes = pair_bytes;
     out->rows = rows;
     out->npairs = npairs;
-    PackArgs a{d_src, out->data, pair_bytes, rows, rows_pad, dim, l2, out->max_norm, d_bad, d_sat};
+    PackArgs a{d_src, out->data, pair_bytes, rows, rows_pad, dim, l2, out->max_norm, d_bad, d_sat, out->max_norm_hi};
     // 8 blocks per SM (69 registers: 3 resident per SM, so ~2.7 waves; measured
     // no faster with 4 resident blocks and one wave, or with 8 row groups in
     // flight per warp at 2 blocks per SM: 1.60 / 1.84 vs 1.58 ms per 128 pairs)
@@ -1454,13 +1487,12 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
         plan_kernel<<<1, kPlanThreads, 0, s>>>(pa);
         FNL_CUDA_TRY(cudaGetLastError());
     }
-    // binary16 accumulators in K3 (experimental, FNL_TC_F16ACC=1; dot only)
-    static const bool f16acc_env = getenv("FNL_TC_F16ACC") && atoi(getenv("FNL_TC_F16ACC")) != 0;
-    const bool acc16 = f16acc_env && !l2;
+    // binary16 accumulators in K3 when the caller established they are safe
+    const bool acc16 = rs.acc16 != 0 && !l2;
     // ---- K2 gather
     {
         GatherArgs g{Q.data, Q.pair_bytes, ids, cap, d_active, d_slot_pair, d_slot_base, qbuf, margin,
-                     T.max_norm, dim, l2, d_hdr, rs.mode, rs.q32, rs.q32_pair_stride, acc16};
+                     T.max_norm, dim, l2, d_hdr, rs.mode, rs.q32, rs.q32_pair_stride, acc16, T.max_norm_hi};
         dim3 grid(ceil_div_u(tp_per_pair * kQueryTilePair * 4, 256), npairs);
         ProfScope prof(ctx, FNL_KCLASS_GATHER);
         gather_kernel<<<grid, 256, 0, s>>>(g);
@@ -1487,7 +1519,7 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     {
         MergeArgs m{partial, d_tp_pair, d_tp_row0, d_tp_qi0, d_hdr, d_active, margin, qbuf, T.data,
                     T.pair_bytes, nt, dim, out, min_dist, out_stride, rescan, rcount, d_near_ties, npairs, shard_keys,
-                    pp, ids, cap, rs};
+                    pp, ids, cap, rs, acc16};
         ProfScope prof(ctx, FNL_KCLASS_MERGE);
         const uint32_t grid = tp_max * kMergeSlices;
         if (dim == 24) {
@@ -1568,6 +1600,14 @@ bool tensor_route_ok(int mode, bool l2, uint32_t dim, float qmax_norm, float tma
     return true;
 }
 
+bool acc16_ok(bool l2, float qmax_norm, float tmax_norm) {
+    static const bool off = getenv("FNL_TC_F16ACC") && atoi(getenv("FNL_TC_F16ACC")) == 0;
+    if (off || l2) return false;
+    // |partial sums| <= |q| |t| < 2^14: far inside binary16 (max 65504), so no
+    // score or partial sum saturates
+    return (double)qmax_norm * 1.001 * (double)tmax_norm * 1.001 < 16384.0;
+}
+
 int tensor_nn_dense(fnl_context* ctx, const float* d_q, uint32_t nq, const float* d_t, uint32_t nt,
                     uint32_t dim, bool l2, uint32_t* d_nearest, float* d_min_dist, int mode, bool* routed) {
     if (routed) {
@@ -1580,6 +1620,7 @@ int tensor_nn_dense(fnl_context* ctx, const float* d_q, uint32_t nq, const float
     FNL_CUDA_TRY(cudaMemsetAsync(scratch, 0xFF, 16, s));
     FNL_CUDA_TRY(cudaMemsetAsync(scratch + 2, 0, 16, s));
     PackedMaps Q, T;
+    bool acc16 = false;  // binary16 accumulators only once the norms are known
     TRY(tensor_pack(ctx, "tc.dense.q", d_q, 1, nq, dim, l2, scratch, scratch + 2, &Q));
     TRY(tensor_pack(ctx, "tc.dense.t", d_t, 1, nt, dim, l2, scratch + 1, scratch + 3, &T));
     if (routed) {
@@ -1594,6 +1635,7 @@ int tensor_nn_dense(fnl_context* ctx, const float* d_q, uint32_t nq, const float
         const unsigned long long bad = std::min(h[0], h[1]);
         if (!tensor_route_ok(mode, l2, dim, n[0], n[1], h[2] + h[3], bad)) return FNL_OK;
         *routed = true;
+        acc16 = acc16_ok(l2, n[0], n[1]);
     }
     unsigned long long* ties;
     TRY(ws_arr(ctx, "tc.dense.ties", 2, &ties));
@@ -1603,6 +1645,7 @@ int tensor_nn_dense(fnl_context* ctx, const float* d_q, uint32_t nq, const float
     FNL_CUDA_TRY(cudaMemcpyAsync(d_nq, &nq, 4, cudaMemcpyHostToDevice, s));  // pageable: staged before return
     ResolveSrc rs;
     rs.mode = mode;
+    rs.acc16 = acc16;
     rs.q32 = d_q;
     rs.q32_pair_stride = (uint64_t)nq * dim;
     rs.t32 = d_t;
@@ -1645,6 +1688,7 @@ int tensor_mutual_dense(fnl_context* ctx, const float* d1, uint32_t p1, const fl
     FNL_CUDA_TRY(cudaStreamSynchronize(s));  // hn is pageable stack memory
     ResolveSrc f;
     f.mode = mode;
+    f.acc16 = acc16_ok(l2, n[0], n[1]);
     f.q32 = d1;
     f.q32_pair_stride = (uint64_t)p1 * dim;
     f.t32 = d2;

@@ -35,6 +35,9 @@ struct PackedMaps {
     uint32_t rows = 0;        // real rows per map
     uint32_t npairs = 0;
     float* max_norm = nullptr;  // per pair: max L2 norm of a binary16 row (device)
+    // per pair: max norm of a row's packed channels 16..31, the first K step of
+    // the binary16-accumulator MMA (bounds the partial sum it rounds)
+    float* max_norm_hi = nullptr;
 };
 
 // K1: fp32 maps (npairs x rows x dim, device) -> packed binary16.  Role
@@ -86,6 +89,9 @@ enum ResolveMode : int {
 // the pass's query ids) and target map rows, npairs stacked maps each.
 struct ResolveSrc {
     int mode = kResolveRounded;
+    // K3 may accumulate in binary16 (dot metric, |q| |t| small enough that no
+    // partial sum saturates; see acc16_ok): certified with a wider margin
+    int acc16 = 0;
     const float* q32 = nullptr;
     uint64_t q32_pair_stride = 0;  // floats
     const float* t32 = nullptr;
@@ -97,6 +103,10 @@ struct ResolveSrc {
 // (kResolveFull / kResolveHybrid), and hybrid distances must not saturate.
 bool tensor_route_ok(int mode, bool l2, uint32_t dim, float qmax_norm, float tmax_norm,
                      unsigned long long sat, unsigned long long bad);
+// binary16 accumulators are safe when every score / partial sum stays far
+// inside binary16 range: dot metric and max|q| max|t| < 2^14 (FNL_TC_F16ACC=0
+// turns them off)
+bool acc16_ok(bool l2, float qmax_norm, float tmax_norm);
 struct ShardPeers {
     long long* keys[kMaxShardPeers];
     uint32_t n;
