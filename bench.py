@@ -302,6 +302,7 @@ def main_b200(args):
     stats = step_device(with_stats=True)
     rows_per_step = sum(s["query_rows"] for s in stats)
     ties_per_step = sum(s["near_tie_rows"] for s in stats)
+    rescans_per_step = sum(s["rescan_rows"] for s in stats)
     torch.cuda.synchronize()
     fnl.kernel_timing(reset=True)
     query_rows, near_ties = 0, 0
@@ -470,6 +471,7 @@ def main_b200(args):
                              "per GPU per step > 126 MB L2 (no L2 flush needed)",
                    "query_rows_per_step": tot_rows / args.steps,
                    "near_tie_rows_per_step": near_ties / args.steps if world == 1 else None,
+                   "rescan_rows_per_step": rescans_per_step if world == 1 else None,
                    "matches_per_step_rank0": matches_last,
                    "pairs_by_rank": [[int(a), int(b)] for a, b, _ in by_rank],
                    "matches_by_rank": [int(m) for _, _, m in by_rank],

@@ -367,7 +367,7 @@ struct TcArgs {
     uint32_t nt;
     const TcItem* items;
     const uint32_t* nitems;  // device item count (plan header)
-    float4* partial;  // [item][col half][256][2] = (b1, b2, b3, b4), (t1, t2, t3 bits, 0)
+    float4* partial;  // [item][col half][256][3] = (b1..b4), (b5, b6, t1, t2), (t3, t4, t5 bits, 0)
     int debug;        // profiling only: 1 = epilogue releases buffers unread, 16 = clock trace of CTA 0
     unsigned long long* trace;  // [4][4096] clock64 stamps (debug & 16)
 };
@@ -391,6 +391,7 @@ constexpr int kStages = 4;
 // (column quarter = (w-3)/4, TMEM lane quadrant = w%4)
 constexpr uint32_t kSubPerTile = 4;  // 64-target sub-tiles per 256-target tile
 constexpr int kPartialSplit = 2;     // partial states per (work unit, row): one per 128-column half
+constexpr int kPartialF4 = 3;        // float4s per partial state: b1..b6, t1..t5
 constexpr int kEpiWarps = 16;
 constexpr int kFirstEpiWarp = 3;
 constexpr int kScanThreads = (kFirstEpiWarp + kEpiWarps) * 32;
@@ -406,16 +407,47 @@ constexpr uint32_t kSubTile = 64;  // winner granularity handed to the merge
 
 // Per query row and 64-target sub-tile: m = max of the 64 fp32 scores
 // (3-input-max tree, ~0.5 ALU op per score, no data-dependent branch), then a
-// branch-free insert of (m, sub-tile) into the row's top-4 of sub-tile maxima:
-// b1 >= b2 >= b3 >= b4 with the sub-tiles t1, t2, t3 of the first three.  The
-// merge resolves t1, then t2, then t3 with the exact reference chain, and
-// closes the row as soon as the exact winner beats the next bound (b2, b3 or
-// b4) by the certification margin; only rows with four sub-tiles inside the
-// margin are re-scanned.
+// branch-free insert of (m, sub-tile) into the row's top-kTopSub of sub-tile maxima:
+// b1 >= ... >= b6 with the sub-tiles t1..t5 of the first five.  The merge
+// resolves t1, t2, ... with the exact reference chain and closes the row as
+// soon as the exact winner beats the next bound by the certification margin;
+// only rows with six sub-tiles inside the margin are re-scanned (with binary16
+// accumulators the margin is ~2^-11 |q| |t|, and a top-4 state sent ~230 rows
+// per 128-pair step to the full rescan).
+constexpr int kTopSub = 6;  // <= 6 (partial state: 3 float4)
 struct RowState {
-    float b1, b2, b3, b4;
-    uint32_t t1, t2, t3;
+    float b[kTopSub];
+    uint32_t t[kTopSub - 1];
 };
+__device__ __forceinline__ RowState row_state_init() {
+    RowState st;
+#pragma unroll
+    for (int i = 0; i < kTopSub; ++i) st.b[i] = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < kTopSub - 1; ++i) st.t[i] = 0xFFFFFFFFu;
+    return st;
+}
+
+// Binary16-accumulator path: a sub-tile maximum is an exact binary16 value, so
+// as an fp32 its 13 low mantissa bits are zero; they carry the sub-tile index
+// relative to the work unit's first tile (< 8192: the plan caps a unit at 2048
+// tiles).  Keys of different maxima order like the maxima (the index moves a
+// value by less than one binary16 ulp), so the row's top-6 is a plain
+// min/max network over keys -- no index selects.
+constexpr uint32_t kKeyBits = 13;
+constexpr uint32_t kKeyMask = (1u << kKeyBits) - 1u;
+constexpr uint32_t kMaxUnitTiles = (1u << kKeyBits) / kSubPerTile;  // 2048
+__device__ __forceinline__ float key_of(float m, uint32_t rel) {
+    m = fmaxf(m, -0x1p126f);  // -inf (all padding) -> a finite floor, so the index bits stay a number
+    return __uint_as_float((__float_as_uint(m) & ~kKeyMask) | rel);
+}
+__device__ __forceinline__ float key_value(float k) { return __uint_as_float(__float_as_uint(k) & ~kKeyMask); }
+__device__ __forceinline__ uint32_t key_rel(float k) { return __float_as_uint(k) & kKeyMask; }
+__device__ __forceinline__ void key_insert(float (&kb)[kTopSub], float m) {
+#pragma unroll
+    for (int i = kTopSub - 1; i >= 1; --i) kb[i] = fmaxf(kb[i], fminf(kb[i - 1], m));
+    kb[0] = fmaxf(kb[0], m);
+}
 
 __device__ __forceinline__ float tile_max64(const float* v) {
     float r[22];
@@ -430,14 +462,17 @@ __device__ __forceinline__ float tile_max64(const float* v) {
 }
 
 __device__ __forceinline__ void tile_update(RowState& st, float m, uint32_t tile) {
-    const bool gt1 = m > st.b1, gt2 = m > st.b2, gt3 = m > st.b3;
-    st.b4 = fmaxf(st.b4, fminf(st.b3, m));
-    st.t3 = gt2 ? st.t2 : (gt3 ? tile : st.t3);
-    st.b3 = fmaxf(st.b3, fminf(st.b2, m));
-    st.t2 = gt1 ? st.t1 : (gt2 ? tile : st.t2);
-    st.b2 = fmaxf(st.b2, fminf(st.b1, m));
-    st.t1 = gt1 ? tile : st.t1;
-    st.b1 = fmaxf(st.b1, m);
+    bool gt[kTopSub - 1];
+#pragma unroll
+    for (int i = 0; i < kTopSub - 1; ++i) gt[i] = m > st.b[i];
+    st.b[kTopSub - 1] = fmaxf(st.b[kTopSub - 1], fminf(st.b[kTopSub - 2], m));
+#pragma unroll
+    for (int i = kTopSub - 2; i >= 1; --i) {
+        st.t[i] = gt[i - 1] ? st.t[i - 1] : (gt[i] ? tile : st.t[i]);
+        st.b[i] = fmaxf(st.b[i], fminf(st.b[i - 1], m));
+    }
+    st.t[0] = gt[0] ? tile : st.t[0];
+    st.b[0] = fmaxf(st.b[0], m);
 }
 
 // 64 consecutive scores of one row -> sub-tile update (padding masked)
@@ -458,7 +493,7 @@ __device__ __forceinline__ void subtile_scan(RowState& st, const Frag& f, const 
     // statistics: ~3 ln(#sub-tiles) updates per row over a whole scan), so the
     // branch-free top-3 insert runs only when some lane of the warp needs it
     const float m = tile_max64(v);
-    if (__any_sync(0xFFFFFFFFu, m > st.b4)) tile_update(st, m, sub);
+    if (__any_sync(0xFFFFFFFFu, m > st.b[kTopSub - 1])) tile_update(st, m, sub);
 }
 
 // binary16 accumulator variant: 64 scores of one row as 32 packed f16x2
@@ -640,7 +675,10 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
         Frag f0, f1;
         for (uint32_t u = blockIdx.x; u < nitems; u += G) {
             const TcItem item = a.items[u];
-            RowState st{-INFINITY, -INFINITY, -INFINITY, -INFINITY, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+            RowState st = row_state_init();
+            float kb[kTopSub];  // kF16: top-6 keys
+#pragma unroll
+            for (int i = 0; i < kTopSub; ++i) kb[i] = key_of(-INFINITY, 0);
             const bool warp_real = qt * 128u + quad * 32u < item.nvalid;  // else all rows padding
             const bool tile_live = qt * 128u < item.nvalid;                // else no MMAs were issued
             for (uint32_t t = item.tile_begin; t < item.tile_end && tile_live; ++t, ++k) {
@@ -661,10 +699,12 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&accfree[qt * 2 + h]);  // all 128 columns read
-                    const float m0 = tile_max64_h(f0, sub0, a.nt), m1 = tile_max64_h(f1, sub0 + 1, a.nt);
-                    if (__any_sync(0xFFFFFFFFu, fmaxf(m0, m1) > st.b4)) {
-                        tile_update(st, m0, sub0);
-                        tile_update(st, m1, sub0 + 1);
+                    const uint32_t rel = (t - item.tile_begin) * kSubPerTile + 2u * h;
+                    const float k0 = key_of(tile_max64_h(f0, sub0, a.nt), rel);
+                    const float k1 = key_of(tile_max64_h(f1, sub0 + 1, a.nt), rel + 1);
+                    if (__any_sync(0xFFFFFFFFu, fmaxf(k0, k1) > kb[kTopSub - 1])) {
+                        key_insert(kb, k0);
+                        key_insert(kb, k1);
                     }
                     continue;
                 }
@@ -691,17 +731,31 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&accfree[qt * 2 + h]);  // this warp's 128 columns drained
                 if (tw && lane == 0) a.trace[16384 + k] = clock64();
-                if (__any_sync(0xFFFFFFFFu, m0 > st.b4)) tile_update(st, m0, sub0);
+                if (__any_sync(0xFFFFFFFFu, m0 > st.b[kTopSub - 1])) tile_update(st, m0, sub0);
                 subtile_scan(st, f0, f1, sub0 + 1, a.nt);
                 if (tw) {
                     __syncwarp();
-                    if (lane == 0) a.trace[20480 + k] = clock64() + (st.b1 > 1e30f ? 1 : 0);
+                    if (lane == 0) a.trace[20480 + k] = clock64() + (st.b[0] > 1e30f ? 1 : 0);
                 }
             }
             const uint32_t row = qt * 128u + quad * 32u + lane;  // 0..255 within the tile pair
-            float4* po = a.partial + (((uint64_t)u * kPartialSplit + h) * kQueryTilePair + row) * 2;
-            po[0] = make_float4(st.b1, st.b2, st.b3, st.b4);
-            po[1] = make_float4(__uint_as_float(st.t1), __uint_as_float(st.t2), __uint_as_float(st.t3), 0.0f);
+            float4* po = a.partial + (((uint64_t)u * kPartialSplit + h) * kQueryTilePair + row) * kPartialF4;
+            if constexpr (kF16) {  // keys -> (bound, absolute sub-tile) state
+#pragma unroll
+                for (int i = 0; i < kTopSub; ++i) st.b[i] = key_value(kb[i]);
+#pragma unroll
+                for (int i = 0; i < kTopSub - 1; ++i) st.t[i] = item.tile_begin * kSubPerTile + key_rel(kb[i]);
+            }
+            // 12 slots: b[0..kTopSub) then t[0..kTopSub-1) at slot 6
+            float w[4 * kPartialF4];
+#pragma unroll
+            for (int i = 0; i < 4 * kPartialF4; ++i) w[i] = 0.0f;
+#pragma unroll
+            for (int i = 0; i < kTopSub; ++i) w[i] = st.b[i];
+#pragma unroll
+            for (int i = 0; i < kTopSub - 1; ++i) w[6 + i] = __uint_as_float(st.t[i]);
+#pragma unroll
+            for (int i = 0; i < kPartialF4; ++i) po[i] = make_float4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
         }
     }
     tc_fence_before();
@@ -890,8 +944,8 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs a) {
     //   chain (four targets per lane, (cmp, index) key min), close the row if
     //   the exact winner beats B2 by the margin, else resolve T2 against B3,
     //   then T3 against B4; rows still open go to the full rescan
-    __shared__ uint32_t s_t[kMergeRows][3];
-    __shared__ float s_b[kMergeRows][3];
+    __shared__ uint32_t s_t[kMergeRows][kTopSub - 1];
+    __shared__ float s_b[kMergeRows][kTopSub - 1];
     const uint32_t tp = blockIdx.x / kMergeSlices, slice = blockIdx.x % kMergeSlices;
     if (tp >= a.hdr[1]) return;
     const uint32_t splits = a.hdr[3];
@@ -903,37 +957,41 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs a) {
     const uint32_t qi0 = a.tp_qi0[tp] + slice * kMergeRows;     // its query index within the pair
     const uint32_t r = threadIdx.x;
     if (r < nrows) {
-        float B[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-        uint32_t T[3] = {kNoTile, kNoTile, kNoTile};
+        // global top-6 over the splits: B[0..5] with sub-tiles T[0..4]; B[5]
+        // bounds everything below the fifth
+        float B[kTopSub];
+        uint32_t T[kTopSub - 1];
+#pragma unroll
+        for (int i = 0; i < kTopSub; ++i) B[i] = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < kTopSub - 1; ++i) T[i] = kNoTile;
         auto insert = [&](float v, uint32_t t) {
-            if (v > B[0]) {
-                B[3] = fmaxf(B[3], B[2]);
-                B[2] = B[1], T[2] = T[1];
-                B[1] = B[0], T[1] = T[0];
-                B[0] = v, T[0] = t;
-            } else if (v > B[1]) {
-                B[3] = fmaxf(B[3], B[2]);
-                B[2] = B[1], T[2] = T[1];
-                B[1] = v, T[1] = t;
-            } else if (v > B[2]) {
-                B[3] = fmaxf(B[3], B[2]);
-                B[2] = v, T[2] = t;
-            } else {
-                B[3] = fmaxf(B[3], v);
+            // sorted insert into the first five (branch-free shifts); what falls
+            // off the fifth only raises the bound B[5]
+            B[kTopSub - 1] = fmaxf(B[kTopSub - 1], fminf(B[kTopSub - 2], v));
+#pragma unroll
+            for (int i = kTopSub - 2; i >= 1; --i) {
+                const bool gp = v > B[i - 1], gi = v > B[i];
+                T[i] = gp ? T[i - 1] : (gi ? t : T[i]);
+                B[i] = gp ? B[i - 1] : (gi ? v : B[i]);
             }
+            if (v > B[0]) T[0] = t, B[0] = v;
         };
         for (uint32_t s = 0; s < splits * kPartialSplit; ++s) {
-            const float4* pp =
-                a.partial + (((uint64_t)tp * splits * kPartialSplit + s) * kQueryTilePair + slice * kMergeRows + r) * 2;
-            const float4 p = pp[0];
-            const float4 p2 = pp[1];
-            insert(p.x, __float_as_uint(p2.x));
-            insert(p.y, __float_as_uint(p2.y));
-            insert(p.z, __float_as_uint(p2.z));
-            B[3] = fmaxf(B[3], p.w);
+            const float4* pp = a.partial + (((uint64_t)tp * splits * kPartialSplit + s) * kQueryTilePair +
+                                            slice * kMergeRows + r) * kPartialF4;
+            float w[4 * kPartialF4];
+#pragma unroll
+            for (int i = 0; i < kPartialF4; ++i) {
+                const float4 v = pp[i];
+                w[4 * i] = v.x, w[4 * i + 1] = v.y, w[4 * i + 2] = v.z, w[4 * i + 3] = v.w;
+            }
+#pragma unroll
+            for (int i = 0; i < kTopSub - 1; ++i) insert(w[i], __float_as_uint(w[6 + i]));
+            B[kTopSub - 1] = fmaxf(B[kTopSub - 1], w[kTopSub - 1]);
         }
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
+        for (int c = 0; c < kTopSub - 1; ++c) {
             s_t[r][c] = T[c];
             s_b[r][c] = B[c + 1];
         }
@@ -961,7 +1019,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs a) {
         float dmin = INFINITY;
         bool done = !valid;
 #pragma unroll 1
-        for (int c = 0; c < 3; ++c) {
+        for (int c = 0; c < kTopSub - 1; ++c) {
             const uint32_t st = done ? kNoTile : s_t[row][c];
             if (st != kNoTile) {
 #pragma unroll
@@ -1362,7 +1420,10 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a) {
         uint32_t best = 1;
         float best_cost = 3.0e38f;
         const uint32_t smax = min(min(a.ntiles, 64u), ntp ? max(1u, a.nitems_cap / ntp) : 1u);
-        for (uint32_t sp = 1; sp <= smax; ++sp) {
+        // a unit spans at most kMaxUnitTiles target tiles (K3's sub-tile keys)
+        const uint32_t sp_min = (a.ntiles + kMaxUnitTiles - 1) / kMaxUnitTiles;
+        best = sp_min;
+        for (uint32_t sp = sp_min; sp <= smax; ++sp) {
             const float waves = (float)((ntp * sp + a.sms - 1) / a.sms);
             const float cost = waves * (float)((a.ntiles + sp - 1) / sp + 3u);
             if (cost < best_cost) best_cost = cost, best = sp;
@@ -1450,7 +1511,8 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     const uint32_t tp_per_pair = ceil_div_u(cap, kQueryTilePair);
     const uint32_t tp_max = npairs * tp_per_pair;
     const uint32_t rows_max = tp_max * kQueryTilePair;
-    const uint32_t nitems_cap = std::max<uint32_t>(2 * tp_max, std::min<uint32_t>(64 * tp_max, 64 * sms));
+    const uint32_t nitems_cap = std::max<uint32_t>(std::max<uint32_t>(2 * tp_max, tp_max * ceil_div_u(ntiles, kMaxUnitTiles)),
+                                                   std::min<uint32_t>(64 * tp_max, 64 * sms));
     const size_t item_off = (8 + 2 * (size_t)npairs + 3 * (size_t)tp_max + 3) & ~(size_t)3;
     const size_t words = item_off + 8 * (size_t)nitems_cap;
     uint32_t* dlist = nullptr;
@@ -1472,7 +1534,7 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     unsigned long long* keys;
     TRY(ws_arr(ctx, "tc.qbuf", (size_t)rows_max * kPackRowBytes, &qbuf));
     TRY(ws_arr(ctx, "tc.margin", rows_max, &margin));
-    TRY(ws_arr(ctx, "tc.partial", (size_t)nitems_cap * kPartialSplit * kQueryTilePair * 2, &partial));
+    TRY(ws_arr(ctx, "tc.partial", (size_t)nitems_cap * kPartialSplit * kQueryTilePair * kPartialF4, &partial));
     TRY(ws_arr(ctx, "tc.rescan", (size_t)3 * rows_max, &rescan));
     TRY(ws_arr(ctx, "tc.rcount", 1, &rcount));
     TRY(ws_arr(ctx, "tc.keys", rows_max, &keys));

@@ -81,11 +81,11 @@ def test_quantised_ties_across_subtiles(fnl, ref, metric):
 
 @pytest.mark.parametrize("metric", ["l2", "dot"])
 def test_duplicated_targets(fnl, ref, metric):
-    # every target appears 5 times, in different 64-target sub-tiles: the
-    # three candidate sub-tiles cannot settle it, so the rows are rescanned
-    # and the lowest of the five indices must win
-    base = ref.gen_random(1, 700, 24, 77).reshape(700, 24)
-    B = np.concatenate([base] * 5).reshape(50, 70, 24)
+    # every target appears 7 times, in different 64-target sub-tiles: the
+    # five candidate sub-tiles the merge resolves cannot settle it, so the
+    # rows are rescanned and the lowest of the seven indices must win
+    base = ref.gen_random(1, 500, 24, 77).reshape(500, 24)
+    B = np.concatenate([base] * 7).reshape(50, 70, 24)
     A = ref.gen_random(50, 70, 24, 78)
     nn_all(fnl, ref, A, B, metric)
     for backend in ("single", "hybrid", "tensor"):
