@@ -936,7 +936,7 @@ constexpr uint32_t kMergeThreads = 256;
 constexpr uint32_t kNoTile = 0xFFFFFFFFu;
 
 template <bool kL2, int DIM, int MODE>
-__global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs a) {
+__global__ void __launch_bounds__(kMergeThreads, 4) merge_kernel(MergeArgs a) {
     // phase 1 (thread per row): global top-4 of sub-tile maxima over the
     //   target splits / column halves -> candidates T1, T2, T3 and the bounds
     //   B2, B3, B4 on everything not yet resolved after 1, 2, 3 of them
