@@ -22,6 +22,11 @@ F1 = fnl.gen_random(32, 24, 48, 41)
 F2 = fnl.gen_random(32, 24, 48, 141)
 for be in ("single", "hybrid"):
     print(be, "d48", fnl.reciprocal_match(F1, F2, backend=be, metric="dot", stride=4)[0].shape[0])
+# ragged target count (3,500 = 54 x 64 + 44): the last sub-tile's padding masks
+G1 = fnl.gen_random(50, 70, 24, 51)
+G2 = fnl.gen_random(50, 70, 24, 151)
+for be in ("single", "tensor"):
+    print(be, "ragged", fnl.reciprocal_match(G1, G2, backend=be, metric="dot", stride=4)[0].shape[0])
 r = fnl.nn_tensor(D1, D2, metric="dot")
 print("dense", len(r["nearest"]))
 print("mutual", fnl.mutual_nn_exact(D1, D2, metric="dot").shape[0])
