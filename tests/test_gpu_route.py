@@ -106,6 +106,31 @@ def test_magnitudes(fnl, ref, metric, scale):
     nn_all(fnl, ref, A, B, metric)
 
 
+@pytest.mark.parametrize("metric", ["l2", "dot"])
+def test_binary16_accumulator_near_duplicates(fnl, ref, metric):
+    # K3 accumulates dot scores in binary16 (relative resolution ~2^-11):
+    # targets that differ by ~1e-4 relative are indistinguishable to it but
+    # not to the reference's fp32 chain; seven perturbed copies of every
+    # target, in different sub-tiles, must still resolve to the reference's
+    # winner (certified merge over five candidates, then the full rescan)
+    rng = np.random.default_rng(12)
+    base = ref.gen_random(1, 500, 24, 81).reshape(500, 24)
+    copies = [base * np.float32(1 + 1e-4 * k) + rng.normal(scale=3e-5, size=base.shape) for k in range(7)]
+    B = np.concatenate(copies).astype(np.float32).reshape(50, 70, 24)
+    A = ref.gen_random(50, 70, 24, 82)
+    nn_all(fnl, ref, A, B, metric)
+    for backend in ("single", "hybrid", "tensor"):
+        m1, r1 = fnl.reciprocal_match(A, B, backend=backend, metric=metric, stride=5)
+        if backend == "tensor":
+            r16 = np.vectorize(ref.to_half_round, otypes=[np.float32])
+            m2, r2 = ref.reciprocal_match(r16(A), r16(B), backend="single", metric=metric, stride=5)
+        else:
+            m2, r2 = ref.reciprocal_match(A, B, backend=backend, metric=metric, stride=5)
+        assert np.array_equal(m1, m2), backend
+    st = route_of(fnl, A, B, "single", metric)
+    assert st["tensor_route"] == 1 and st["near_tie_rows"] > 0
+
+
 def test_hybrid_castout_ties(fnl, ref):
     # distances clustered inside one binary16 ulp: the reference's fp16
     # cast-out makes them ties decided by index, far beyond any fp32 gap
