@@ -159,7 +159,8 @@ int fnl_reciprocal_match_batch(fnl_context* ctx, uint32_t npairs, const float* h
  * context stream except for one small convergence read per iteration.  For
  * speed, non-finite inputs are not rejected here (the host-buffer entry points
  * validate like the reference); they still take the route that keeps the
- * results identical to the reference's arithmetic on those values. */
+ * results identical to the reference's arithmetic on those values.  The maps
+ * must be 16-byte aligned (FNL_EINVAL otherwise). */
 int fnl_reciprocal_match_batch_device(fnl_context* ctx, uint32_t npairs, const float* d_d1,
                                       const float* d_d2, uint32_t h, uint32_t w, uint32_t dim,
                                       const fnl_match_config* cfg, int backend,

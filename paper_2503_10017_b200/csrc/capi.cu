@@ -631,6 +631,9 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
               const fnl_shard_spec* shard = nullptr) {
     TRY(check_cfg(cfg));
     if (!valid_backend(backend)) return fail(FNL_EINVAL, "reciprocal_match: unknown backend");
+    // the kernels read map rows with 16-byte vector loads
+    if ((reinterpret_cast<uintptr_t>(d_d1) | reinterpret_cast<uintptr_t>(d_d2)) & 15u)
+        return fail(FNL_EINVAL, "reciprocal_match: device maps must be 16-byte aligned");
     if (dim == 0 || h1 == 0 || w1 == 0 || h2 == 0 || w2 == 0)
         return fail(FNL_EINVAL, "FeatureMap: height, width and dim must all be >= 1");
     const bool hyb = backend_hybrid(backend, cfg->precision);

@@ -885,7 +885,17 @@ __device__ __forceinline__ void load_query(const uint8_t* qbuf, uint32_t grow, f
         for (int k = 0; k < 8; ++k) q[c0 + k] = __half2float(h[k]);
     }
 }
+// fp32 query row: 16-byte loads when the row is 16-byte aligned (dim a
+// multiple of 4 and an aligned map), else scalar
 __device__ __forceinline__ void load_query32(const float* row, uint32_t dim, float (&q)[kPackK]) {
+    if ((dim & 3u) == 0 && (reinterpret_cast<uintptr_t>(row) & 15u) == 0) {
+#pragma unroll
+        for (uint32_t c = 0; c < kPackK; c += 4) {
+            const float4 v = c < dim ? __ldg(reinterpret_cast<const float4*>(row + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            q[c] = v.x, q[c + 1] = v.y, q[c + 2] = v.z, q[c + 3] = v.w;
+        }
+        return;
+    }
 #pragma unroll
     for (uint32_t c = 0; c < kPackK; ++c) q[c] = c < dim ? __ldg(row + c) : 0.0f;
 }
