@@ -705,11 +705,16 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&accfree[qt * 2 + h]);  // all 128 columns read
+                    if (tw && lane == 0) a.trace[16384 + k] = clock64();
                     const uint32_t rel = (t - item.tile_begin) * kSubPerTile + 2u * h;
                     const float k0 = key_of(tile_max64_h(f0, sub0, a.nt), rel);
                     const float k1 = key_of(tile_max64_h(f1, sub0 + 1, a.nt), rel + 1);
                     if (__any_sync(0xFFFFFFFFu, fmaxf(k0, k1) > kb[kTopSub - 1])) {
                         key_insert2(kb, k0, k1);
+                    }
+                    if (tw) {
+                        __syncwarp();
+                        if (lane == 0) a.trace[20480 + k] = clock64() + (kb[0] > 1e30f ? 1 : 0);
                     }
                     continue;
                 }
