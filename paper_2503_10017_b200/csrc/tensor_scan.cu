@@ -249,7 +249,7 @@ struct GatherArgs {
     // 128-byte lines of the packed layout (3.9x DRAM over-fetch, round 1)
     const float* q32;
     uint64_t q32_pair_stride;
-    bool acc16;  // K3 accumulates in binary16 (dot only): add its rounding to the margin
+    bool acc16;  // K3 accumulates in binary16: add its first rounding to the margin
     const float* tmax_hi;  // per pair max target norm over channels 16..31 (acc16)
 };
 
@@ -342,6 +342,13 @@ __global__ void gather_kernel(GatherArgs a) {
             const float S = (qn + tn) * (qn + tn);
             m = ldexpf(A, -15) + (d + 2.0f) * ldexpf(S, -25) + ldexpf(tn * tn, -20) + (d + 2.0f) * ldexpf(qn * qn, -25);
             if (full) m += ldexpf(qn * tn, -10) + ldexpf(tn * tn, -11) + ldexpf(sd * (qn + tn), -24);
+            // binary16 accumulator: the first K step (channels 16..31) also holds
+            // the -|t|^2/2 terms when dim >= 14: |partial| <= |q_hi| |t_hi| + |t|^2/2
+            if (a.acc16) {
+                const float qh = sqrtf(sh) * 1.001f + ldexpf(sd, -24);
+                const float th = a.tmax_hi[pair] * 1.001f + ldexpf(sd, -24);
+                m += 1.001f * ldexpf(qh * th + 0.501f * tn * tn, -11) + ldexpf(1.0f, -23);
+            }
         }
         a.margin[drow] = 1.25f * m + 1e-30f;
     }
@@ -1570,7 +1577,7 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
         FNL_CUDA_TRY(cudaGetLastError());
     }
     // binary16 accumulators in K3 when the caller established they are safe
-    const bool acc16 = rs.acc16 != 0 && !l2;
+    const bool acc16 = rs.acc16 != 0;
     // ---- K2 gather
     {
         GatherArgs g{Q.data, Q.pair_bytes, ids, cap, d_active, d_slot_pair, d_slot_base, qbuf, margin,
@@ -1684,10 +1691,14 @@ bool tensor_route_ok(int mode, bool l2, uint32_t dim, float qmax_norm, float tma
 
 bool acc16_ok(bool l2, float qmax_norm, float tmax_norm) {
     static const bool off = getenv("FNL_TC_F16ACC") && atoi(getenv("FNL_TC_F16ACC")) == 0;
-    if (off || l2) return false;
-    // |partial sums| <= |q| |t| < 2^14: far inside binary16 (max 65504), so no
-    // score or partial sum saturates
-    return (double)qmax_norm * 1.001 * (double)tmax_norm * 1.001 < 16384.0;
+    if (off) return false;
+    // every score / partial sum stays below 2^14, far inside binary16 (max
+    // 65504): dot |q.t| <= |q| |t|; l2 |q.t - |t|^2/2| <= |q| |t| + |t|^2/2,
+    // with either map as the target side
+    const double q = (double)qmax_norm * 1.001, t = (double)tmax_norm * 1.001;
+    if (!l2) return q * t < 16384.0;
+    const double m = std::max(q, t);
+    return 1.5 * m * m < 16384.0;
 }
 
 int tensor_nn_dense(fnl_context* ctx, const float* d_q, uint32_t nq, const float* d_t, uint32_t nt,

@@ -89,8 +89,8 @@ enum ResolveMode : int {
 // the pass's query ids) and target map rows, npairs stacked maps each.
 struct ResolveSrc {
     int mode = kResolveRounded;
-    // K3 may accumulate in binary16 (dot metric, |q| |t| small enough that no
-    // partial sum saturates; see acc16_ok): certified with a wider margin
+    // K3 may accumulate in binary16 (norms small enough that no partial sum
+    // saturates; see acc16_ok): certified with a wider margin
     int acc16 = 0;
     const float* q32 = nullptr;
     uint64_t q32_pair_stride = 0;  // floats
@@ -104,8 +104,8 @@ struct ResolveSrc {
 bool tensor_route_ok(int mode, bool l2, uint32_t dim, float qmax_norm, float tmax_norm,
                      unsigned long long sat, unsigned long long bad);
 // binary16 accumulators are safe when every score / partial sum stays far
-// inside binary16 range: dot metric and max|q| max|t| < 2^14 (FNL_TC_F16ACC=0
-// turns them off)
+// inside binary16 range: max|q| max|t| < 2^14 (dot), 1.5 max(|q|,|t|)^2 < 2^14
+// (l2); FNL_TC_F16ACC=0 turns them off
 bool acc16_ok(bool l2, float qmax_norm, float tmax_norm);
 struct ShardPeers {
     long long* keys[kMaxShardPeers];
