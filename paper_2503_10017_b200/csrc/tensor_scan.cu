@@ -810,6 +810,7 @@ struct MergeArgs {
     uint32_t cap;
     ResolveSrc rs;              // kResolveFull: original fp32 rows
     bool acc16;                 // K3 scores are binary16 accumulations: + 2^-11 |bound|
+    bool prefilter;             // kResolveFull: binary16 prefilter before the fp32 rows
 };
 
 // sharded mode: this rank's winner key of output slot o -- a local store, or
@@ -1048,7 +1049,33 @@ __global__ void __launch_bounds__(kMergeThreads, 4) merge_kernel(MergeArgs a) {
 #pragma unroll 1
         for (int c = 0; c < kTopSub - 1; ++c) {
             const uint32_t st = done ? kNoTile : s_t[row][c];
-            if (st != kNoTile) {
+            if (MODE == kResolveFull && a.prefilter) {
+                // Full precision: a binary16 prefilter (the chain over the packed
+                // rows, 48 of 96 bytes per target) keeps only targets within 4E of
+                // the sub-tile's best approximation -- E bounds the input rounding
+                // and both chains and is inside the certification margin -- and
+                // only those read their fp32 rows
+                float da[kSubTile / 16];
+                float dam = INFINITY;
+#pragma unroll
+                for (uint32_t h = 0; h < kSubTile / 16; ++h) {
+                    const uint32_t t = st * kSubTile + h * 16 + hl;
+                    da[h] = (st != kNoTile && t < a.nt) ? packed_chain<kL2, DIM>(q, tm, t, a.dim) : INFINITY;
+                    dam = fminf(dam, da[h]);
+                }
+#pragma unroll
+                for (int o = 8; o > 0; o >>= 1) dam = fminf(dam, __shfl_xor_sync(0xFFFFFFFFu, dam, o));
+                const float thr = dam + 4.0f * (kL2 ? 2.0f * M : M);
+#pragma unroll
+                for (uint32_t h = 0; h < kSubTile / 16; ++h) {
+                    const uint32_t t = st * kSubTile + h * 16 + hl;
+                    if (st != kNoTile && t < a.nt && da[h] <= thr) {
+                        const float d = f32_chain<kL2, DIM>(q, t32 + (uint64_t)t * a.dim, a.dim);
+                        key = umin64(key, pack_key(d, t));
+                        dmin = fminf(dmin, d);
+                    }
+                }
+            } else if (st != kNoTile) {
 #pragma unroll
                 for (uint32_t h = 0; h < kSubTile; h += 16) {
                     const uint32_t t = st * kSubTile + h + hl;
@@ -1512,6 +1539,12 @@ int tensor_pack(fnl_context* ctx, const char* tag, const float* d_src, uint32_t 
     return FNL_OK;
 }
 
+// full-precision merge resolves through a binary16 prefilter (FNL_MERGE_PREFILTER=0: off)
+static bool merge_prefilter() {
+    static const bool on = !(getenv("FNL_MERGE_PREFILTER") && atoi(getenv("FNL_MERGE_PREFILTER")) == 0);
+    return on;
+}
+
 int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const uint32_t* ids, uint32_t cap,
                    const uint32_t* d_active, const uint8_t* d_done, const PackedMaps& T, uint32_t dim, bool l2,
                    uint32_t* out, uint32_t out_stride, float* min_dist, unsigned long long* d_near_ties,
@@ -1608,7 +1641,7 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     {
         MergeArgs m{partial, d_tp_pair, d_tp_row0, d_tp_qi0, d_hdr, d_active, margin, qbuf, T.data,
                     T.pair_bytes, nt, dim, out, min_dist, out_stride, rescan, rcount, d_near_ties, npairs, shard_keys,
-                    pp, ids, cap, rs, acc16};
+                    pp, ids, cap, rs, acc16, merge_prefilter()};
         ProfScope prof(ctx, FNL_KCLASS_MERGE);
         const uint32_t grid = tp_max * kMergeSlices;
         if (dim == 24) {
