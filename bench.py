@@ -457,13 +457,14 @@ def main_b200(args):
         "metric": METRIC_NAME, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None,
-        "dtype": "f16 in / fp32 accumulate (tensor cores); fp32 reference chain for the decision",
+        "dtype": "f16 in / f16 accumulate (tensor-core candidate scores, certified margin); fp32 reference chain for the decision",
         "data": "synthetic",
         "config": {"workload": "C2/C4: FastNN-Lite reciprocal matching of 512x384 d=24 pairs, stride 8 "
                                f"(3072 samples), T=10, convergence 0.99, dot metric, backend {args.backend} "
-                               "on the tcgen05 route (HybridCast: binary16 in / fp32 accumulate scores nominate "
-                               "candidate sub-tiles; the winner is decided by the reference chain in the "
-                               "backend's own arithmetic, so results are identical to the reference's)",
+                               "on the tcgen05 route (HybridCast: binary16-in tensor-core scores, accumulated "
+                               "in binary16 when the norms allow it, nominate candidate sub-tiles; the winner "
+                               "is decided by the reference chain in the backend's own arithmetic, so results "
+                               "are identical to the reference's)",
                    "pairs_per_gpu_per_step": B, "global_batch": B * world, "height": H, "width": W,
                    "dim": D, "stride": STRIDE, "backend": args.backend, "parallelism": f"pairs dp{world}",
                    "inputs": f"pool of {POOL} gen_random maps (seeds 1000..{1000 + POOL - 1}), pair k = "
@@ -484,7 +485,7 @@ def main_b200(args):
         "gpu_launches": int(timing["total_launches"]),
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_burst, "unit": "TFLOP/s",
                      "frac": (achieved / peak_burst) if achieved else None, "traffic": traffic,
-                     "kernel": "tc_scan_kernel (tcgen05 score + running argmax)",
+                     "kernel": "tc_scan_kernel (tcgen05 scores + running top-6 sub-tile maxima)",
                      "flop_per_score": FLOP_PER_SCORE, "peak_kind": f"{peak_kind} bf16 dense burst",
                      "frac_of_sustained": (achieved / peak_sust) if (achieved and peak_sust) else None,
                      "frac_of_spec": (achieved / SPEC_DENSE_F16_TFLOPS) if achieved else None,
