@@ -93,6 +93,9 @@ typedef struct {
     /* 1 when the run took the tensor route (K1 pack + tcgen05 K3 + certified
      * resolution), 0 when it ran on the CUDA-core exact scan K4 */
     uint32_t tensor_route;
+    /* NN query rows actually computed: query_rows minus the reverse queries
+     * answered from the run's reverse-NN memo (tensor route) */
+    uint64_t computed_query_rows;
 } fnl_run_stats;
 
 typedef struct fnl_context fnl_context;

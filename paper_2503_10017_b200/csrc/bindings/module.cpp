@@ -100,6 +100,7 @@ py::dict stats_dict(const fnl_run_stats& s) {
     d["near_tie_rows"] = s.near_tie_rows;
     d["rescan_rows"] = s.rescan_rows;
     d["tensor_route"] = s.tensor_route;
+    d["computed_query_rows"] = s.computed_query_rows;
     d["query_rows"] = s.query_rows;
     d["forward_nn_us"] = s.forward_nn_us;
     d["reverse_nn_us"] = s.reverse_nn_us;

@@ -875,6 +875,33 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
         return exact_nn(ctx, sa, cap, npairs, l2, hyb, fa);
     };
 
+    // reverse-NN memo (tensor route, one process; FNL_REV_MEMO=0 turns it off)
+    static const bool memo_env = !(getenv("FNL_REV_MEMO") && atoi(getenv("FNL_REV_MEMO")) == 0);
+    const bool memo = tc && !sharded && memo_env && samples > 0;
+    if (memo) {
+        TRY(dev_arr(ctx, "m.revcache", (size_t)npairs * p2, &m.rev_cache));
+        TRY(dev_arr(ctx, "m.revlist", pc, &m.rev_list));
+        TRY(dev_arr(ctx, "m.revout", pc, &m.rev_out));
+        TRY(dev_arr(ctx, "m.revn", npairs, &m.rev_n));
+        FNL_CUDA_TRY(cudaMemsetAsync(m.rev_cache, 0xFF, (size_t)npairs * p2 * 4, s));
+    }
+    auto reverse_pass = [&]() -> int {
+        if (!memo) return nn_pass(P2, p2, m.active_v, P1, p1, m.back);
+        ++call;
+        FNL_CUDA_TRY(cudaMemsetAsync(m.rev_n, 0, (size_t)npairs * 4, s));
+        FNL_CUDA_TRY(fnl::launch_rev_lookup(m, s));
+        fnl::ResolveSrc rs;
+        rs.mode = mode;
+        rs.acc16 = acc16;
+        rs.q32 = d_d2;
+        rs.q32_pair_stride = (uint64_t)p2 * dim;
+        rs.t32 = d_d1;
+        rs.t32_pair_stride = (uint64_t)p1 * dim;
+        TRY(fnl::tensor_nn_pass(ctx, npairs, T2, m.rev_list, cap, m.rev_n, m.done, T1, dim, l2, m.rev_out, cap,
+                                nullptr, near_ties, 0, 0, nullptr, nullptr, &rs));
+        FNL_CUDA_TRY(fnl::launch_rev_fill(m, s));
+        return FNL_OK;
+    };
     unsigned int* lag_done = nullptr;  // pinned [2]: n_done after iterations t-1, t
     cudaEvent_t* lag_ev = nullptr;
     if (tc) {
@@ -888,7 +915,7 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
     }
     for (uint32_t t = 1; t <= T && samples > 0; ++t) {
         timer.begin(kPhaseReverse);
-        TRY(nn_pass(P2, p2, m.active_v, P1, p1, m.back));
+        TRY(reverse_pass());
         timer.end();
         timer.begin(kPhaseHarvest);
         {
@@ -997,6 +1024,13 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
                 o.near_tie_rows = ties_h[p];
                 o.rescan_rows = ties_h[npairs + p];
                 o.tensor_route = 1;
+            }
+            o.computed_query_rows = o.query_rows;
+            if (memo) {
+                uint64_t rev_logical = 0;
+                for (const Call& k : calls)
+                    if (!k.fwd) rev_logical += k.nq;
+                o.computed_query_rows = o.query_rows - rev_logical + ps[fnl::kStatRevComputed];
             }
         }
     }

@@ -141,13 +141,29 @@ struct MatchState {
     uint32_t* n_pairs;            // [npairs]
     uint32_t* stats;              // [npairs][kStatWords] (see below)
     unsigned int* n_done;         // scalar
+    // reverse-NN memo (tensor route): NN in map 1 of every map-2 pixel already
+    // queried in this run, so a reverse pass only computes pixels it has not
+    // seen (the chains u -> v -> u' that have not converged mostly come back
+    // to a v of an earlier iteration)
+    uint32_t* rev_cache;          // [npairs][p2]: NN, or kRevUnknown / kRevPending
+    uint32_t* rev_list;           // [npairs][cap]: pixels this reverse pass computes
+    uint32_t* rev_n;              // [npairs]
+    uint32_t* rev_out;            // [npairs][cap]: their NN
 };
-// stats words per pair: converged, duplicates, iterations, history_len, history[FNL_MAX_ITERS]
+constexpr uint32_t kRevUnknown = 0xFFFFFFFFu, kRevPending = 0xFFFFFFFEu;
+// stats words per pair: converged, duplicates, iterations, history_len,
+// history[FNL_MAX_ITERS], reverse rows actually computed
 constexpr int kStatConverged = 0, kStatDups = 1, kStatIters = 2, kStatHistLen = 3, kStatHist = 4;
-constexpr int kStatWords = 4 + 64;
+constexpr int kStatRevComputed = 4 + 64;
+constexpr int kStatWords = 4 + 64 + 1;
 
 cudaError_t launch_match_init(const MatchState& m, cudaStream_t s);
 cudaError_t launch_harvest(const MatchState& m, uint32_t iteration, cudaStream_t s);
+// reverse-NN memo: back[i] from the memo where known; unseen pixels claimed
+// (once each) into rev_list / rev_n for the pass; then memo <- pass results
+// and back[i] <- memo for every active i
+cudaError_t launch_rev_lookup(const MatchState& m, cudaStream_t s);
+cudaError_t launch_rev_fill(const MatchState& m, cudaStream_t s);
 
 // confidence-thresholded compaction of finished MatchSets (in place, stable)
 struct ConfArgs {

@@ -233,6 +233,57 @@ __global__ void __launch_bounds__(kHarvestThreads) confidence_compact_kernel(Con
     }
 }
 
+// ---------------------------------------------------------------- reverse-NN memo
+__global__ void rev_lookup_kernel(MatchState m) {
+    const uint32_t p = blockIdx.y;
+    if (m.done[p]) return;
+    const uint32_t n = m.n_active[p];
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t* V = m.active_v + (size_t)p * m.cap;
+    uint32_t* cache = m.rev_cache + (size_t)p * m.p2;
+    bool claim = false;
+    uint32_t j = 0;
+    if (i < n) {
+        j = V[i];
+        const uint32_t c = cache[j];
+        if (c < kRevPending) m.back[(size_t)p * m.cap + i] = c;
+        else if (c == kRevUnknown) claim = atomicCAS(&cache[j], kRevUnknown, kRevPending) == kRevUnknown;
+    }
+    // warp-aggregated slot allocation in the pass's query list
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t ballot = __ballot_sync(0xFFFFFFFFu, claim);
+    if (ballot == 0) return;
+    uint32_t base = 0;
+    if (lane == (uint32_t)__ffs(ballot) - 1u) base = atomicAdd(&m.rev_n[p], (uint32_t)__popc(ballot));
+    base = __shfl_sync(0xFFFFFFFFu, base, __ffs(ballot) - 1);
+    if (claim) m.rev_list[(size_t)p * m.cap + base + __popc(ballot & ((1u << lane) - 1u))] = j;
+}
+
+__global__ void __launch_bounds__(kHarvestThreads) rev_fill_kernel(MatchState m) {
+    const uint32_t p = blockIdx.x;
+    if (m.done[p]) return;
+    const uint32_t nl = m.rev_n[p], n = m.n_active[p];
+    uint32_t* cache = m.rev_cache + (size_t)p * m.p2;
+    const uint32_t* L = m.rev_list + (size_t)p * m.cap;
+    const uint32_t* R = m.rev_out + (size_t)p * m.cap;
+    for (uint32_t k = threadIdx.x; k < nl; k += blockDim.x) cache[L[k]] = R[k];
+    __syncthreads();
+    const uint32_t* V = m.active_v + (size_t)p * m.cap;
+    uint32_t* B = m.back + (size_t)p * m.cap;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) B[i] = cache[V[i]];
+    if (threadIdx.x == 0) m.stats[(size_t)p * kStatWords + kStatRevComputed] += nl;
+}
+
+cudaError_t launch_rev_lookup(const MatchState& m, cudaStream_t s) {
+    const uint32_t n = m.cap > 0 ? m.cap : 1;
+    rev_lookup_kernel<<<dim3((n + 255) / 256, m.npairs), 256, 0, s>>>(m);
+    return cudaGetLastError();
+}
+cudaError_t launch_rev_fill(const MatchState& m, cudaStream_t s) {
+    rev_fill_kernel<<<m.npairs, kHarvestThreads, 0, s>>>(m);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_confidence_compact(const ConfArgs& a, uint32_t npairs, cudaStream_t s) {
     if (npairs == 0) return cudaSuccess;
     confidence_compact_kernel<<<npairs, kHarvestThreads, 0, s>>>(a);

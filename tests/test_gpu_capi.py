@@ -26,7 +26,7 @@ class RunStats(ctypes.Structure):
                 ("query_rows", ctypes.c_uint64), ("subsample_us", ctypes.c_double),
                 ("forward_nn_us", ctypes.c_double), ("reverse_nn_us", ctypes.c_double),
                 ("harvest_us", ctypes.c_double), ("rescan_rows", ctypes.c_uint64),
-                ("tensor_route", ctypes.c_uint32)]
+                ("tensor_route", ctypes.c_uint32), ("computed_query_rows", ctypes.c_uint64)]
 
 
 @pytest.fixture(scope="module")
