@@ -214,3 +214,18 @@ def test_mutual_nn_errors_match_reference(fnl, ref):
         assert str(ours.value) == str(theirs.value)
     with pytest.raises(ValueError, match="non-finite"):
         fnl.mutual_nn_tensor(A, bad)
+
+
+def test_reverse_memo_saves_rows_and_keeps_matchsets(fnl, ref):
+    # the reverse-NN memo answers repeated reverse queries without a scan: the
+    # rows actually scored drop below the reference's query rows while every
+    # MatchSet stays the reference's
+    D1 = np.stack([ref.gen_random(64, 48, 24, 300 + i) for i in range(4)])
+    D2 = np.stack([ref.gen_random(64, 48, 24, 400 + i) for i in range(4)])
+    pairs, counts, stats = fnl.reciprocal_match_batch(D1, D2, backend="single", metric="dot")
+    for i, st in enumerate(stats):
+        want, _ = ref.reciprocal_match(D1[i], D2[i], backend="single", metric="dot")
+        assert np.array_equal(pairs[i][: counts[i]], want), i
+        assert st["tensor_route"] == 1
+        assert st["computed_query_rows"] <= st["query_rows"]
+    assert sum(st["computed_query_rows"] for st in stats) < sum(st["query_rows"] for st in stats)
