@@ -635,7 +635,8 @@ def bench_c5(fnl, world, rank, local, backend, reps=3):
     ms = e0.elapsed_time(e1) / reps
     ms = allreduce([ms], op=__import__("torch").distributed.ReduceOp.MAX)[0] if world > 1 else ms
     rows = stats[0]["query_rows"]
-    flops = FLOP_PER_SCORE * C5_H * C5_W * rows
+    computed = stats[0]["computed_query_rows"]  # reverse queries answered by the memo excluded
+    flops = FLOP_PER_SCORE * C5_H * C5_W * computed
     peer = None
     if world > 1:
         # the same pair with the peer-memory transport (keys pushed by the merge
@@ -677,7 +678,7 @@ def bench_c5(fnl, world, rank, local, backend, reps=3):
                         f"({((C5_H + 7) // 8) * ((C5_W + 7) // 8)} samples), dot, backend {backend}, target columns "
                         f"sharded over {world} rank(s), int64 MIN all-reduce of (dist, index) keys per NN pass",
             "shards": world, "ms_per_pair": round(ms, 3), "pairs_per_s": round(1000.0 / ms, 2),
-            "query_rows": int(rows), "iterations": int(stats[0]["iterations"]),
+            "query_rows": int(rows), "computed_query_rows": int(computed), "iterations": int(stats[0]["iterations"]),
             "matches": int(counts[0].item()),
             "aggregate_tflops": round(flops / (ms / 1e3) / 1e12, 1), "peer_memory": peer, "parity": parity}
 

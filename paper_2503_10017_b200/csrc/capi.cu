@@ -789,8 +789,10 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
         FNL_CUDA_TRY(cudaMemsetAsync(barrier_err, 0, 4, s));
     }
     uint32_t peer_pass = 0;
+    // d_count: per-pair query counts of the pass (default: the active counts)
     auto nn_pass = [&](const Prepared& Q, uint32_t qrows, const uint32_t* ids, const Prepared& Tm,
-                       uint32_t nt, uint32_t* out) -> int {
+                       uint32_t nt, uint32_t* out, const uint32_t* d_count = nullptr) -> int {
+        if (!d_count) d_count = m.n_active;
         if (tc) {
             const bool fwd = qrows == p1 && ids == m.active_u;
             const fnl::PackedMaps& TQ = fwd ? T1 : T2;
@@ -804,7 +806,7 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
             rs.t32_pair_stride = (uint64_t)(fwd ? p2 : p1) * dim;
             ++call;
             if (!sharded)
-                return fnl::tensor_nn_pass(ctx, npairs, TQ, ids, cap, m.n_active, m.done, TT, dim, l2, out, cap,
+                return fnl::tensor_nn_pass(ctx, npairs, TQ, ids, cap, d_count, m.done, TT, dim, l2, out, cap,
                                            nullptr, near_ties, 0, 0, nullptr, nullptr, &rs);            // target shard of this rank: contiguous 256-target tiles
             const uint64_t tiles = ceil_div(nt, fnl::kTargetTileRows);
             const uint32_t tb = (uint32_t)(tiles * shard->rank / shard->count);
@@ -823,19 +825,19 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
                     pp.keys[r] = reinterpret_cast<long long*>(shard->peer_keys[r]) + par * nkeys;
                 long long* own = reinterpret_cast<long long*>(shard->d_keys) + par * nkeys;
                 if (te > tb)
-                    TRY(fnl::tensor_nn_pass(ctx, npairs, TQ, ids, cap, m.n_active, m.done, TT, dim, l2, out, cap,
+                    TRY(fnl::tensor_nn_pass(ctx, npairs, TQ, ids, cap, d_count, m.done, TT, dim, l2, out, cap,
                                             nullptr, near_ties, tb, te, own, &pp, &rs));
                 const uint64_t seq = ++*shard->barrier_seq;
                 TRY(fnl::tensor_shard_barrier(ctx, reinterpret_cast<unsigned int* const*>(shard->peer_flags),
                                               shard->count,
                                               reinterpret_cast<unsigned int*>(shard->peer_flags[shard->rank]),
                                               (unsigned int)(seq * shard->count), barrier_err));
-                TRY(fnl::tensor_shard_finalize(ctx, npairs, own, cap, m.n_active, m.done, out));
+                TRY(fnl::tensor_shard_finalize(ctx, npairs, own, cap, d_count, m.done, out));
                 return fnl::tensor_shard_reset(ctx, own, nkeys);
             }
             TRY(fnl::tensor_shard_reset(ctx, reinterpret_cast<long long*>(shard->d_keys), nkeys));
             if (te > tb)
-                TRY(fnl::tensor_nn_pass(ctx, npairs, TQ, ids, cap, m.n_active, m.done, TT, dim, l2, out, cap,
+                TRY(fnl::tensor_nn_pass(ctx, npairs, TQ, ids, cap, d_count, m.done, TT, dim, l2, out, cap,
                                         nullptr, near_ties, tb, te,
                                         reinterpret_cast<long long*>(shard->d_keys), nullptr, &rs));
             if (shard->comm) {
@@ -845,7 +847,7 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
                 return fail(FNL_ERUNTIME, "sharded reciprocal_match: key reduction callback failed");
             }
             return fnl::tensor_shard_finalize(ctx, npairs, reinterpret_cast<const long long*>(shard->d_keys), cap,
-                                              m.n_active, m.done, out);
+                                              d_count, m.done, out);
         }
         fnl::ScanArgs sa{};
         sa.qmap = Q.data;
@@ -877,7 +879,9 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
 
     // reverse-NN memo (tensor route, one process; FNL_REV_MEMO=0 turns it off)
     static const bool memo_env = !(getenv("FNL_REV_MEMO") && atoi(getenv("FNL_REV_MEMO")) == 0);
-    const bool memo = tc && !sharded && memo_env && samples > 0;
+    // (the claimant lists are built in entry order, so every rank of a
+    // sharded run queries the same rows in the same slots)
+    const bool memo = tc && memo_env && samples > 0;
     if (memo) {
         TRY(dev_arr(ctx, "m.revcache", (size_t)npairs * p2, &m.rev_cache));
         TRY(dev_arr(ctx, "m.revlist", pc, &m.rev_list));
@@ -887,18 +891,9 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
     }
     auto reverse_pass = [&]() -> int {
         if (!memo) return nn_pass(P2, p2, m.active_v, P1, p1, m.back);
-        ++call;
         FNL_CUDA_TRY(cudaMemsetAsync(m.rev_n, 0, (size_t)npairs * 4, s));
         FNL_CUDA_TRY(fnl::launch_rev_lookup(m, s));
-        fnl::ResolveSrc rs;
-        rs.mode = mode;
-        rs.acc16 = acc16;
-        rs.q32 = d_d2;
-        rs.q32_pair_stride = (uint64_t)p2 * dim;
-        rs.t32 = d_d1;
-        rs.t32_pair_stride = (uint64_t)p1 * dim;
-        TRY(fnl::tensor_nn_pass(ctx, npairs, T2, m.rev_list, cap, m.rev_n, m.done, T1, dim, l2, m.rev_out, cap,
-                                nullptr, near_ties, 0, 0, nullptr, nullptr, &rs));
+        TRY(nn_pass(P2, p2, m.rev_list, P1, p1, m.rev_out, m.rev_n));
         FNL_CUDA_TRY(fnl::launch_rev_fill(m, s));
         return FNL_OK;
     };

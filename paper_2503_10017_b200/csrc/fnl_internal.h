@@ -145,12 +145,12 @@ struct MatchState {
     // queried in this run, so a reverse pass only computes pixels it has not
     // seen (the chains u -> v -> u' that have not converged mostly come back
     // to a v of an earlier iteration)
-    uint32_t* rev_cache;          // [npairs][p2]: NN, or kRevUnknown / kRevPending
+    uint32_t* rev_cache;          // [npairs][p2]: NN, kRevUnknown, or 2^31 | claiming entry
     uint32_t* rev_list;           // [npairs][cap]: pixels this reverse pass computes
     uint32_t* rev_n;              // [npairs]
     uint32_t* rev_out;            // [npairs][cap]: their NN
 };
-constexpr uint32_t kRevUnknown = 0xFFFFFFFFu, kRevPending = 0xFFFFFFFEu;
+constexpr uint32_t kRevUnknown = 0xFFFFFFFFu;
 // stats words per pair: converged, duplicates, iterations, history_len,
 // history[FNL_MAX_ITERS], reverse rows actually computed
 constexpr int kStatConverged = 0, kStatDups = 1, kStatIters = 2, kStatHistLen = 3, kStatHist = 4;
@@ -160,8 +160,8 @@ constexpr int kStatWords = 4 + 64 + 1;
 cudaError_t launch_match_init(const MatchState& m, cudaStream_t s);
 cudaError_t launch_harvest(const MatchState& m, uint32_t iteration, cudaStream_t s);
 // reverse-NN memo: back[i] from the memo where known; unseen pixels claimed
-// (once each) into rev_list / rev_n for the pass; then memo <- pass results
-// and back[i] <- memo for every active i
+// (once each, by their lowest entry) into rev_list / rev_n in entry order for
+// the pass; then memo <- pass results and back[i] <- memo for every active i
 cudaError_t launch_rev_lookup(const MatchState& m, cudaStream_t s);
 cudaError_t launch_rev_fill(const MatchState& m, cudaStream_t s);
 

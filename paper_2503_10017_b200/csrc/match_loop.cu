@@ -234,29 +234,45 @@ __global__ void __launch_bounds__(kHarvestThreads) confidence_compact_kernel(Con
 }
 
 // ---------------------------------------------------------------- reverse-NN memo
-__global__ void rev_lookup_kernel(MatchState m) {
+// rev_cache[j]: the NN of map-2 pixel j once known (< 2^31), kRevUnknown, or
+// 2^31 | i while active entry i is the lowest one asking for j in this pass.
+// Lookup: known pixels answer back[i] at once; unknown ones take the minimum
+// claimant by atomicMin.  Compaction: the claimants, in entry order (block
+// scans, so every rank of a sharded run builds the same list), form the pass's
+// query list.  Fill: results into the memo, back[i] for every active entry.
+constexpr uint32_t kRevClaim = 0x80000000u;
+
+__global__ void rev_claim_kernel(MatchState m) {
     const uint32_t p = blockIdx.y;
     if (m.done[p]) return;
-    const uint32_t n = m.n_active[p];
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    const uint32_t* V = m.active_v + (size_t)p * m.cap;
+    if (i >= m.n_active[p]) return;
+    const uint32_t j = m.active_v[(size_t)p * m.cap + i];
     uint32_t* cache = m.rev_cache + (size_t)p * m.p2;
-    bool claim = false;
-    uint32_t j = 0;
-    if (i < n) {
-        j = V[i];
-        const uint32_t c = cache[j];
-        if (c < kRevPending) m.back[(size_t)p * m.cap + i] = c;
-        else if (c == kRevUnknown) claim = atomicCAS(&cache[j], kRevUnknown, kRevPending) == kRevUnknown;
+    const uint32_t c = cache[j];
+    if (c < kRevClaim) m.back[(size_t)p * m.cap + i] = c;
+    else atomicMin(&cache[j], kRevClaim | i);
+}
+
+__global__ void __launch_bounds__(kHarvestThreads) rev_compact_kernel(MatchState m) {
+    __shared__ uint32_t warp_tot[33];
+    const uint32_t p = blockIdx.x;
+    if (m.done[p]) return;
+    const uint32_t n = m.n_active[p];
+    const uint32_t* V = m.active_v + (size_t)p * m.cap;
+    const uint32_t* cache = m.rev_cache + (size_t)p * m.p2;
+    uint32_t* L = m.rev_list + (size_t)p * m.cap;
+    uint32_t kept = 0;
+    for (uint32_t c0 = 0; c0 < n; c0 += kHarvestThreads) {
+        const uint32_t i = c0 + threadIdx.x;
+        const uint32_t j = i < n ? V[i] : 0u;
+        const bool claim = i < n && cache[j] == (kRevClaim | i);
+        uint32_t total;
+        const uint32_t off = block_scan(claim ? 1u : 0u, warp_tot, total);
+        if (claim) L[kept + off] = j;
+        kept += total;
     }
-    // warp-aggregated slot allocation in the pass's query list
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t ballot = __ballot_sync(0xFFFFFFFFu, claim);
-    if (ballot == 0) return;
-    uint32_t base = 0;
-    if (lane == (uint32_t)__ffs(ballot) - 1u) base = atomicAdd(&m.rev_n[p], (uint32_t)__popc(ballot));
-    base = __shfl_sync(0xFFFFFFFFu, base, __ffs(ballot) - 1);
-    if (claim) m.rev_list[(size_t)p * m.cap + base + __popc(ballot & ((1u << lane) - 1u))] = j;
+    if (threadIdx.x == 0) m.rev_n[p] = kept;
 }
 
 __global__ void __launch_bounds__(kHarvestThreads) rev_fill_kernel(MatchState m) {
@@ -276,7 +292,8 @@ __global__ void __launch_bounds__(kHarvestThreads) rev_fill_kernel(MatchState m)
 
 cudaError_t launch_rev_lookup(const MatchState& m, cudaStream_t s) {
     const uint32_t n = m.cap > 0 ? m.cap : 1;
-    rev_lookup_kernel<<<dim3((n + 255) / 256, m.npairs), 256, 0, s>>>(m);
+    rev_claim_kernel<<<dim3((n + 255) / 256, m.npairs), 256, 0, s>>>(m);
+    rev_compact_kernel<<<m.npairs, kHarvestThreads, 0, s>>>(m);
     return cudaGetLastError();
 }
 cudaError_t launch_rev_fill(const MatchState& m, cudaStream_t s) {
