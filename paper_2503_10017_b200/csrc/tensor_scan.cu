@@ -364,8 +364,20 @@ __global__ void gather_kernel(GatherArgs a) {
 struct TcItem {
     uint32_t pair, qrow0, tile_begin, tile_end;  // qrow0: first gathered row (multiple of 256)
     uint32_t nvalid;                             // real query rows in the tile pair (<= 256)
-    uint32_t pad0, pad1, pad2;
+    uint32_t dual;  // nvalid <= 128: both query tiles score the same 128 rows, query tile 0
+                    // over the first half of the tile range, query tile 1 over the second
+    uint32_t pad1, pad2;
 };
+// a tile pair runs in dual mode when its second query tile would be all padding
+__host__ __device__ __forceinline__ bool tp_dual(uint32_t nvalid) { return nvalid <= kTileRows; }
+// dual mode: steps of a unit, and the first tile of query tile 1
+__device__ __forceinline__ uint32_t unit_steps(const TcItem& it) {
+    const uint32_t n = it.tile_end - it.tile_begin;
+    return it.dual ? (n + 1) / 2 : n;
+}
+__device__ __forceinline__ uint32_t unit_mid(const TcItem& it) {
+    return it.tile_begin + (it.tile_end - it.tile_begin + 1) / 2;
+}
 
 struct TcArgs {
     const uint8_t* qbuf;
@@ -403,7 +415,8 @@ constexpr int kEpiWarps = 16;
 constexpr int kFirstEpiWarp = 3;
 constexpr int kScanThreads = (kFirstEpiWarp + kEpiWarps) * 32;
 constexpr uint32_t kSmemA = 2 * kTileBytes;                  // 16 KB: two query tiles
-constexpr uint32_t kSmemB = kStages * kBTileBytes;           // 64 KB ring
+constexpr uint32_t kStageBytes = 2 * kBTileBytes;            // a stage holds two B tiles (dual mode)
+constexpr uint32_t kSmemB = kStages * kStageBytes;           // 128 KB ring
 constexpr uint32_t kSmemBars = (2 * kStages + 8 + 2 + 2) * 8;
 // A double buffered (next unit's queries load under the current unit); padded
 // past half the SM's shared memory so no second CTA co-resides and spins in
@@ -548,7 +561,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint32_t tmem_slot;
     uint8_t* sA = smem;                  // [2][16 KB]
-    uint8_t* sB = smem + 2 * kSmemA;     // [kStages][16 KB]
+    uint8_t* sB = smem + 2 * kSmemA;     // [kStages][2][16 KB]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kSmemA + kSmemB);
     uint64_t* full = bars;                     // [kStages]  B tile landed
     uint64_t* empty = bars + kStages;          // [kStages]  both query tiles' MMAs on the slot retired
@@ -601,13 +614,19 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
             }
             __syncwarp();
             const uint8_t* tbase = a.tmap + (uint64_t)item.pair * a.t_pair_bytes;
-            for (uint32_t t = item.tile_begin; t < item.tile_end; ++t, ++k) {
+            const uint32_t steps = unit_steps(item), tmid = unit_mid(item);
+            for (uint32_t st = 0; st < steps; ++st, ++k) {
                 const uint32_t s = k % kStages;
+                const uint32_t t0 = item.tile_begin + st, t1 = tmid + st;
+                const bool two = item.dual && t1 < item.tile_end;
                 mbar_wait(&empty[s], ((k / kStages) & 1u) ^ 1u);
                 if (trace && lane == 0 && k < 4096) a.trace[k] = clock64();
                 if (elect_one()) {
-                    mbar_expect_tx(&full[s], kBTileBytes);
-                    bulk_g2s(sB + s * kBTileBytes, tbase + (uint64_t)t * kBTileBytes, kBTileBytes, &full[s]);
+                    mbar_expect_tx(&full[s], two ? 2 * kBTileBytes : kBTileBytes);
+                    bulk_g2s(sB + s * kStageBytes, tbase + (uint64_t)t0 * kBTileBytes, kBTileBytes, &full[s]);
+                    if (two)
+                        bulk_g2s(sB + s * kStageBytes + kBTileBytes, tbase + (uint64_t)t1 * kBTileBytes, kBTileBytes,
+                                 &full[s]);
                 }
                 __syncwarp();
             }
@@ -622,11 +641,11 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
         uint32_t k = 0, i = 0, kq = 0;  // kq: tiles this query tile's chains were issued for
         for (uint32_t u = blockIdx.x; u < nitems; u += G, ++i) {
             const TcItem item = a.items[u];
-            const uint32_t nt_unit = item.tile_end - item.tile_begin;
+            const uint32_t nt_unit = unit_steps(item);
             const uint32_t ab = i & 1u;
             mbar_wait(&afull[ab], (i >> 1) & 1u);
             tc_fence_after();
-            if (qt * 128u >= item.nvalid) {
+            if (qt * 128u >= item.nvalid && !item.dual) {
                 // an all-padding query tile (the last tile pair of a pass with
                 // n % 256 <= 128 live rows): no MMAs, so its chains do not
                 // compete for the tensor pipe; the B slots and the query buffer
@@ -641,12 +660,21 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
                 __syncwarp();
                 continue;
             }
-            const uint64_t ad = umma_desc(smem_addr(sA + ab * kSmemA + qt * kTileBytes));
-            for (uint32_t t = 0; t < nt_unit; ++t, ++k, ++kq) {
+            // dual mode: query tile 1 scores query tile 0's rows against the stage's
+            // second B tile (the second half of the unit's tile range)
+            const bool q1dual = item.dual && qt == 1;
+            const uint64_t ad = umma_desc(smem_addr(sA + ab * kSmemA + (item.dual ? 0u : qt * kTileBytes)));
+            const uint32_t tmid = unit_mid(item);
+            for (uint32_t t = 0; t < nt_unit; ++t, ++k) {
                 const uint32_t s = k % kStages;
                 if (trace && qt == 0 && lane == 0 && k < 4096) a.trace[4096 + k] = clock64();
                 mbar_wait(&full[s], (k / kStages) & 1u);
-                const uint64_t bd = umma_desc(b_addr + s * kBTileBytes);
+                if (q1dual && tmid + t >= item.tile_end) {  // odd range: no second tile on the last step
+                    if (elect_one()) mbar_arrive(&empty[s]);
+                    __syncwarp();
+                    continue;
+                }
+                const uint64_t bd = umma_desc(b_addr + s * kStageBytes + (q1dual ? kBTileBytes : 0u));
 #pragma unroll
                 for (uint32_t h = 0; h < 2; ++h) {
                     // each 128-target half of the tile is its own accumulator chain,
@@ -670,6 +698,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
                     }
                     __syncwarp();
                 }
+                ++kq;
             }
             if (elect_one()) tc_commit(&afree[ab]);  // this issuer no longer reads this unit's query tile
             __syncwarp();
@@ -692,9 +721,15 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
             float kb[kTopSub];  // kF16: top-6 keys
 #pragma unroll
             for (int i = 0; i < kTopSub; ++i) kb[i] = key_of(-INFINITY, 0);
-            const bool warp_real = qt * 128u + quad * 32u < item.nvalid;  // else all rows padding
-            const bool tile_live = qt * 128u < item.nvalid;                // else no MMAs were issued
-            for (uint32_t t = item.tile_begin; t < item.tile_end && tile_live; ++t, ++k) {
+            // dual mode: query tile 1 holds query tile 0's rows and the second
+            // half of the unit's targets
+            const bool q1dual = item.dual && qt == 1;
+            const uint32_t qrow_base = item.dual ? 0u : qt * 128u;
+            const bool warp_real = qrow_base + quad * 32u < item.nvalid;  // else all rows padding
+            const bool tile_live = qrow_base < item.nvalid;                // else no MMAs were issued
+            const uint32_t t_first = q1dual ? unit_mid(item) : item.tile_begin;
+            const uint32_t t_last = item.dual && qt == 0 ? unit_mid(item) : item.tile_end;
+            for (uint32_t t = t_first; t < t_last && tile_live; ++t, ++k) {
                 mbar_wait(&tfull[qt * 2 + h], k & 1u);
                 const bool tw = trace && warp == kFirstEpiWarp && k < 4096;
                 if (tw && lane == 0) a.trace[12288 + k] = clock64();
@@ -1005,9 +1040,13 @@ __global__ void __launch_bounds__(kMergeThreads, 4) merge_kernel(MergeArgs a) {
             }
             if (v > B[0]) T[0] = t, B[0] = v;
         };
-        for (uint32_t s = 0; s < splits * kPartialSplit; ++s) {
-            const float4* pp = a.partial + (((uint64_t)tp * splits * kPartialSplit + s) * kQueryTilePair +
-                                            slice * kMergeRows + r) * kPartialF4;
+        // dual tile pairs (<= 128 rows): query tile 1 scored the same rows over
+        // the second half of each unit's targets, in partial rows 128..255
+        const uint32_t nsrc = tp_dual(tp_rows) ? 2u : 1u;
+        for (uint32_t s = 0; s < splits * kPartialSplit * nsrc; ++s) {
+            const uint32_t sp = s % (splits * kPartialSplit), hi = s / (splits * kPartialSplit);
+            const float4* pp = a.partial + (((uint64_t)tp * splits * kPartialSplit + sp) * kQueryTilePair +
+                                            hi * kTileRows + slice * kMergeRows + r) * kPartialF4;
             float w[4 * kPartialF4];
 #pragma unroll
             for (int i = 0; i < kPartialF4; ++i) {
@@ -1503,7 +1542,8 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a) {
         it.tile_begin = a.tile_begin + sp * per;
         it.tile_end = a.tile_begin + min(a.ntiles, (sp + 1) * per);
         it.nvalid = min(kQueryTilePair, a.n_active[pair] - qi0);
-        it.pad0 = it.pad1 = it.pad2 = 0;
+        it.dual = tp_dual(it.nvalid) ? 1u : 0u;
+        it.pad1 = it.pad2 = 0;
         a.items[u] = it;
     }
 }
