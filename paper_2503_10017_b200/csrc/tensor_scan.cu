@@ -63,8 +63,20 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
 // kind::f16 instruction descriptor: A/B fp16, D fp32, both K-major, M=128, N=128.
 constexpr uint32_t kIdescF16M128N128 = (1u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
 
+// gathered query tiles (qbuf, K3's A operand): row-group-major, 512 B per 8 rows
 __host__ __device__ __forceinline__ uint64_t packed_offset(uint32_t row, uint32_t chunk) {
     return (uint64_t)(row >> 3) * 512u + chunk * 128u + (row & 7u) * 16u;
+}
+// packed maps (K3's B operand): chunk-major per 256-row tile, cpr chunks stored
+__host__ __device__ __forceinline__ uint64_t map_offset(uint32_t row, uint32_t chunk, uint32_t cpr) {
+    return (uint64_t)(row >> 8) * cpr * kChunkBytes + chunk * kChunkBytes + ((row >> 3) & 31u) * 128u +
+           (row & 7u) * 16u;
+}
+// B-operand descriptor of the chunk-major layout: LBO 4 KB (next chunk), SBO
+// 128 B (next 8-row group)
+__device__ __forceinline__ uint64_t umma_desc_b(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(kChunkBytes >> 4) << 16) | ((uint64_t)(128u >> 4) << 32) |
+           (1ull << 46);
 }
 
 __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
@@ -91,6 +103,7 @@ struct PackArgs {
     unsigned long long* bad;         // per pair first non-finite flat index
     unsigned long long* sat;         // per pair saturation count
     float* max_norm_hi;              // per pair: max norm over packed channels 16..31
+    uint32_t cpr;                    // stored chunks per row
 };
 
 constexpr int kPackThreads = 256;
@@ -144,12 +157,14 @@ __device__ __forceinline__ float pack_store(const PackArgs& a, uint8_t* dst, uin
             if (c == a.dim + 1) v[i] = lo;
         }
     }
-    uint4 out;
-    out.x = pack_half2(v[0], v[1]);
-    out.y = pack_half2(v[2], v[3]);
-    out.z = pack_half2(v[4], v[5]);
-    out.w = pack_half2(v[6], v[7]);
-    *reinterpret_cast<uint4*>(dst + packed_offset(row, chunk)) = out;
+    if (chunk < a.cpr) {  // chunks past cpr hold no data (zero for this map)
+        uint4 out;
+        out.x = pack_half2(v[0], v[1]);
+        out.y = pack_half2(v[2], v[3]);
+        out.z = pack_half2(v[4], v[5]);
+        out.w = pack_half2(v[6], v[7]);
+        *reinterpret_cast<uint4*>(dst + map_offset(row, chunk, a.cpr)) = out;
+    }
     return real ? ss : 0.0f;
 }
 
@@ -251,6 +266,7 @@ struct GatherArgs {
     uint64_t q32_pair_stride;
     bool acc16;  // K3 accumulates in binary16: add its first rounding to the margin
     const float* tmax_hi;  // per pair max target norm over channels 16..31 (acc16)
+    uint32_t qcpr;         // stored chunks per row of qmap
 };
 
 __global__ void gather_kernel(GatherArgs a) {
@@ -284,7 +300,9 @@ __global__ void gather_kernel(GatherArgs a) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) h[k] = __float2half_rn(half_round_sat(v[k], sat));
         } else {
-            val = *reinterpret_cast<const uint4*>(a.qmap + pair * a.qmap_pair_bytes + packed_offset(src_row, chunk));
+            val = chunk < a.qcpr ? *reinterpret_cast<const uint4*>(a.qmap + pair * a.qmap_pair_bytes +
+                                                                   map_offset(src_row, chunk, a.qcpr))
+                                 : make_uint4(0, 0, 0, 0);
             *reinterpret_cast<uint4*>(h) = val;
         }
         // query role: channels dim, dim+1 become 1.0 (l2) / 0 (dot)
@@ -383,6 +401,7 @@ struct TcArgs {
     const uint8_t* qbuf;
     const uint8_t* tmap;
     uint64_t t_pair_bytes;
+    uint32_t cpr;  // 16-B K chunks stored per target row (chunk-major tiles)
     uint32_t nt;
     const TcItem* items;
     const uint32_t* nitems;  // device item count (plan header)
@@ -596,6 +615,17 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
                      "r"(512));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
+    // chunks [cpr, 4) of every ring slot are K padding the loads never write:
+    // zero them once, visible to the async proxy before the first MMA
+    if (a.cpr < 4u) {
+        const uint32_t pad = (4u - a.cpr) * kChunkBytes / 16u;  // uint4 per slot
+        for (uint32_t i = threadIdx.x; i < 2u * kStages * pad; i += blockDim.x) {
+            const uint32_t slot = i / pad;
+            reinterpret_cast<uint4*>(sB + slot * kBTileBytes + a.cpr * kChunkBytes)[i - slot * pad] =
+                make_uint4(0u, 0u, 0u, 0u);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -614,6 +644,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
             }
             __syncwarp();
             const uint8_t* tbase = a.tmap + (uint64_t)item.pair * a.t_pair_bytes;
+            const uint32_t tb = a.cpr * kChunkBytes;  // stored bytes of one target tile
             const uint32_t steps = unit_steps(item), tmid = unit_mid(item);
             for (uint32_t st = 0; st < steps; ++st, ++k) {
                 const uint32_t s = k % kStages;
@@ -622,11 +653,9 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
                 mbar_wait(&empty[s], ((k / kStages) & 1u) ^ 1u);
                 if (trace && lane == 0 && k < 4096) a.trace[k] = clock64();
                 if (elect_one()) {
-                    mbar_expect_tx(&full[s], two ? 2 * kBTileBytes : kBTileBytes);
-                    bulk_g2s(sB + s * kStageBytes, tbase + (uint64_t)t0 * kBTileBytes, kBTileBytes, &full[s]);
-                    if (two)
-                        bulk_g2s(sB + s * kStageBytes + kBTileBytes, tbase + (uint64_t)t1 * kBTileBytes, kBTileBytes,
-                                 &full[s]);
+                    mbar_expect_tx(&full[s], two ? 2 * tb : tb);
+                    bulk_g2s(sB + s * kStageBytes, tbase + (uint64_t)t0 * tb, tb, &full[s]);
+                    if (two) bulk_g2s(sB + s * kStageBytes + kBTileBytes, tbase + (uint64_t)t1 * tb, tb, &full[s]);
                 }
                 __syncwarp();
             }
@@ -674,7 +703,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
                     __syncwarp();
                     continue;
                 }
-                const uint64_t bd = umma_desc(b_addr + s * kStageBytes + (q1dual ? kBTileBytes : 0u));
+                const uint64_t bd = umma_desc_b(b_addr + s * kStageBytes + (q1dual ? kBTileBytes : 0u));
 #pragma unroll
                 for (uint32_t h = 0; h < 2; ++h) {
                     // each 128-target half of the tile is its own accumulator chain,
@@ -683,15 +712,16 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
                     if (trace && qt == 0 && h == 0 && lane == 0 && k < 4096) a.trace[8192 + k] = clock64();
                     tc_fence_after();
                     if (elect_one()) {
-                        // half h starts 16 row groups (8 KB) further; K-step 1 starts 256 B
-                        // (two 8-channel chunks) further: +16 in descriptor units
-                        const uint64_t bh = bd + (uint64_t)h * (8192u >> 4);
+                        // half h starts 16 row groups (2 KB) further; K-step 1 starts two
+                        // chunks (8 KB) further in B and 256 B further in A
+                        const uint64_t bh = bd + (uint64_t)h * (2048u >> 4);
+                        constexpr uint64_t kB1 = (2u * kChunkBytes) >> 4;
                         if (kF16) {  // channels 16..31 first: the rounded partial sum is the smaller one
-                            tc_mma_f16(d + h * 128u, ad + 16u, bh + 16u, kIdesc, 0u);
+                            tc_mma_f16(d + h * 128u, ad + 16u, bh + kB1, kIdesc, 0u);
                             tc_mma_f16(d + h * 128u, ad, bh, kIdesc, 1u);
                         } else {
                             tc_mma_f16(d + h * 128u, ad, bh, kIdesc, 0u);
-                            tc_mma_f16(d + h * 128u, ad + 16u, bh + 16u, kIdesc, 1u);
+                            tc_mma_f16(d + h * 128u, ad + 16u, bh + kB1, kIdesc, 1u);
                         }
                         tc_commit(&tfull[qt * 2 + h]);
                         if (h == 1) tc_commit(&empty[s]);
@@ -830,6 +860,7 @@ struct MergeArgs {
     const uint8_t* qbuf;
     const uint8_t* tmap;
     uint64_t t_pair_bytes;
+    uint32_t tcpr;
     uint32_t nt;
     uint32_t dim;
     uint32_t* out;
@@ -863,12 +894,12 @@ __device__ __forceinline__ void shard_emit(long long* local, const ShardPeers& p
 // DIM == 0: runtime dim <= kPackK (all loops unrolled to kPackK, predicated).
 template <bool kL2, int DIM>
 __device__ __forceinline__ float packed_chain(const float (&q)[kPackK], const uint8_t* map, uint32_t row,
-                                              uint32_t dim) {
+                                              uint32_t dim, uint32_t cpr) {
     float acc = 0.0f;
 #pragma unroll
     for (uint32_t c0 = 0; c0 < kPackK; c0 += 8) {
-        if (DIM > 0 ? c0 < (uint32_t)DIM : c0 < dim) {
-            const uint4 raw = *reinterpret_cast<const uint4*>(map + packed_offset(row, c0 >> 3));
+        if (DIM > 0 ? c0 < (uint32_t)DIM : c0 < dim) {  // (dim <= 8 cpr: these chunks are stored)
+            const uint4 raw = *reinterpret_cast<const uint4*>(map + map_offset(row, c0 >> 3, cpr));
             const __half* h = reinterpret_cast<const __half*>(&raw);
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
@@ -967,9 +998,9 @@ __device__ __forceinline__ void mode_query(const uint8_t* qbuf, uint32_t grow, c
 // guarantees no saturation on this path).
 template <bool kL2, int DIM, int MODE>
 __device__ __forceinline__ float mode_chain(const float (&q)[kPackK], const uint8_t* tm, const float* t32,
-                                            uint32_t t, uint32_t dim) {
+                                            uint32_t t, uint32_t dim, uint32_t cpr) {
     if constexpr (MODE == kResolveFull) return f32_chain<kL2, DIM>(q, t32 + (uint64_t)t * dim, dim);
-    else return packed_chain<kL2, DIM>(q, tm, t, dim);
+    else return packed_chain<kL2, DIM>(q, tm, t, dim, cpr);
 }
 template <int MODE>
 __device__ __forceinline__ float mode_cmp(float d) {
@@ -1099,7 +1130,7 @@ __global__ void __launch_bounds__(kMergeThreads, 4) merge_kernel(MergeArgs a) {
 #pragma unroll
                 for (uint32_t h = 0; h < kSubTile / 16; ++h) {
                     const uint32_t t = st * kSubTile + h * 16 + hl;
-                    da[h] = (st != kNoTile && t < a.nt) ? packed_chain<kL2, DIM>(q, tm, t, a.dim) : INFINITY;
+                    da[h] = (st != kNoTile && t < a.nt) ? packed_chain<kL2, DIM>(q, tm, t, a.dim, a.tcpr) : INFINITY;
                     dam = fminf(dam, da[h]);
                 }
 #pragma unroll
@@ -1119,7 +1150,7 @@ __global__ void __launch_bounds__(kMergeThreads, 4) merge_kernel(MergeArgs a) {
                 for (uint32_t h = 0; h < kSubTile; h += 16) {
                     const uint32_t t = st * kSubTile + h + hl;
                     if (t < a.nt) {
-                        const float d = mode_chain<kL2, DIM, MODE>(q, tm, t32, t, a.dim);
+                        const float d = mode_chain<kL2, DIM, MODE>(q, tm, t32, t, a.dim, a.tcpr);
                         key = umin64(key, pack_key(mode_cmp<MODE>(d), t));
                         dmin = fminf(dmin, d);
                     }
@@ -1155,7 +1186,7 @@ __global__ void __launch_bounds__(kMergeThreads, 4) merge_kernel(MergeArgs a) {
                                 if (d == 0.0f)  // keys merge +-0: the winner's own zero (hybrid cast) or canonical
                                     d = MODE == kResolveHybrid
                                             ? mode_cmp<MODE>(mode_chain<kL2, DIM, MODE>(
-                                                  q, tm, t32, (uint32_t)(key & 0xFFFFFFFFull), a.dim))
+                                                  q, tm, t32, (uint32_t)(key & 0xFFFFFFFFull), a.dim, a.tcpr))
                                             : (kL2 ? 0.0f : -0.0f);
                                 a.min_dist[o] = d;
                             }
@@ -1184,6 +1215,7 @@ struct RescanArgs {
     const uint8_t* qbuf;
     const uint8_t* tmap;
     uint64_t t_pair_bytes;
+    uint32_t tcpr;
     uint32_t t_begin, nt;           // scanned target range [t_begin, nt)
     uint32_t dim;
     uint32_t chunk;                 // targets per work unit
@@ -1211,7 +1243,7 @@ __global__ void __launch_bounds__(kRescanThreads) rescan_kernel(RescanArgs a) {
         const uint32_t t0 = a.t_begin + (uint32_t)ch * a.chunk, t1 = min(a.nt, t0 + a.chunk);
         unsigned long long key = ~0ull;
         for (uint32_t t = t0 + threadIdx.x; t < t1; t += kRescanThreads)
-            key = umin64(key, pack_key(mode_cmp<MODE>(mode_chain<kL2, DIM, MODE>(q, tm, t32, t, a.dim)), t));
+            key = umin64(key, pack_key(mode_cmp<MODE>(mode_chain<kL2, DIM, MODE>(q, tm, t32, t, a.dim, a.tcpr)), t));
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) key = umin64(key, __shfl_xor_sync(0xFFFFFFFFu, key, o));
         if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = key;
@@ -1247,7 +1279,7 @@ __global__ void rescan_finish_kernel(RescanArgs a, uint32_t* out, float* min_dis
                     float q[kPackK];
                     mode_query<MODE>(a.qbuf, a.rescan[3 * k], a.rs, a.ids, a.cap, pair, qi, a.dim, q);
                     d = mode_cmp<MODE>(mode_chain<kL2, DIM, MODE>(q, a.tmap + pair * a.t_pair_bytes, nullptr, idx,
-                                                                    a.dim));
+                                                                    a.dim, a.tcpr));
                 } else {
                     d = kL2 ? 0.0f : -0.0f;  // canonical sign of an exact zero
                 }
@@ -1305,7 +1337,7 @@ __global__ void shard_reset_kernel(long long* keys, uint64_t n) {
 constexpr int kSelftestThreads = 320;
 constexpr uint32_t kTmemA = 384;  // self-test: query tiles copied into TMEM columns 384..415
 __global__ void __launch_bounds__(kSelftestThreads, 1) selftest_kernel(const uint8_t* qbuf, const uint8_t* tmap,
-                                                                    float* out, int mode) {
+                                                                    uint32_t cpr, float* out, int mode) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint32_t tmem_slot;
     __shared__ uint64_t bar_ld, bar_mma;
@@ -1320,14 +1352,18 @@ __global__ void __launch_bounds__(kSelftestThreads, 1) selftest_kernel(const uin
                      "r"(512));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
+    // the chunks the map does not store are zero K padding
+    for (uint32_t i = cpr * kChunkBytes / 16u + threadIdx.x; i < kBTileBytes / 16u; i += blockDim.x)
+        reinterpret_cast<uint4*>(smem + kSmemA)[i] = make_uint4(0u, 0u, 0u, 0u);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_slot;
     if (threadIdx.x == 0) {
-        mbar_expect_tx(&bar_ld, kSmemA + kTileBytes);
+        mbar_expect_tx(&bar_ld, kSmemA + cpr * kChunkBytes);
         bulk_g2s(smem, qbuf, kSmemA, &bar_ld);
-        bulk_g2s(smem + kSmemA, tmap, kTileBytes, &bar_ld);
+        bulk_g2s(smem + kSmemA, tmap, cpr * kChunkBytes, &bar_ld);
         mbar_wait(&bar_ld, 0);
         tc_fence_after();
         const uint32_t a_addr = smem_addr(smem), b_addr = a_addr + kSmemA;
@@ -1335,7 +1371,7 @@ __global__ void __launch_bounds__(kSelftestThreads, 1) selftest_kernel(const uin
             for (uint32_t qt = 0; qt < 2; ++qt)
                 for (uint32_t ks = 0; ks < 2; ++ks)
                     tc_mma_f16(tmem + qt * 128u, umma_desc(a_addr + qt * kTileBytes + ks * 256u),
-                               umma_desc(b_addr + ks * 256u), kIdescF16M128N128, ks);
+                               umma_desc_b(b_addr + ks * 2u * kChunkBytes), kIdescF16M128N128, ks);
         } else {  // production path: query tiles copied into TMEM, TS MMA
             for (uint32_t qt = 0; qt < 2; ++qt)
                 for (uint32_t ks = 0; ks < 2; ++ks)
@@ -1343,7 +1379,7 @@ __global__ void __launch_bounds__(kSelftestThreads, 1) selftest_kernel(const uin
             for (uint32_t qt = 0; qt < 2; ++qt)
                 for (uint32_t ks = 0; ks < 2; ++ks)
                     tc_mma_f16_ts(tmem + qt * 128u, tmem + kTmemA + qt * 16u + ks * 8u,
-                                  umma_desc(b_addr + ks * 256u), kIdescF16M128N128, ks);
+                                  umma_desc_b(b_addr + ks * 2u * kChunkBytes), kIdescF16M128N128, ks);
         }
         tc_commit(&bar_mma);
     }
@@ -1557,7 +1593,8 @@ int tensor_pack(fnl_context* ctx, const char* tag, const float* d_src, uint32_t 
                                     " metric); use the exact backends");
     // padded to whole 256-target B tiles (also a whole number of 128-row operand tiles)
     const uint32_t rows_pad = ceil_div_u(rows, kTargetTileRows) * kTargetTileRows;
-    const uint64_t pair_bytes = (uint64_t)rows_pad * kPackRowBytes;
+    const uint32_t cpr = ceil_div_u(dim + (l2 ? 2u : 0u), 8);  // chunks that carry data
+    const uint64_t pair_bytes = (uint64_t)(rows_pad / kTargetTileRows) * cpr * kChunkBytes;
     std::string t(tag);
     TRY(ws_arr(ctx, (t + ".packed").c_str(), (size_t)npairs * pair_bytes, &out->data));
     TRY(ws_arr(ctx, (t + ".maxnorm").c_str(), 2 * (size_t)npairs, &out->max_norm));
@@ -1565,9 +1602,11 @@ int tensor_pack(fnl_context* ctx, const char* tag, const float* d_src, uint32_t 
     cudaStream_t s = ctx_stream(ctx);
     FNL_CUDA_TRY(cudaMemsetAsync(out->max_norm, 0, 2 * (size_t)npairs * sizeof(float), s));
     out->pair_bytes = pair_bytes;
+    out->cpr = cpr;
     out->rows = rows;
     out->npairs = npairs;
-    PackArgs a{d_src, out->data, pair_bytes, rows, rows_pad, dim, l2, out->max_norm, d_bad, d_sat, out->max_norm_hi};
+    PackArgs a{d_src, out->data, pair_bytes, rows, rows_pad, dim, l2, out->max_norm, d_bad, d_sat, out->max_norm_hi,
+               cpr};
     // 8 blocks per SM (69 registers: 3 resident per SM, so ~2.7 waves; measured
     // no faster with 4 resident blocks and one wave, or with 8 row groups in
     // flight per warp at 2 blocks per SM: 1.60 / 1.84 vs 1.58 ms per 128 pairs)
@@ -1654,7 +1693,7 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     // ---- K2 gather
     {
         GatherArgs g{Q.data, Q.pair_bytes, ids, cap, d_active, d_slot_pair, d_slot_base, qbuf, margin,
-                     T.max_norm, dim, l2, d_hdr, rs.mode, rs.q32, rs.q32_pair_stride, acc16, T.max_norm_hi};
+                     T.max_norm, dim, l2, d_hdr, rs.mode, rs.q32, rs.q32_pair_stride, acc16, T.max_norm_hi, Q.cpr};
         dim3 grid(ceil_div_u(tp_per_pair * kQueryTilePair * 4, 256), npairs);
         ProfScope prof(ctx, FNL_KCLASS_GATHER);
         gather_kernel<<<grid, 256, 0, s>>>(g);
@@ -1668,7 +1707,7 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
             TRY(ws_arr(ctx, "tc.trace", 6 * 4096, &trace));
             FNL_CUDA_TRY(cudaMemsetAsync(trace, 0, 6 * 4096 * 8, s));
         }
-        TcArgs t{qbuf, T.data, T.pair_bytes, nt, d_items, d_hdr + 2, partial, debug_mode, trace};
+        TcArgs t{qbuf, T.data, T.pair_bytes, T.cpr, nt, d_items, d_hdr + 2, partial, debug_mode, trace};
         const uint32_t grid = std::min<uint32_t>(nitems_cap, sms);
         cudaEvent_t end_ev;
         ctx_score_begin(ctx, &end_ev);
@@ -1680,7 +1719,7 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     // ---- K3b merge + certification
     {
         MergeArgs m{partial, d_tp_pair, d_tp_row0, d_tp_qi0, d_hdr, d_active, margin, qbuf, T.data,
-                    T.pair_bytes, nt, dim, out, min_dist, out_stride, rescan, rcount, d_near_ties, npairs, shard_keys,
+                    T.pair_bytes, T.cpr, nt, dim, out, min_dist, out_stride, rescan, rcount, d_near_ties, npairs, shard_keys,
                     pp, ids, cap, rs, acc16, merge_prefilter()};
         ProfScope prof(ctx, FNL_KCLASS_MERGE);
         const uint32_t grid = tp_max * kMergeSlices;
@@ -1695,7 +1734,7 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     }
     // ---- K4' exact re-decision of rows left open (grid-stride over a device count)
     {
-        RescanArgs r{rescan, rcount, qbuf, T.data, T.pair_bytes, tile_begin * kBTileRows,
+        RescanArgs r{rescan, rcount, qbuf, T.data, T.pair_bytes, T.cpr, tile_begin * kBTileRows,
                      std::min(nt, tile_end * kBTileRows), dim, 4096u, keys, l2, ids, cap, rs};
         const uint32_t grid = 2 * (uint32_t)ctx_sm_count(ctx);
         ProfScope prof(ctx, FNL_KCLASS_RESCAN);
@@ -1894,9 +1933,10 @@ int tensor_selftest_scores(fnl_context* ctx, const float* d_q, const float* d_t,
     FNL_CUDA_TRY(cudaMemcpyAsync(act, &n, 4, cudaMemcpyHostToDevice, s));
     FNL_CUDA_TRY(cudaMemcpyAsync(lists, host, 8, cudaMemcpyHostToDevice, s));
     GatherArgs g{Q.data, Q.pair_bytes, nullptr, n, act, lists, lists + 1, qbuf, margin, T.max_norm, dim, l2};
+    g.qcpr = Q.cpr;
     gather_kernel<<<dim3(4, 1), 256, 0, s>>>(g);
     FNL_CUDA_TRY(cudaGetLastError());
-    selftest_kernel<<<1, kSelftestThreads, kSmemTotal, s>>>(qbuf, T.data, d_out, mode);
+    selftest_kernel<<<1, kSelftestThreads, kSmemTotal, s>>>(qbuf, T.data, T.cpr, d_out, mode);
     FNL_CUDA_TRY(cudaGetLastError());
     FNL_CUDA_TRY(cudaStreamSynchronize(s));
     return FNL_OK;

@@ -25,13 +25,19 @@ constexpr uint32_t kTileRows = 128;        // rows per UMMA operand tile
 constexpr uint32_t kTileBytes = kTileRows * kPackRowBytes;  // 8 KB
 constexpr uint32_t kQueryTilePair = 256;   // query rows per CTA (two M=128 tiles)
 
-// Maps in the UMMA canonical K-major no-swizzle layout: rows grouped by 8
-// (512 B per group), inside a group channel chunk kc (8 halves, 16 B) at
-// kc*128 and row r%8 at (r%8)*16.  A run of 128 rows is one contiguous 8 KB
-// operand tile, so a single cp.async.bulk stages it.
+// Packed maps, chunk-major per 256-row tile (a UMMA canonical K-major
+// no-swizzle operand with LBO = 4 KB between channel chunks, SBO = 128 B
+// between 8-row groups): tile T at T * cpr * 4 KB, channel chunk c (8 halves,
+// 16 B per row) at c * 4 KB inside it, row group g at g * 128, row r%8 at
+// (r%8) * 16.  Only the cpr = ceil((dim + 2 l2) / 8) chunks that carry data are
+// stored (3 for dot at d = 24: 48 of 64 bytes per row); K3 keeps the missing
+// chunks zero in shared memory, so one cp.async.bulk of cpr * 4 KB stages a
+// 256-target tile.
+constexpr uint32_t kChunkBytes = 256 * 16;  // one 8-channel chunk of a 256-row tile
 struct PackedMaps {
     uint8_t* data = nullptr;
-    uint64_t pair_bytes = 0;  // bytes per pair's map (rows padded to 128)
+    uint32_t cpr = 4;         // stored channel chunks per row
+    uint64_t pair_bytes = 0;  // bytes per pair's map (rows padded to 256)
     uint32_t rows = 0;        // real rows per map
     uint32_t npairs = 0;
     float* max_norm = nullptr;  // per pair: max L2 norm of a binary16 row (device)
