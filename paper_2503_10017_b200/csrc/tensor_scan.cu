@@ -242,6 +242,142 @@ __global__ void __launch_bounds__(kPackThreads) pack_kernel(PackArgs a, uint32_t
     }
 }
 
+// K1 v2 (TMA-staged): one thread per target row.  A 256-row target tile of
+// fp32 rows is one contiguous block (256 x dim x 4 B, 24 KB at d = 24), so a
+// single cp.async.bulk stages it into shared memory; persistent blocks keep
+// kPackStages tiles in flight (the copy engine, not warps, holds the bytes in
+// flight), each thread rounds its own row (no idle lane for d = 24, no norm
+// shuffles) and writes the row's cpr chunks, which are contiguous across the
+// threads of a warp in the chunk-major layout.  Same outputs, bit for bit, as
+// pack_kernel (norm^2 summed per 8-channel chunk, then (s0 + s1) + (s2 + s3)).
+// Needs rows x dim to be a multiple of 4 (16-byte tile sizes); else K1 v1.
+constexpr int kPackStages = 3;
+constexpr uint32_t kPackTileRows = 256;
+
+__device__ __forceinline__ void pack2_flush(const PackArgs& a, uint32_t pair, uint32_t& sat, float& nmax,
+                                            float& nmax_hi) {
+    sat = warp_sum(sat);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        nmax = fmaxf(nmax, __shfl_xor_sync(0xFFFFFFFFu, nmax, o));
+        nmax_hi = fmaxf(nmax_hi, __shfl_xor_sync(0xFFFFFFFFu, nmax_hi, o));
+    }
+    if ((threadIdx.x & 31u) == 0) {
+        if (sat) atomicAdd(a.sat + pair, (unsigned long long)sat);
+        nmax = sqrtf(nmax);
+        nmax_hi = sqrtf(nmax_hi);
+        if (nmax > 0.0f) atomicMax(reinterpret_cast<unsigned int*>(a.max_norm) + pair, __float_as_uint(nmax));
+        if (nmax_hi > 0.0f)
+            atomicMax(reinterpret_cast<unsigned int*>(a.max_norm_hi) + pair, __float_as_uint(nmax_hi));
+    }
+    sat = 0;
+    nmax = 0.0f;
+    nmax_hi = 0.0f;
+}
+
+__global__ void __launch_bounds__(kPackTileRows) pack_tma_kernel(PackArgs a, uint32_t npairs) {
+    extern __shared__ __align__(128) uint8_t psm[];
+    __shared__ __align__(8) uint64_t full[kPackStages];
+    const uint32_t tid = threadIdx.x;
+    const uint32_t tiles_per_pair = a.rows_pad / kPackTileRows;
+    const uint64_t total = (uint64_t)npairs * tiles_per_pair;
+    const uint32_t stage_bytes = kPackTileRows * a.dim * 4u;
+    const uint64_t i0 = total * blockIdx.x / gridDim.x, i1 = total * (blockIdx.x + 1) / gridDim.x;
+    if (i0 >= i1) return;
+    auto issue = [&](uint64_t i, uint32_t st) {
+        const uint32_t pair = (uint32_t)(i / tiles_per_pair);
+        const uint32_t r0 = (uint32_t)(i - (uint64_t)pair * tiles_per_pair) * kPackTileRows;
+        const uint32_t nrows = r0 < a.rows ? min(kPackTileRows, a.rows - r0) : 0u;
+        if (nrows == 0) {
+            mbar_arrive(&full[st]);  // an all-padding tile: nothing to stage
+            return;
+        }
+        const uint32_t bytes = nrows * a.dim * 4u;
+        mbar_expect_tx(&full[st], bytes);
+        bulk_g2s(psm + st * stage_bytes, a.src + ((uint64_t)pair * a.rows + r0) * a.dim, bytes, &full[st]);
+    };
+    if (tid == 0) {
+        for (int st = 0; st < kPackStages; ++st) mbar_init(&full[st], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (uint32_t st = 0; st < kPackStages && i0 + st < i1; ++st) issue(i0 + st, st);
+    }
+    __syncthreads();
+    uint32_t cur = (uint32_t)(i0 / tiles_per_pair);
+    uint32_t sat = 0;
+    float nmax = 0.0f, nmax_hi = 0.0f;
+    for (uint64_t i = i0; i < i1; ++i) {
+        const uint32_t k = (uint32_t)(i - i0), st = k % kPackStages;
+        const uint32_t pair = (uint32_t)(i / tiles_per_pair);
+        if (pair != cur) {  // block-uniform
+            pack2_flush(a, cur, sat, nmax, nmax_hi);
+            cur = pair;
+        }
+        const uint32_t r0 = (uint32_t)(i - (uint64_t)pair * tiles_per_pair) * kPackTileRows;
+        const uint32_t row = r0 + tid;
+        const bool real = row < a.rows;
+        mbar_wait(&full[st], (k / kPackStages) & 1u);
+        float v[kPackK];
+        const float* srow = reinterpret_cast<const float*>(psm + st * stage_bytes) + tid * a.dim;
+        if ((a.dim & 3u) == 0) {
+#pragma unroll
+            for (uint32_t c = 0; c < kPackK; c += 4) {
+                float4 x = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                if (real && c < a.dim) x = *reinterpret_cast<const float4*>(srow + c);
+                v[c] = x.x, v[c + 1] = x.y, v[c + 2] = x.z, v[c + 3] = x.w;
+            }
+        } else {
+#pragma unroll
+            for (uint32_t c = 0; c < kPackK; ++c) v[c] = (real && c < a.dim) ? srow[c] : 0.0f;
+        }
+        __syncthreads();  // every row of the stage is in registers: refill it
+        if (tid == 0 && i + kPackStages < i1) issue(i + kPackStages, st);
+        float s4[4];
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+            float ss = 0.0f;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int c = ch * 8 + j;
+                float x = v[c];
+                if (!isfinite(x)) atomicMin(a.bad + pair, (unsigned long long)row * a.dim + c);
+                x = half_round_sat(x, sat);
+                v[c] = x;
+                ss = __fmaf_rn(x, x, ss);
+            }
+            s4[ch] = ss;
+        }
+        const float hi2 = s4[2] + s4[3];
+        const float n2 = (s4[0] + s4[1]) + hi2;
+        if (real) {
+            nmax = fmaxf(nmax, n2);
+            nmax_hi = fmaxf(nmax_hi, hi2);
+            if (a.l2) {
+                const float half_n2 = -0.5f * n2;
+                const float h = __half2float(__float2half_rn(half_n2));
+                const float l = __half2float(__float2half_rn(half_n2 - h));
+#pragma unroll
+                for (uint32_t c = 0; c < kPackK; ++c) {
+                    if (c == a.dim) v[c] = h;
+                    if (c == a.dim + 1) v[c] = l;
+                }
+            }
+        }
+        uint8_t* dst = a.dst + (uint64_t)pair * a.pair_bytes;
+#pragma unroll
+        for (uint32_t ch = 0; ch < 4; ++ch) {
+            if (ch < a.cpr) {
+                uint4 out;
+                out.x = pack_half2(v[8 * ch], v[8 * ch + 1]);
+                out.y = pack_half2(v[8 * ch + 2], v[8 * ch + 3]);
+                out.z = pack_half2(v[8 * ch + 4], v[8 * ch + 5]);
+                out.w = pack_half2(v[8 * ch + 6], v[8 * ch + 7]);
+                *reinterpret_cast<uint4*>(dst + map_offset(row, ch, a.cpr)) = out;
+            }
+        }
+    }
+    pack2_flush(a, cur, sat, nmax, nmax_hi);
+}
+
 // ---------------------------------------------------------------- K2 gather
 struct GatherArgs {
     const uint8_t* qmap;  // packed query-side maps
@@ -407,7 +543,7 @@ struct TcArgs {
     const uint32_t* nitems;  // device item count (plan header)
     float4* partial;  // [item][col half][256][3] = (b1..b4), (b5, b6, t1, t2), (t3, t4, t5 bits, 0)
     int debug;        // profiling only: 1 = epilogue releases buffers unread, 16 = clock trace of CTA 0
-    unsigned long long* trace;  // [4][4096] clock64 stamps (debug & 16)
+    unsigned long long* trace;  // [7][4096] clock64 stamps of CTA 0 (debug & 16, tools/tc_trace.py)
 };
 
 // K3 structure (v11; measured on this B200 with the clock traces of
@@ -709,7 +845,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
                     // each 128-target half of the tile is its own accumulator chain,
                     // refilled as soon as its four epilogue warps drained it
                     mbar_wait(&accfree[qt * 2 + h], (kq & 1u) ^ 1u);
-                    if (trace && qt == 0 && h == 0 && lane == 0 && k < 4096) a.trace[8192 + k] = clock64();
+                    if (trace && qt == 0 && lane == 0 && k < 4096) a.trace[8192 + h * 4096 + k] = clock64();
                     tc_fence_after();
                     if (elect_one()) {
                         // half h starts 16 row groups (2 KB) further; K-step 1 starts two
@@ -762,7 +898,9 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
             for (uint32_t t = t_first; t < t_last && tile_live; ++t, ++k) {
                 mbar_wait(&tfull[qt * 2 + h], k & 1u);
                 const bool tw = trace && warp == kFirstEpiWarp && k < 4096;
-                if (tw && lane == 0) a.trace[12288 + k] = clock64();
+                // chain (qt 0, half 0): every quadrant's wake and release (k < 1024)
+                const bool tq = trace && e < 4 && k < 1024;
+                if (tq && lane == 0) a.trace[16384 + quad * 1024 + k] = clock64();
                 if (!warp_real || (a.debug & 1)) {  // nothing to score: hand the buffer straight back
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&accfree[qt * 2 + h]);
@@ -777,7 +915,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&accfree[qt * 2 + h]);  // all 128 columns read
-                    if (tw && lane == 0) a.trace[16384 + k] = clock64();
+                    if (tq && lane == 0) a.trace[20480 + quad * 1024 + k] = clock64();
                     const uint32_t rel = (t - item.tile_begin) * kSubPerTile + 2u * h;
                     const float k0 = key_of(tile_max64_h(f0, sub0, a.nt), rel);
                     const float k1 = key_of(tile_max64_h(f1, sub0 + 1, a.nt), rel + 1);
@@ -786,7 +924,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
                     }
                     if (tw) {
                         __syncwarp();
-                        if (lane == 0) a.trace[20480 + k] = clock64() + (kb[0] > 1e30f ? 1 : 0);
+                        if (lane == 0) a.trace[24576 + k] = clock64() + (kb[0] > 1e30f ? 1 : 0);
                     }
                     continue;
                 }
@@ -812,12 +950,12 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&accfree[qt * 2 + h]);  // this warp's 128 columns drained
-                if (tw && lane == 0) a.trace[16384 + k] = clock64();
+                if (tq && lane == 0) a.trace[20480 + quad * 1024 + k] = clock64();
                 if (__any_sync(0xFFFFFFFFu, m0 > st.b[kTopSub - 1])) tile_update(st, m0, sub0);
                 subtile_scan(st, f0, f1, sub0 + 1, a.nt);
                 if (tw) {
                     __syncwarp();
-                    if (lane == 0) a.trace[20480 + k] = clock64() + (st.b[0] > 1e30f ? 1 : 0);
+                    if (lane == 0) a.trace[24576 + k] = clock64() + (st.b[0] > 1e30f ? 1 : 0);
                 }
             }
             const uint32_t row = qt * 128u + quad * 32u + lane;  // 0..255 within the tile pair
@@ -1428,6 +1566,8 @@ int ensure_attrs() {
     FNL_CUDA_TRY(cudaFuncSetAttribute(tc_scan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal));
     FNL_CUDA_TRY(cudaFuncSetAttribute(tc_scan_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal));
     FNL_CUDA_TRY(cudaFuncSetAttribute(selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal));
+    FNL_CUDA_TRY(cudaFuncSetAttribute(pack_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kPackStages * kPackTileRows * kPackK * 4));
     if (dev >= 0 && dev < 64) attr_done[dev] = true;
     return FNL_OK;
 }
@@ -1461,8 +1601,8 @@ static bool debug_mode_trace_dump(fnl_context* ctx, cudaStream_t s) {
     static const int debug_mode = getenv("FNL_TC_DEBUG") ? atoi(getenv("FNL_TC_DEBUG")) : 0;
     if (!(debug_mode & 16)) return false;
     unsigned long long* trace = nullptr;
-    if (ws_arr(ctx, "tc.trace", 6 * 4096, &trace) != FNL_OK) return false;
-    static unsigned long long host[6 * 4096];
+    if (ws_arr(ctx, "tc.trace", 7 * 4096, &trace) != FNL_OK) return false;
+    static unsigned long long host[7 * 4096];
     cudaMemcpyAsync(host, trace, sizeof(host), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     const char* path = getenv("FNL_TC_TRACE") ? getenv("FNL_TC_TRACE") : "/tmp/fnl_tc_trace.bin";
@@ -1610,9 +1750,19 @@ int tensor_pack(fnl_context* ctx, const char* tag, const float* d_src, uint32_t 
     // 8 blocks per SM (69 registers: 3 resident per SM, so ~2.7 waves; measured
     // no faster with 4 resident blocks and one wave, or with 8 row groups in
     // flight per warp at 2 blocks per SM: 1.60 / 1.84 vs 1.58 ms per 128 pairs)
-    const uint32_t grid = 8u * (uint32_t)ctx_sm_count(ctx);
     ProfScope prof(ctx, FNL_KCLASS_PACK);
-    pack_kernel<<<grid, kPackThreads, 0, s>>>(a, npairs);
+    static const int pack_v = getenv("FNL_PACK_V") ? atoi(getenv("FNL_PACK_V")) : 2;
+    if (pack_v == 2 && ((uint64_t)rows * dim) % 4 == 0) {
+        // K1 v2: 2 resident blocks per SM, kPackStages staged tiles each
+        const uint32_t smem = kPackStages * kPackTileRows * dim * 4u;
+        TRY(ensure_attrs());
+        static const uint32_t bps = getenv("FNL_PACK_BPS") ? (uint32_t)atoi(getenv("FNL_PACK_BPS")) : 2u;
+        const uint32_t grid = std::max(1u, bps) * (uint32_t)ctx_sm_count(ctx);
+        pack_tma_kernel<<<grid, kPackTileRows, smem, s>>>(a, npairs);
+    } else {
+        const uint32_t grid = 8u * (uint32_t)ctx_sm_count(ctx);
+        pack_kernel<<<grid, kPackThreads, 0, s>>>(a, npairs);
+    }
     FNL_CUDA_TRY(cudaGetLastError());
     ctx_count_launches(ctx, 1);
     return FNL_OK;
@@ -1704,8 +1854,8 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
         static const int debug_mode = getenv("FNL_TC_DEBUG") ? atoi(getenv("FNL_TC_DEBUG")) : 0;
         unsigned long long* trace = nullptr;
         if (debug_mode & 16) {
-            TRY(ws_arr(ctx, "tc.trace", 6 * 4096, &trace));
-            FNL_CUDA_TRY(cudaMemsetAsync(trace, 0, 6 * 4096 * 8, s));
+            TRY(ws_arr(ctx, "tc.trace", 7 * 4096, &trace));
+            FNL_CUDA_TRY(cudaMemsetAsync(trace, 0, 7 * 4096 * 8, s));
         }
         TcArgs t{qbuf, T.data, T.pair_bytes, T.cpr, nt, d_items, d_hdr + 2, partial, debug_mode, trace};
         const uint32_t grid = std::min<uint32_t>(nitems_cap, sms);

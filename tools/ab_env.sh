@@ -15,6 +15,6 @@ try:
 except Exception as e:
     print(sys.argv[1], sys.argv[2], "FAILED", e); sys.exit(0)
 kb=d["config"]["kernel_breakdown_rank0"]
-print(sys.argv[1], sys.argv[2], "pairs/s", round(d["value"]), "ms", round(d["ms_per_step"],3), "score", kb["score"]["ms"], "frac", round(d["roofline"]["frac"],3), "clk", d["clocks"]["sm_mhz"])
+print(sys.argv[1], sys.argv[2], "pairs/s", round(d["value"]), "ms", round(d["ms_per_step"],3), "score", kb["score"]["ms"], "pack", kb["pack"]["ms"], kb["pack"].get("hbm_gbs"), "merge", kb["merge"]["ms"], "frac", round(d["roofline"]["frac"],3), "clk", d["clocks"]["sm_mhz"])
 PY
 done
