@@ -899,7 +899,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
                 mbar_wait(&tfull[qt * 2 + h], k & 1u);
                 const bool tw = trace && warp == kFirstEpiWarp && k < 4096;
                 // chain (qt 0, half 0): every quadrant's wake and release (k < 1024)
-                const bool tq = trace && e < 4 && k < 1024;
+                const bool tq = kF16 && trace && e < 4 && k < 1024;  // (binary16 path only: registers)
                 if (tq && lane == 0) a.trace[16384 + quad * 1024 + k] = clock64();
                 if (!warp_real || (a.debug & 1)) {  // nothing to score: hand the buffer straight back
                     __syncwarp();
