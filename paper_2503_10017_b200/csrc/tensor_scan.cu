@@ -1747,9 +1747,10 @@ int tensor_pack(fnl_context* ctx, const char* tag, const float* d_src, uint32_t 
     out->npairs = npairs;
     PackArgs a{d_src, out->data, pair_bytes, rows, rows_pad, dim, l2, out->max_norm, d_bad, d_sat, out->max_norm_hi,
                cpr};
-    // 8 blocks per SM (69 registers: 3 resident per SM, so ~2.7 waves; measured
-    // no faster with 4 resident blocks and one wave, or with 8 row groups in
-    // flight per warp at 2 blocks per SM: 1.60 / 1.84 vs 1.58 ms per 128 pairs)
+    // K1 v2 (TMA-staged, one thread per row) whenever every 256-row tile is a
+    // whole number of 16-byte units: 1.26 vs 1.56 ms per 128 C2 pairs for v1
+    // (FNL_PACK_V=1; 3 blocks per SM for v2 measured no faster).  v1: 8 blocks
+    // per SM, 4 lanes per row, any dim / row count.
     ProfScope prof(ctx, FNL_KCLASS_PACK);
     static const int pack_v = getenv("FNL_PACK_V") ? atoi(getenv("FNL_PACK_V")) : 2;
     if (pack_v == 2 && ((uint64_t)rows * dim) % 4 == 0) {
