@@ -777,6 +777,7 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
     {
         fnl::ProfScope prof(ctx, FNL_KCLASS_HARVEST);
         FNL_CUDA_TRY(fnl::launch_match_init(m, s));
+        ctx->total_launches += 1;
     }
     timer.end();
 
@@ -895,6 +896,7 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
         FNL_CUDA_TRY(fnl::launch_rev_lookup(m, s));
         TRY(nn_pass(P2, p2, m.rev_list, P1, p1, m.rev_out, m.rev_n));
         FNL_CUDA_TRY(fnl::launch_rev_fill(m, s));
+        ctx->total_launches += 3;  // claim, compact, fill
         return FNL_OK;
     };
     unsigned int* lag_done = nullptr;  // pinned [2]: n_done after iterations t-1, t
