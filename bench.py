@@ -404,6 +404,35 @@ def main_b200(args):
         other_outputs[bk] = (op, oc)
     fnl.kernel_timing(reset=True)
 
+    # ---- configs[1]: ONE 512x384 pair per call (latency; device-resident, same
+    # backend), the batch-1 view of the metric next to the batched value
+    single = None
+    if not args.no_other_backends:
+        op1 = torch.empty_like(out_pairs[:1])
+        oc1 = torch.empty_like(out_counts[:1])
+
+        def run_one():
+            fnl.reciprocal_match_device(d1.data_ptr(), d2.data_ptr(), 1, H, W, D, op1.data_ptr(), oc1.data_ptr(),
+                                        backend=args.backend, stride=STRIDE, metric=METRIC,
+                                        stream=stream.cuda_stream, with_stats=False)
+        for _ in range(3):
+            run_one()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        nrep = 20
+        e0.record(stream)
+        for _ in range(nrep):
+            run_one()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms1 = e0.elapsed_time(e1) / nrep
+        single = {"workload": "configs[1]: one C2 pair per call (pair 0 of the batch), device-resident, backend "
+                              + args.backend + ", CUDA events over 20 back-to-back calls",
+                  "ms_per_pair": round(ms1, 3), "pairs_per_s": round(1e3 / ms1, 1),
+                  "identical_to_batched": bool(torch.equal(oc1[0], out_counts[0]) and
+                                               torch.equal(op1[0, :int(oc1[0])], out_pairs[0, :int(oc1[0])]))}
+    fnl.kernel_timing(reset=True)
+
     # ---- C5: one oversized 1536x1152 pair, target columns sharded over the ranks
     c5 = None
     if not args.no_c5:
@@ -508,6 +537,7 @@ def main_b200(args):
         "cpu_baseline": cpu,
         "parity_sample": parity,
         "other_backends": other,
+        "c2_single_pair": single,
         "clocks": clk.summary(),
         "c5_sharded_pair": c5,
         "c3_flashmatch": c3,

@@ -1162,22 +1162,28 @@ __device__ __forceinline__ unsigned long long umin64(unsigned long long a, unsig
 // L2/HBM loads per row, so the kernel is latency bound and wants many rows in
 // flight -- four slices per tile pair give each warp 8 rows instead of 32
 // (measured: 1.07 -> 0.74 ms per 128-pair step; 32-row slices: 0.84 ms).
-constexpr uint32_t kMergeRows = 64;
-constexpr uint32_t kMergeSlices = kQueryTilePair / kMergeRows;
+// Passes with few tile pairs (one pair's passes) use 16-row slices instead:
+// 16 times the CTAs, and phase 1 spreads a row's up to 256 split entries over
+// 16 threads.
 constexpr uint32_t kMergeThreads = 256;
 constexpr uint32_t kNoTile = 0xFFFFFFFFu;
 
-template <bool kL2, int DIM, int MODE>
+template <bool kL2, int DIM, int MODE, uint32_t kMergeRows>
 __global__ void __launch_bounds__(kMergeThreads, 4) merge_kernel(MergeArgs a) {
-    // phase 1 (thread per row): global top-4 of sub-tile maxima over the
-    //   target splits / column halves -> candidates T1, T2, T3 and the bounds
-    //   B2, B3, B4 on everything not yet resolved after 1, 2, 3 of them
+    constexpr uint32_t kMergeSlices = kQueryTilePair / kMergeRows;
+    constexpr uint32_t kMergeParts = kMergeThreads / kMergeRows;  // phase-1 threads per row
+    // phase 1 (four threads per row): global top-6 of sub-tile maxima over
+    //   the target splits / column halves -> candidates T1..T5 and the bounds
+    //   B2..B6 on everything not yet resolved after 1..5 of them
     // phase 2 (16 lanes per row, two rows per warp): resolve T1 with the exact
     //   chain (four targets per lane, (cmp, index) key min), close the row if
     //   the exact winner beats B2 by the margin, else resolve T2 against B3,
-    //   then T3 against B4; rows still open go to the full rescan
+    //   and so on; rows still open after T5 go to the full rescan
     __shared__ uint32_t s_t[kMergeRows][kTopSub - 1];
     __shared__ float s_b[kMergeRows][kTopSub - 1];
+    // phase 1 partial lists handed down the fold tree (top-5 and the bound on the rest)
+    __shared__ float s_pb[kMergeParts / 2][kMergeRows][kTopSub];
+    __shared__ uint32_t s_pt[kMergeParts / 2][kMergeRows][kTopSub - 1];
     const uint32_t tp = blockIdx.x / kMergeSlices, slice = blockIdx.x % kMergeSlices;
     if (tp >= a.hdr[1]) return;
     const uint32_t splits = a.hdr[3];
@@ -1188,34 +1194,38 @@ __global__ void __launch_bounds__(kMergeThreads, 4) merge_kernel(MergeArgs a) {
     const uint32_t row0 = a.tp_row0[tp] + slice * kMergeRows;  // first gathered row of the slice
     const uint32_t qi0 = a.tp_qi0[tp] + slice * kMergeRows;     // its query index within the pair
     const uint32_t r = threadIdx.x;
-    if (r < nrows) {
-        // global top-6 over the splits: B[0..5] with sub-tiles T[0..4]; B[5]
-        // bounds everything below the fifth
-        float B[kTopSub];
-        uint32_t T[kTopSub - 1];
+    // global top-6 over the splits: B[0..5] with sub-tiles T[0..4]; B[5]
+    // bounds everything below the fifth.  The (split, half, source) entries
+    // of a row are spread over kMergeParts threads (a single pair's passes
+    // split the targets up to 64 ways), whose lists part 0 then folds
+    const uint32_t pr = r % kMergeRows, part = r / kMergeRows;
+    float B[kTopSub];
+    uint32_t T[kTopSub - 1];
 #pragma unroll
-        for (int i = 0; i < kTopSub; ++i) B[i] = -INFINITY;
+    for (int i = 0; i < kTopSub; ++i) B[i] = -INFINITY;
 #pragma unroll
-        for (int i = 0; i < kTopSub - 1; ++i) T[i] = kNoTile;
-        auto insert = [&](float v, uint32_t t) {
-            // sorted insert into the first five (branch-free shifts); what falls
-            // off the fifth only raises the bound B[5]
-            B[kTopSub - 1] = fmaxf(B[kTopSub - 1], fminf(B[kTopSub - 2], v));
+    for (int i = 0; i < kTopSub - 1; ++i) T[i] = kNoTile;
+    auto insert = [&](float v, uint32_t t) {
+        // sorted insert into the first five (branch-free shifts); what falls
+        // off the fifth only raises the bound B[5]
+        B[kTopSub - 1] = fmaxf(B[kTopSub - 1], fminf(B[kTopSub - 2], v));
 #pragma unroll
-            for (int i = kTopSub - 2; i >= 1; --i) {
-                const bool gp = v > B[i - 1], gi = v > B[i];
-                T[i] = gp ? T[i - 1] : (gi ? t : T[i]);
-                B[i] = gp ? B[i - 1] : (gi ? v : B[i]);
-            }
-            if (v > B[0]) T[0] = t, B[0] = v;
-        };
+        for (int i = kTopSub - 2; i >= 1; --i) {
+            const bool gp = v > B[i - 1], gi = v > B[i];
+            T[i] = gp ? T[i - 1] : (gi ? t : T[i]);
+            B[i] = gp ? B[i - 1] : (gi ? v : B[i]);
+        }
+        if (v > B[0]) T[0] = t, B[0] = v;
+    };
+    if (pr < nrows) {
         // dual tile pairs (<= 128 rows): query tile 1 scored the same rows over
         // the second half of each unit's targets, in partial rows 128..255
         const uint32_t nsrc = tp_dual(tp_rows) ? 2u : 1u;
-        for (uint32_t s = 0; s < splits * kPartialSplit * nsrc; ++s) {
+#pragma unroll 4
+        for (uint32_t s = part; s < splits * kPartialSplit * nsrc; s += kMergeParts) {
             const uint32_t sp = s % (splits * kPartialSplit), hi = s / (splits * kPartialSplit);
             const float4* pp = a.partial + (((uint64_t)tp * splits * kPartialSplit + sp) * kQueryTilePair +
-                                            hi * kTileRows + slice * kMergeRows + r) * kPartialF4;
+                                            hi * kTileRows + slice * kMergeRows + pr) * kPartialF4;
             float w[4 * kPartialF4];
 #pragma unroll
             for (int i = 0; i < kPartialF4; ++i) {
@@ -1226,10 +1236,29 @@ __global__ void __launch_bounds__(kMergeThreads, 4) merge_kernel(MergeArgs a) {
             for (int i = 0; i < kTopSub - 1; ++i) insert(w[i], __float_as_uint(w[6 + i]));
             B[kTopSub - 1] = fmaxf(B[kTopSub - 1], w[kTopSub - 1]);
         }
+    }
+    // fold the parts' lists pairwise: log2(kMergeParts) rounds
+#pragma unroll
+    for (uint32_t h = kMergeParts / 2; h >= 1; h >>= 1) {
+        if (part >= h && part < 2 * h) {
+#pragma unroll
+            for (int i = 0; i < kTopSub; ++i) s_pb[part - h][pr][i] = B[i];
+#pragma unroll
+            for (int i = 0; i < kTopSub - 1; ++i) s_pt[part - h][pr][i] = T[i];
+        }
+        __syncthreads();
+        if (part < h) {
+#pragma unroll
+            for (int i = 0; i < kTopSub - 1; ++i) insert(s_pb[part][pr][i], s_pt[part][pr][i]);
+            B[kTopSub - 1] = fmaxf(B[kTopSub - 1], s_pb[part][pr][kTopSub - 1]);
+        }
+        __syncthreads();
+    }
+    if (part == 0 && pr < nrows) {
 #pragma unroll
         for (int c = 0; c < kTopSub - 1; ++c) {
-            s_t[r][c] = T[c];
-            s_b[r][c] = B[c + 1];
+            s_t[pr][c] = T[c];
+            s_b[pr][c] = B[c + 1];
         }
     }
     __syncthreads();
@@ -1573,10 +1602,26 @@ int ensure_attrs() {
 }
 
 template <bool kL2, int DIM>
-void launch_merge_mode(int mode, uint32_t grid, const MergeArgs& m, cudaStream_t s) {
-    if (mode == kResolveFull) merge_kernel<kL2, DIM, kResolveFull><<<grid, kMergeThreads, 0, s>>>(m);
-    else if (mode == kResolveHybrid) merge_kernel<kL2, DIM, kResolveHybrid><<<grid, kMergeThreads, 0, s>>>(m);
-    else merge_kernel<kL2, DIM, kResolveRounded><<<grid, kMergeThreads, 0, s>>>(m);
+void launch_merge_rows(int mode, uint32_t grid, const MergeArgs& m, cudaStream_t s, bool small) {
+    if (small) {
+        grid *= kQueryTilePair / 16;
+        if (mode == kResolveFull) merge_kernel<kL2, DIM, kResolveFull, 16><<<grid, kMergeThreads, 0, s>>>(m);
+        else if (mode == kResolveHybrid) merge_kernel<kL2, DIM, kResolveHybrid, 16><<<grid, kMergeThreads, 0, s>>>(m);
+        else merge_kernel<kL2, DIM, kResolveRounded, 16><<<grid, kMergeThreads, 0, s>>>(m);
+        return;
+    }
+    grid *= kQueryTilePair / 64;
+    if (mode == kResolveFull) merge_kernel<kL2, DIM, kResolveFull, 64><<<grid, kMergeThreads, 0, s>>>(m);
+    else if (mode == kResolveHybrid) merge_kernel<kL2, DIM, kResolveHybrid, 64><<<grid, kMergeThreads, 0, s>>>(m);
+    else merge_kernel<kL2, DIM, kResolveRounded, 64><<<grid, kMergeThreads, 0, s>>>(m);
+}
+template <bool kL2, int DIM>
+void launch_merge_mode(int mode, uint32_t tp_max, uint32_t sms, const MergeArgs& m, cudaStream_t s) {
+    // 64-row slices (4 per tile pair) fill the GPU once there are >= one tile
+    // pair per SM; below that (a single pair's passes) 16-row slices
+    static const int env = getenv("FNL_MERGE_SMALL") ? atoi(getenv("FNL_MERGE_SMALL")) : -1;
+    const bool small = env >= 0 ? env != 0 : tp_max < sms;
+    launch_merge_rows<kL2, DIM>(mode, tp_max, m, s, small);
 }
 template <bool kL2, int DIM, int MODE>
 void launch_rescan_t(uint32_t grid, const RescanArgs& r, uint32_t* out, float* min_dist, uint32_t out_stride,
@@ -1873,13 +1918,13 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
                     T.pair_bytes, T.cpr, nt, dim, out, min_dist, out_stride, rescan, rcount, d_near_ties, npairs, shard_keys,
                     pp, ids, cap, rs, acc16, merge_prefilter()};
         ProfScope prof(ctx, FNL_KCLASS_MERGE);
-        const uint32_t grid = tp_max * kMergeSlices;
+        const uint32_t sms_u = (uint32_t)ctx_sm_count(ctx);
         if (dim == 24) {
-            if (l2) launch_merge_mode<true, 24>(rs.mode, grid, m, s);
-            else launch_merge_mode<false, 24>(rs.mode, grid, m, s);
+            if (l2) launch_merge_mode<true, 24>(rs.mode, tp_max, sms_u, m, s);
+            else launch_merge_mode<false, 24>(rs.mode, tp_max, sms_u, m, s);
         } else {
-            if (l2) launch_merge_mode<true, 0>(rs.mode, grid, m, s);
-            else launch_merge_mode<false, 0>(rs.mode, grid, m, s);
+            if (l2) launch_merge_mode<true, 0>(rs.mode, tp_max, sms_u, m, s);
+            else launch_merge_mode<false, 0>(rs.mode, tp_max, sms_u, m, s);
         }
         FNL_CUDA_TRY(cudaGetLastError());
     }
