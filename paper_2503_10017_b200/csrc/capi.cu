@@ -67,6 +67,17 @@ struct fnl_context {
     double class_ms[FNL_KCLASS_COUNT] = {};
     uint64_t class_launches[FNL_KCLASS_COUNT] = {};
     cudaEvent_t lag[2] = {nullptr, nullptr};  // lagged convergence check of the reciprocal loop
+    // graph replay of the reciprocal loop for small batches (run_match)
+    uint64_t ws_gen = 0;  // bumped on every workspace (re)allocation
+    struct LoopGraph {
+        std::vector<uint64_t> key;
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        uint64_t launches = 0;  // kernels per loop iteration
+    };
+    std::vector<LoopGraph> graphs;
+    std::vector<uint64_t> last_key;  // loop key of the previous host-driven run
+    cudaStream_t cap_stream = nullptr;
 };
 
 namespace {
@@ -95,6 +106,7 @@ int dev_buf(fnl_context* ctx, const char* name, size_t bytes, void** out) {
         b.p = nullptr;
         b.bytes = 0;
         const size_t want = std::max<size_t>(bytes, 256);
+        ++ctx->ws_gen;  // captured loop graphs hold the old pointers
         cudaError_t e = cudaMalloc(&b.p, want);
         if (e != cudaSuccess) return fnl::fail_cuda(e, name, __FILE__, __LINE__);
         b.bytes = want;
@@ -386,6 +398,11 @@ extern "C" int fnl_context_destroy(fnl_context* ctx) {
     for (auto& ev : ctx->ev_free) { cudaEventDestroy(ev.first); cudaEventDestroy(ev.second); }
     for (auto& e : ctx->lag)
         if (e) cudaEventDestroy(e);
+    for (auto& g : ctx->graphs) {
+        cudaGraphExecDestroy(g.exec);
+        cudaGraphDestroy(g.graph);
+    }
+    if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     cudaStreamDestroy(ctx->own_stream);
     cudaStreamDestroy(ctx->copy_stream);
     delete ctx;
@@ -621,6 +638,9 @@ int check_cfg(const fnl_match_config* cfg) {
                                     " is not supported by this build");
     return FNL_OK;
 }
+
+// batches up to this many pairs replay the reciprocal loop as a CUDA graph
+constexpr uint32_t kLoopGraphMaxPairs = 16;
 
 // The device-resident matcher over npairs stacked pairs.  d_d1 / d_d2 are raw
 // fp32 maps on the device.  Results stay on the device in the MatchState.
@@ -910,7 +930,99 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
         TRY(nn_pass(P1, p1, m.active_u, P2, p2, m.active_v));
         timer.end();
     }
-    for (uint32_t t = 1; t <= T && samples > 0; ++t) {
+    // ---- small batches: the loop is launch-bound (a pass is a few tens of
+    // microseconds of GPU work behind ~40 us of host launch cost), so it runs
+    // as ONE CUDA graph: a WHILE node whose body is an iteration (reverse
+    // pass, harvest, condition kernel, forward pass) and whose condition the
+    // device sets (some pair not done and t < T).  Captured on the second run
+    // with an identical configuration (same buffers, shapes, route and
+    // workspace), replayed afterwards; the forward pass after the last
+    // harvest sees every pair done and does nothing.
+    bool replayed = false;
+    std::vector<uint64_t> loop_key;
+    static const bool graph_env = !(getenv("FNL_LOOP_GRAPH") && atoi(getenv("FNL_LOOP_GRAPH")) == 0);
+    const bool graph_ok = graph_env && tc && !sharded && !h_stats && !ctx->profile_all && samples > 0 &&
+                          npairs <= kLoopGraphMaxPairs;
+    auto make_key = [&]() {
+        return std::vector<uint64_t>{npairs, (uint64_t)(uintptr_t)d_d1, (uint64_t)(uintptr_t)d_d2, h1, w1, h2, w2,
+                                     dim, cfg->k, cfg->grid_stride, T,
+                                     (uint64_t)(cfg->convergence_fraction * 1e15), (uint64_t)cfg->metric,
+                                     (uint64_t)cfg->precision, cfg->block_size, (uint64_t)backend,
+                                     (uint64_t)(uintptr_t)d_pairs_out, (uint64_t)(uintptr_t)d_npairs_out,
+                                     (uint64_t)acc16, (uint64_t)mode, (uint64_t)memo, ctx->ws_gen};
+    };
+    if (graph_ok) {
+        loop_key = make_key();
+        uint32_t* d_iter = nullptr;
+        TRY(dev_arr(ctx, "m.iter", 1, &d_iter));
+        if (ctx->ws_gen != loop_key.back()) loop_key = make_key();  // (first use of m.iter)
+        fnl_context::LoopGraph* lg = nullptr;
+        for (auto& g : ctx->graphs)
+            if (g.key == loop_key) lg = &g;
+        if (!lg && ctx->last_key == loop_key) {
+            // capture the iteration into the WHILE node's body graph
+            fnl_context::LoopGraph ng;
+            ng.key = loop_key;
+            cudaGraphConditionalHandle handle;
+            cudaGraphNodeParams cp{};
+            cudaGraphNode_t wnode;
+            FNL_CUDA_TRY(cudaGraphCreate(&ng.graph, 0));
+            FNL_CUDA_TRY(cudaGraphConditionalHandleCreate(&handle, ng.graph, 1, cudaGraphCondAssignDefault));
+            cp.type = cudaGraphNodeTypeConditional;
+            cp.conditional.handle = handle;
+            cp.conditional.type = cudaGraphCondTypeWhile;
+            cp.conditional.size = 1;
+            FNL_CUDA_TRY(cudaGraphAddNode(&wnode, ng.graph, nullptr, 0, &cp));
+            if (!ctx->cap_stream) FNL_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+            const cudaStream_t user = s;
+            const bool timing = ctx->timing;
+            const uint64_t gen0 = ctx->ws_gen, l0 = ctx->total_launches;
+            ctx->stream = s = ctx->cap_stream;
+            ctx->timing = false;  // no event marks inside the graph
+            m.iter = d_iter;
+            int rc = FNL_OK;
+            cudaGraph_t captured = nullptr;
+            cudaError_t ce = cudaStreamBeginCaptureToGraph(s, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                                           cudaStreamCaptureModeThreadLocal);
+            if (ce == cudaSuccess) {
+                rc = reverse_pass();
+                if (rc == FNL_OK) rc = fnl::launch_harvest(m, 0, s) == cudaSuccess ? FNL_OK : FNL_ERUNTIME;
+                if (rc == FNL_OK) rc = fnl::launch_loop_cond(m, handle, s) == cudaSuccess ? FNL_OK : FNL_ERUNTIME;
+                if (rc == FNL_OK) rc = nn_pass(P1, p1, m.active_u, P2, p2, m.active_v);
+                ce = cudaStreamEndCapture(s, &captured);
+            }
+            ctx->stream = s = user;
+            ctx->timing = timing;
+            ng.launches = ctx->total_launches - l0 + 2;  // + harvest, condition
+            ctx->total_launches = l0;
+            if (ce == cudaSuccess && rc == FNL_OK && ctx->ws_gen == gen0)
+                ce = cudaGraphInstantiate(&ng.exec, ng.graph, 0);
+            if (ce != cudaSuccess || rc != FNL_OK || ctx->ws_gen != gen0 || !ng.exec) {
+                // not capturable here: keep the host-driven loop
+                cudaGetLastError();
+                if (ng.exec) cudaGraphExecDestroy(ng.exec);
+                cudaGraphDestroy(ng.graph);
+                m.iter = nullptr;
+            } else {
+                if (ctx->graphs.size() >= 4) {
+                    cudaGraphExecDestroy(ctx->graphs.front().exec);
+                    cudaGraphDestroy(ctx->graphs.front().graph);
+                    ctx->graphs.erase(ctx->graphs.begin());
+                }
+                ctx->graphs.push_back(ng);
+                lg = &ctx->graphs.back();
+            }
+        }
+        if (getenv("FNL_LOOP_GRAPH_DEBUG"))  // tests: which calls replay
+            fprintf(stderr, "fnl loop graph: replay %d graphs %zu\n", lg != nullptr, ctx->graphs.size());
+        if (lg) {
+            FNL_CUDA_TRY(cudaMemsetAsync(d_iter, 0, 4, s));
+            FNL_CUDA_TRY(cudaGraphLaunch(lg->exec, s));
+            ctx->total_launches += lg->launches;  // (one iteration's worth)
+            replayed = true;
+        }
+    }
+    for (uint32_t t = 1; t <= T && samples > 0 && !replayed; ++t) {
         timer.begin(kPhaseReverse);
         TRY(reverse_pass());
         timer.end();
@@ -944,6 +1056,7 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
         TRY(nn_pass(P1, p1, m.active_u, P2, p2, m.active_v));
         timer.end();
     }
+    if (graph_ok && !replayed) ctx->last_key = make_key();
 
     if (peer) {
         unsigned int err = 0;

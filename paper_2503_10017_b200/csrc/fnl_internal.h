@@ -149,6 +149,10 @@ struct MatchState {
     uint32_t* rev_list;           // [npairs][cap]: pixels this reverse pass computes
     uint32_t* rev_n;              // [npairs]
     uint32_t* rev_out;            // [npairs][cap]: their NN
+    // graph-replayed loop: iterations harvested so far (device counter, the
+    // harvest and loop-condition kernels read it); null when the host drives
+    // the loop and passes the iteration by value
+    uint32_t* iter;
 };
 constexpr uint32_t kRevUnknown = 0xFFFFFFFFu;
 // stats words per pair: converged, duplicates, iterations, history_len,
@@ -159,6 +163,9 @@ constexpr int kStatWords = 4 + 64 + 1;
 
 cudaError_t launch_match_init(const MatchState& m, cudaStream_t s);
 cudaError_t launch_harvest(const MatchState& m, uint32_t iteration, cudaStream_t s);
+// graph-replayed loop: after harvest, advance *m.iter and set the WHILE
+// node's condition (more iterations: some pair not done and t < max_iters)
+cudaError_t launch_loop_cond(const MatchState& m, cudaGraphConditionalHandle h, cudaStream_t s);
 // reverse-NN memo: back[i] from the memo where known; unseen pixels claimed
 // (once each, by their lowest entry) into rev_list / rev_n in entry order for
 // the pass; then memo <- pass results and back[i] <- memo for every active i

@@ -79,9 +79,10 @@ __device__ __forceinline__ uint32_t block_scan(uint32_t flag, uint32_t* warp_tot
     return off;
 }
 
-__global__ void __launch_bounds__(kHarvestThreads) harvest_kernel(MatchState m, uint32_t t) {
+__global__ void __launch_bounds__(kHarvestThreads) harvest_kernel(MatchState m, uint32_t t_arg) {
     const uint32_t p = blockIdx.x;
     if (m.done[p]) return;
+    const uint32_t t = m.iter ? *m.iter + 1 : t_arg;  // graph replay: the device counter
     __shared__ uint32_t hkey[kHashSlots];
     __shared__ uint32_t hpos[kHashSlots];
     __shared__ uint32_t warp_tot[33];
@@ -168,6 +169,17 @@ __global__ void __launch_bounds__(kHarvestThreads) harvest_kernel(MatchState m, 
 
 cudaError_t launch_harvest(const MatchState& m, uint32_t iteration, cudaStream_t s) {
     harvest_kernel<<<m.npairs, kHarvestThreads, 0, s>>>(m, iteration);
+    return cudaGetLastError();
+}
+
+__global__ void loop_cond_kernel(MatchState m, cudaGraphConditionalHandle h) {
+    const uint32_t t = *m.iter + 1;  // the iteration just harvested
+    *m.iter = t;
+    cudaGraphSetConditional(h, (*m.n_done < m.npairs && t < m.max_iters) ? 1u : 0u);
+}
+
+cudaError_t launch_loop_cond(const MatchState& m, cudaGraphConditionalHandle h, cudaStream_t s) {
+    loop_cond_kernel<<<1, 1, 0, s>>>(m, h);
     return cudaGetLastError();
 }
 

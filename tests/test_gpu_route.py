@@ -229,3 +229,41 @@ def test_reverse_memo_saves_rows_and_keeps_matchsets(fnl, ref):
         assert st["tensor_route"] == 1
         assert st["computed_query_rows"] <= st["query_rows"]
     assert sum(st["computed_query_rows"] for st in stats) < sum(st["query_rows"] for st in stats)
+
+
+@pytest.mark.parametrize("npairs,max_iters", [(1, 10), (3, 10), (2, 2)])
+def test_loop_graph_replay_matches_reference(fnl, ref, npairs, max_iters, monkeypatch, capfd):
+    # small batches replay the reciprocal loop as a CUDA graph (WHILE node,
+    # condition set on the device) from the second identical call on: every
+    # replay -- including one on NEW maps written into the same buffers --
+    # must still give the reference's MatchSets
+    import torch
+    H, W, D = 64, 48, 24
+
+    def maps(seed):
+        a = np.stack([ref.gen_random(H, W, D, seed + i) for i in range(npairs)])
+        b = np.stack([ref.gen_random(H, W, D, seed + 100 + i) for i in range(npairs)])
+        return a, b
+
+    d1 = torch.empty((npairs, H, W, D), dtype=torch.float32, device="cuda")
+    d2 = torch.empty_like(d1)
+    samples = ((H + 7) // 8) * ((W + 7) // 8)
+    out = torch.empty((npairs, samples, 3), dtype=torch.int32, device="cuda")
+    cnt = torch.empty((npairs,), dtype=torch.int32, device="cuda")
+    monkeypatch.setenv("FNL_LOOP_GRAPH_DEBUG", "1")
+    for call, seed in enumerate([500, 500, 500, 700, 700]):
+        a, b = maps(seed)
+        d1.copy_(torch.from_numpy(a))
+        d2.copy_(torch.from_numpy(b))
+        out.fill_(-1)
+        fnl.reciprocal_match_device(d1.data_ptr(), d2.data_ptr(), npairs, H, W, D, out.data_ptr(), cnt.data_ptr(),
+                                    backend="single", metric="dot", max_iters=max_iters, with_stats=False)
+        torch.cuda.synchronize()
+        o, c = out.cpu().numpy(), cnt.cpu().numpy()
+        for i in range(npairs):
+            want, _ = ref.reciprocal_match(a[i], b[i], backend="single", metric="dot", max_iters=max_iters)
+            assert np.array_equal(o[i][: c[i]].astype(np.int64), np.asarray(want, np.int64)), (call, i)
+    # the first call drives the loop from the host, the second captures, and
+    # every later call replays the graph (the fourth on new maps)
+    replays = [ln for ln in capfd.readouterr().err.splitlines() if ln.startswith("fnl loop graph:")]
+    assert len(replays) == 5 and all(ln.startswith("fnl loop graph: replay 1") for ln in replays[1:]), replays
