@@ -753,12 +753,17 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
         // (host-buffer entry points), to check the route, and to choose the
         // K3 accumulator (binary16 when every pair's norms allow it).
         {
-            std::vector<unsigned long long> hb(2 * (size_t)npairs), hs(2 * (size_t)npairs);
-            std::vector<float> hn(2 * (size_t)npairs);
-            FNL_CUDA_TRY(cudaMemcpyAsync(hb.data(), tbad, hb.size() * 8, cudaMemcpyDeviceToHost, s));
-            FNL_CUDA_TRY(cudaMemcpyAsync(hs.data(), tsat, hs.size() * 8, cudaMemcpyDeviceToHost, s));
-            FNL_CUDA_TRY(cudaMemcpyAsync(hn.data(), T1.max_norm, npairs * 4, cudaMemcpyDeviceToHost, s));
-            FNL_CUDA_TRY(cudaMemcpyAsync(hn.data() + npairs, T2.max_norm, npairs * 4, cudaMemcpyDeviceToHost, s));
+            // pinned staging: the four copies are DMA'd back to back behind the
+            // packs and the host waits once (pageable copies each block)
+            void* pin = nullptr;
+            TRY(fnl::ws_pinned(ctx, "m.route", (size_t)npairs * (16 + 16 + 8), &pin));
+            unsigned long long* hb = static_cast<unsigned long long*>(pin);
+            unsigned long long* hs = hb + 2 * (size_t)npairs;
+            float* hn = reinterpret_cast<float*>(hs + 2 * (size_t)npairs);
+            FNL_CUDA_TRY(cudaMemcpyAsync(hb, tbad, (size_t)npairs * 16, cudaMemcpyDeviceToHost, s));
+            FNL_CUDA_TRY(cudaMemcpyAsync(hs, tsat, (size_t)npairs * 16, cudaMemcpyDeviceToHost, s));
+            FNL_CUDA_TRY(cudaMemcpyAsync(hn, T1.max_norm, npairs * 4, cudaMemcpyDeviceToHost, s));
+            FNL_CUDA_TRY(cudaMemcpyAsync(hn + npairs, T2.max_norm, npairs * 4, cudaMemcpyDeviceToHost, s));
             FNL_CUDA_TRY(cudaStreamSynchronize(s));
             if (validate) {
                 // D1 is checked before D2, as the reference converts D1 first
@@ -793,13 +798,6 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
     }
     PhaseTimer timer{ctx};
     timer.enabled = h_stats != nullptr;
-    timer.begin(kPhaseSubsample);
-    {
-        fnl::ProfScope prof(ctx, FNL_KCLASS_HARVEST);
-        FNL_CUDA_TRY(fnl::launch_match_init(m, s));
-        ctx->total_launches += 1;
-    }
-    timer.end();
 
     // ---- NN pass helper: queries = rows of qmap at ids, targets = tmap
     uint32_t call = 0;
@@ -908,7 +906,6 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
         TRY(dev_arr(ctx, "m.revlist", pc, &m.rev_list));
         TRY(dev_arr(ctx, "m.revout", pc, &m.rev_out));
         TRY(dev_arr(ctx, "m.revn", npairs, &m.rev_n));
-        FNL_CUDA_TRY(cudaMemsetAsync(m.rev_cache, 0xFF, (size_t)npairs * p2 * 4, s));
     }
     auto reverse_pass = [&]() -> int {
         if (!memo) return nn_pass(P2, p2, m.active_v, P1, p1, m.back);
@@ -925,11 +922,23 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
         TRY(fnl::ws_pinned(ctx, "m.lagdone", 8, (void**)&lag_done));
         TRY(lag_events(ctx, &lag_ev));
     }
-    if (samples > 0) {
-        timer.begin(kPhaseForward);
-        TRY(nn_pass(P1, p1, m.active_u, P2, p2, m.active_v));
+    // sampling, the memo reset and the first forward pass (src/reciprocal.cpp:128-139)
+    auto prefix = [&]() -> int {
+        timer.begin(kPhaseSubsample);
+        {
+            fnl::ProfScope prof(ctx, FNL_KCLASS_HARVEST);
+            FNL_CUDA_TRY(fnl::launch_match_init(m, s));
+            ctx->total_launches += 1;
+        }
         timer.end();
-    }
+        if (memo) FNL_CUDA_TRY(cudaMemsetAsync(m.rev_cache, 0xFF, (size_t)npairs * p2 * 4, s));
+        if (samples > 0) {
+            timer.begin(kPhaseForward);
+            TRY(nn_pass(P1, p1, m.active_u, P2, p2, m.active_v));
+            timer.end();
+        }
+        return FNL_OK;
+    };
     // ---- small batches: the loop is launch-bound (a pass is a few tens of
     // microseconds of GPU work behind ~40 us of host launch cost), so it runs
     // as ONE CUDA graph: a WHILE node whose body is an iteration (reverse
@@ -972,7 +981,6 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
             cp.conditional.handle = handle;
             cp.conditional.type = cudaGraphCondTypeWhile;
             cp.conditional.size = 1;
-            FNL_CUDA_TRY(cudaGraphAddNode(&wnode, ng.graph, nullptr, 0, &cp));
             if (!ctx->cap_stream) FNL_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
             const cudaStream_t user = s;
             const bool timing = ctx->timing;
@@ -982,9 +990,29 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
             m.iter = d_iter;
             int rc = FNL_OK;
             cudaGraph_t captured = nullptr;
-            cudaError_t ce = cudaStreamBeginCaptureToGraph(s, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+            // main graph: prefix -> WHILE node
+            cudaError_t ce = cudaStreamBeginCaptureToGraph(s, ng.graph, nullptr, nullptr, 0,
                                                            cudaStreamCaptureModeThreadLocal);
             if (ce == cudaSuccess) {
+                rc = prefix();
+                if (rc == FNL_OK) rc = cudaMemsetAsync(d_iter, 0, 4, s) == cudaSuccess ? FNL_OK : FNL_ERUNTIME;
+                cudaStreamCaptureStatus cs_status;
+                const cudaGraphNode_t* deps = nullptr;
+                size_t ndeps = 0;
+                if (rc == FNL_OK) {
+                    ce = cudaStreamGetCaptureInfo(s, &cs_status, nullptr, nullptr, &deps, &ndeps);
+                    if (ce == cudaSuccess) ce = cudaGraphAddNode(&wnode, ng.graph, deps, ndeps, &cp);
+                    if (ce == cudaSuccess)
+                        ce = cudaStreamUpdateCaptureDependencies(s, &wnode, 1, cudaStreamSetCaptureDependencies);
+                }
+                const cudaError_t ee = cudaStreamEndCapture(s, &captured);
+                if (ce == cudaSuccess) ce = ee;
+            }
+            // WHILE body: one iteration
+            if (ce == cudaSuccess && rc == FNL_OK)
+                ce = cudaStreamBeginCaptureToGraph(s, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                                   cudaStreamCaptureModeThreadLocal);
+            if (ce == cudaSuccess && rc == FNL_OK) {
                 rc = reverse_pass();
                 if (rc == FNL_OK) rc = fnl::launch_harvest(m, 0, s) == cudaSuccess ? FNL_OK : FNL_ERUNTIME;
                 if (rc == FNL_OK) rc = fnl::launch_loop_cond(m, handle, s) == cudaSuccess ? FNL_OK : FNL_ERUNTIME;
@@ -993,7 +1021,8 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
             }
             ctx->stream = s = user;
             ctx->timing = timing;
-            ng.launches = ctx->total_launches - l0 + 2;  // + harvest, condition
+            // launches per replay: the prefix plus one iteration (+ harvest, condition)
+            ng.launches = ctx->total_launches - l0 + 2;
             ctx->total_launches = l0;
             if (ce == cudaSuccess && rc == FNL_OK && ctx->ws_gen == gen0)
                 ce = cudaGraphInstantiate(&ng.exec, ng.graph, 0);
@@ -1016,12 +1045,12 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
         if (getenv("FNL_LOOP_GRAPH_DEBUG"))  // tests: which calls replay
             fprintf(stderr, "fnl loop graph: replay %d graphs %zu\n", lg != nullptr, ctx->graphs.size());
         if (lg) {
-            FNL_CUDA_TRY(cudaMemsetAsync(d_iter, 0, 4, s));
             FNL_CUDA_TRY(cudaGraphLaunch(lg->exec, s));
             ctx->total_launches += lg->launches;  // (one iteration's worth)
             replayed = true;
         }
     }
+    if (!replayed) TRY(prefix());
     for (uint32_t t = 1; t <= T && samples > 0 && !replayed; ++t) {
         timer.begin(kPhaseReverse);
         TRY(reverse_pass());
