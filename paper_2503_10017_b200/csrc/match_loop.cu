@@ -268,9 +268,12 @@ __global__ void rev_claim_kernel(MatchState m) {
 
 __global__ void __launch_bounds__(kHarvestThreads) rev_compact_kernel(MatchState m) {
     __shared__ uint32_t warp_tot[33];
+    __shared__ uint32_t s_n;
     const uint32_t p = blockIdx.x;
-    if (m.done[p]) return;
-    const uint32_t n = m.n_active[p];
+    if (threadIdx.x == 0) s_n = m.done[p] ? 0xFFFFFFFFu : m.n_active[p];
+    __syncthreads();
+    const uint32_t n = s_n;  // one read per block: the loop below is CTA-uniform
+    if (n == 0xFFFFFFFFu) return;
     const uint32_t* V = m.active_v + (size_t)p * m.cap;
     const uint32_t* cache = m.rev_cache + (size_t)p * m.p2;
     uint32_t* L = m.rev_list + (size_t)p * m.cap;

@@ -41,3 +41,13 @@ q = torch.randn((1, 2, 200, 64), device="cuda").half(); k = torch.randn((1, 2, 1
 o = fnl.flashmatch(q, k, k)
 torch.cuda.synchronize()
 print("flashmatch", tuple(o.shape), bool(torch.isfinite(o.float()).all()))
+# the device batch API without stats: host-driven first call, then the loop
+# captured and replayed as a CUDA graph (WHILE node) on the same buffers
+dd1 = torch.from_numpy(np.stack([D1, E1[:64, :48]])).cuda().contiguous()
+dd2 = torch.from_numpy(np.stack([D2, E2[:64, :48]])).cuda().contiguous()
+gp = torch.empty((2, S, 3), dtype=torch.int32, device="cuda"); gc = torch.empty(2, dtype=torch.int32, device="cuda")
+for _ in range(3):
+    fnl.reciprocal_match_device(dd1.data_ptr(), dd2.data_ptr(), 2, 64, 48, 24, gp.data_ptr(), gc.data_ptr(),
+                                backend="single", metric="dot", with_stats=False)
+torch.cuda.synchronize()
+print("graph replay", gc.tolist())
