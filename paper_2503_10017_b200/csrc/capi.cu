@@ -1026,6 +1026,9 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
             ctx->total_launches = l0;
             if (ce == cudaSuccess && rc == FNL_OK && ctx->ws_gen == gen0)
                 ce = cudaGraphInstantiate(&ng.exec, ng.graph, 0);
+            if (getenv("FNL_LOOP_GRAPH_DEBUG"))
+                fprintf(stderr, "fnl loop graph: capture ce=%d (%s) rc=%d gen %d exec %d\n", (int)ce,
+                        cudaGetErrorString(ce), rc, (int)(ctx->ws_gen == gen0), ng.exec != nullptr);
             if (ce != cudaSuccess || rc != FNL_OK || ctx->ws_gen != gen0 || !ng.exec) {
                 // not capturable here: keep the host-driven loop
                 cudaGetLastError();
