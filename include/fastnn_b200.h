@@ -163,7 +163,12 @@ int fnl_reciprocal_match_batch(fnl_context* ctx, uint32_t npairs, const float* h
  * speed, non-finite inputs are not rejected here (the host-buffer entry points
  * validate like the reference); they still take the route that keeps the
  * results identical to the reference's arithmetic on those values.  The maps
- * must be 16-byte aligned (FNL_EINVAL otherwise). */
+ * must be 16-byte aligned (FNL_EINVAL otherwise).  With h_stats == NULL and
+ * npairs <= 16 the second call with the same buffers and configuration
+ * captures the reciprocal loop as one CUDA graph (a WHILE node whose
+ * condition the device sets) and later calls replay it: no per-iteration
+ * host read, one graph launch after the pack's route read-back
+ * (FNL_LOOP_GRAPH=0 disables it). */
 int fnl_reciprocal_match_batch_device(fnl_context* ctx, uint32_t npairs, const float* d_d1,
                                       const float* d_d2, uint32_t h, uint32_t w, uint32_t dim,
                                       const fnl_match_config* cfg, int backend,
