@@ -231,8 +231,11 @@ def test_reverse_memo_saves_rows_and_keeps_matchsets(fnl, ref):
     assert sum(st["computed_query_rows"] for st in stats) < sum(st["query_rows"] for st in stats)
 
 
-@pytest.mark.parametrize("npairs,max_iters", [(1, 10), (3, 10), (2, 2)])
-def test_loop_graph_replay_matches_reference(fnl, ref, npairs, max_iters, monkeypatch, capfd):
+@pytest.mark.parametrize("npairs,max_iters,backend,metric", [(1, 10, "single", "dot"), (3, 10, "single", "dot"),
+                                                           (2, 2, "single", "dot"), (2, 1, "single", "dot"),
+                                                           (16, 10, "single", "dot"), (2, 10, "hybrid", "dot"),
+                                                           (2, 10, "single", "l2"), (2, 10, "tensor", "dot")])
+def test_loop_graph_replay_matches_reference(fnl, ref, npairs, max_iters, backend, metric, monkeypatch, capfd):
     # small batches replay the reciprocal loop as a CUDA graph (WHILE node,
     # condition set on the device) from the second identical call on: every
     # replay -- including one on NEW maps written into the same buffers --
@@ -250,6 +253,10 @@ def test_loop_graph_replay_matches_reference(fnl, ref, npairs, max_iters, monkey
     samples = ((H + 7) // 8) * ((W + 7) // 8)
     out = torch.empty((npairs, samples, 3), dtype=torch.int32, device="cuda")
     cnt = torch.empty((npairs,), dtype=torch.int32, device="cuda")
+    def half(x):
+        from oracle import oracle
+        return oracle.half_round_array(x)
+
     monkeypatch.setenv("FNL_LOOP_GRAPH_DEBUG", "1")
     for call, seed in enumerate([500, 500, 500, 700, 700]):
         a, b = maps(seed)
@@ -257,13 +264,17 @@ def test_loop_graph_replay_matches_reference(fnl, ref, npairs, max_iters, monkey
         d2.copy_(torch.from_numpy(b))
         out.fill_(-1)
         fnl.reciprocal_match_device(d1.data_ptr(), d2.data_ptr(), npairs, H, W, D, out.data_ptr(), cnt.data_ptr(),
-                                    backend="single", metric="dot", max_iters=max_iters, with_stats=False)
+                                    backend=backend, metric=metric, max_iters=max_iters, with_stats=False)
         torch.cuda.synchronize()
         o, c = out.cpu().numpy(), cnt.cpu().numpy()
         for i in range(npairs):
-            want, _ = ref.reciprocal_match(a[i], b[i], backend="single", metric="dot", max_iters=max_iters)
+            if backend == "tensor":  # its contract: ref single on binary16-rounded maps
+                want, _ = ref.reciprocal_match(half(a[i]), half(b[i]), backend="single", metric=metric,
+                                               max_iters=max_iters)
+            else:
+                want, _ = ref.reciprocal_match(a[i], b[i], backend=backend, metric=metric, max_iters=max_iters)
             assert np.array_equal(o[i][: c[i]].astype(np.int64), np.asarray(want, np.int64)), (call, i)
     # the first call drives the loop from the host, the second captures, and
     # every later call replays the graph (the fourth on new maps)
-    replays = [ln for ln in capfd.readouterr().err.splitlines() if ln.startswith("fnl loop graph:")]
+    replays = [ln for ln in capfd.readouterr().err.splitlines() if ln.startswith("fnl loop graph: replay")]
     assert len(replays) == 5 and all(ln.startswith("fnl loop graph: replay 1") for ln in replays[1:]), replays
