@@ -77,6 +77,7 @@ struct fnl_context {
     };
     std::vector<LoopGraph> graphs;
     std::vector<uint64_t> last_key;  // loop key of the previous host-driven run
+    std::vector<uint64_t> failed_key;  // a configuration whose capture failed (not retried)
     cudaStream_t cap_stream = nullptr;
 };
 
@@ -968,7 +969,7 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
         fnl_context::LoopGraph* lg = nullptr;
         for (auto& g : ctx->graphs)
             if (g.key == loop_key) lg = &g;
-        if (!lg && ctx->last_key == loop_key) {
+        if (!lg && ctx->last_key == loop_key && ctx->failed_key != loop_key) {
             // capture the iteration into the WHILE node's body graph
             fnl_context::LoopGraph ng;
             ng.key = loop_key;
@@ -1035,6 +1036,7 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
                 if (ng.exec) cudaGraphExecDestroy(ng.exec);
                 cudaGraphDestroy(ng.graph);
                 m.iter = nullptr;
+                ctx->failed_key = loop_key;
             } else {
                 if (ctx->graphs.size() >= 4) {
                     cudaGraphExecDestroy(ctx->graphs.front().exec);
