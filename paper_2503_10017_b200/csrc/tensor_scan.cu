@@ -1672,6 +1672,7 @@ struct PlanArgs {
     uint32_t tile_begin, ntiles;
     uint32_t sms;
     uint32_t nitems_cap;
+    uint32_t switch_cost;  // modelled cost of starting a work unit, in target tiles
     uint32_t* hdr;  // [0] slots [1] tile pairs [2] items [3] splits [4] tiles per split
     uint32_t* slot_pair;
     uint32_t* slot_base;
@@ -1739,7 +1740,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a) {
         best = sp_min;
         for (uint32_t sp = sp_min; sp <= smax; ++sp) {
             const float waves = (float)((ntp * sp + a.sms - 1) / a.sms);
-            const float cost = waves * (float)((a.ntiles + sp - 1) / sp + 3u);
+            const float cost = waves * (float)((a.ntiles + sp - 1) / sp + a.switch_cost);
             if (cost < best_cost) best_cost = cost, best = sp;
         }
         const uint32_t per = (a.ntiles + best - 1) / best;
@@ -1878,7 +1879,9 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
 
     // ---- K2p plan
     {
-        PlanArgs pa{npairs, d_active, d_done, tile_begin, ntiles, sms, nitems_cap, d_hdr,
+        static const uint32_t switch_cost =
+            getenv("FNL_PLAN_SWITCH") ? (uint32_t)atoi(getenv("FNL_PLAN_SWITCH")) : 3u;
+        PlanArgs pa{npairs, d_active, d_done, tile_begin, ntiles, sms, nitems_cap, switch_cost, d_hdr,
                     d_slot_pair, d_slot_base, d_tp_pair, d_tp_row0, d_tp_qi0, d_items};
         ProfScope prof(ctx, FNL_KCLASS_GATHER);
         plan_kernel<<<1, kPlanThreads, 0, s>>>(pa);
