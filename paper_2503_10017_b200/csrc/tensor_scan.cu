@@ -1391,15 +1391,60 @@ struct RescanArgs {
     const uint32_t* ids;
     uint32_t cap;
     ResolveSrc rs;
+    // finish (the last CTA to retire): winners into out / min_dist, or signed
+    // keys into the shard buffers
+    unsigned int* done_ctr;  // zeroed with the row count before each pass
+    uint32_t* out;
+    float* min_dist;
+    uint32_t out_stride;
+    long long* shard_keys;
+    ShardPeers peers;
 };
 
 constexpr int kRescanThreads = 256;
 
+// rows resolved by the scan below: winners out (one CTA)
+template <bool kL2, int DIM, int MODE>
+__device__ void rescan_finish(const RescanArgs& a, uint32_t n) {
+    for (uint32_t k = threadIdx.x; k < n; k += blockDim.x) {
+        const uint32_t pair = a.rescan[3 * k + 1], qi = a.rescan[3 * k + 2];
+        const uint64_t o = (uint64_t)pair * a.out_stride + qi;
+        const unsigned long long key = a.keys[k];
+        if (a.shard_keys) {
+            shard_emit(a.shard_keys, a.peers, o, (long long)(key ^ 0x8000000000000000ull));
+            a.keys[k] = ~0ull;
+            continue;
+        }
+        const uint32_t idx = (uint32_t)(key & 0xFFFFFFFFull);
+        a.out[o] = idx;
+        if (a.min_dist) {
+            float d = from_orderable((uint32_t)(key >> 32));
+            if (d == 0.0f) {
+                if constexpr (MODE == kResolveHybrid) {  // the winner's own signed zero
+                    float q[kPackK];
+                    mode_query<MODE>(a.qbuf, a.rescan[3 * k], a.rs, a.ids, a.cap, pair, qi, a.dim, q);
+                    d = mode_cmp<MODE>(mode_chain<kL2, DIM, MODE>(q, a.tmap + pair * a.t_pair_bytes, nullptr, idx,
+                                                                    a.dim, a.tcpr));
+                } else {
+                    d = kL2 ? 0.0f : -0.0f;  // canonical sign of an exact zero
+                }
+            }
+            a.min_dist[o] = d;
+        }
+        a.keys[k] = ~0ull;
+    }
+}
+
+// Grid-stride over (row, target chunk) units; the last CTA to retire (a
+// counter, zeroed with the row count before the pass) writes the winners,
+// so a pass with no open rows costs one short launch.
 template <bool kL2, int DIM, int MODE>
 __global__ void __launch_bounds__(kRescanThreads) rescan_kernel(RescanArgs a) {
     const uint64_t count = *a.rescan_count;
+    if (count == 0) return;  // the usual case: nothing to scan, nothing to finish
     const uint64_t nchunks = (a.nt - a.t_begin + a.chunk - 1) / a.chunk;
     __shared__ unsigned long long red[kRescanThreads / 32];
+    __shared__ bool last;
     float q[kPackK];
     for (uint64_t unit = blockIdx.x; unit < count * nchunks; unit += gridDim.x) {
         const uint64_t k = unit / nchunks, ch = unit % nchunks;
@@ -1422,39 +1467,14 @@ __global__ void __launch_bounds__(kRescanThreads) rescan_kernel(RescanArgs a) {
         }
         __syncthreads();
     }
-}
-
-template <bool kL2, int DIM, int MODE>
-__global__ void rescan_finish_kernel(RescanArgs a, uint32_t* out, float* min_dist, uint32_t out_stride,
-                                     long long* shard_keys, ShardPeers peers) {
-    const uint32_t n = *a.rescan_count;
-    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-        const uint32_t pair = a.rescan[3 * k + 1], qi = a.rescan[3 * k + 2];
-        const uint64_t o = (uint64_t)pair * out_stride + qi;
-        const unsigned long long key = a.keys[k];
-        if (shard_keys) {
-            shard_emit(shard_keys, peers, o, (long long)(key ^ 0x8000000000000000ull));
-            a.keys[k] = ~0ull;
-            continue;
-        }
-        const uint32_t idx = (uint32_t)(key & 0xFFFFFFFFull);
-        out[o] = idx;
-        if (min_dist) {
-            float d = from_orderable((uint32_t)(key >> 32));
-            if (d == 0.0f) {
-                if constexpr (MODE == kResolveHybrid) {  // the winner's own signed zero
-                    float q[kPackK];
-                    mode_query<MODE>(a.qbuf, a.rescan[3 * k], a.rs, a.ids, a.cap, pair, qi, a.dim, q);
-                    d = mode_cmp<MODE>(mode_chain<kL2, DIM, MODE>(q, a.tmap + pair * a.t_pair_bytes, nullptr, idx,
-                                                                    a.dim, a.tcpr));
-                } else {
-                    d = kL2 ? 0.0f : -0.0f;  // canonical sign of an exact zero
-                }
-            }
-            min_dist[o] = d;
-        }
-        a.keys[k] = ~0ull;
+    if (threadIdx.x == 0) {
+        __threadfence();  // this CTA's key minima before its retirement
+        last = atomicAdd(a.done_ctr, 1u) == gridDim.x - 1;
     }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    rescan_finish<kL2, DIM, MODE>(a, (uint32_t)count);
 }
 
 __global__ void shard_finalize_kernel(const long long* keys, uint32_t stride, const uint32_t* n_active,
@@ -1624,18 +1644,14 @@ void launch_merge_mode(int mode, uint32_t tp_max, uint32_t sms, const MergeArgs&
     launch_merge_rows<kL2, DIM>(mode, tp_max, m, s, small);
 }
 template <bool kL2, int DIM, int MODE>
-void launch_rescan_t(uint32_t grid, const RescanArgs& r, uint32_t* out, float* min_dist, uint32_t out_stride,
-                     long long* shard_keys, const ShardPeers& pp, cudaStream_t s) {
+void launch_rescan_t(uint32_t grid, const RescanArgs& r, cudaStream_t s) {
     rescan_kernel<kL2, DIM, MODE><<<grid, kRescanThreads, 0, s>>>(r);
-    rescan_finish_kernel<kL2, DIM, MODE><<<4, 256, 0, s>>>(r, out, min_dist, out_stride, shard_keys, pp);
 }
 template <bool kL2, int DIM>
-void launch_rescan_mode(int mode, uint32_t grid, const RescanArgs& r, uint32_t* out, float* min_dist,
-                        uint32_t out_stride, long long* shard_keys, const ShardPeers& pp, cudaStream_t s) {
-    if (mode == kResolveFull) launch_rescan_t<kL2, DIM, kResolveFull>(grid, r, out, min_dist, out_stride, shard_keys, pp, s);
-    else if (mode == kResolveHybrid)
-        launch_rescan_t<kL2, DIM, kResolveHybrid>(grid, r, out, min_dist, out_stride, shard_keys, pp, s);
-    else launch_rescan_t<kL2, DIM, kResolveRounded>(grid, r, out, min_dist, out_stride, shard_keys, pp, s);
+void launch_rescan_mode(int mode, uint32_t grid, const RescanArgs& r, cudaStream_t s) {
+    if (mode == kResolveFull) launch_rescan_t<kL2, DIM, kResolveFull>(grid, r, s);
+    else if (mode == kResolveHybrid) launch_rescan_t<kL2, DIM, kResolveHybrid>(grid, r, s);
+    else launch_rescan_t<kL2, DIM, kResolveRounded>(grid, r, s);
 }
 
 }  // namespace
@@ -1872,9 +1888,9 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     TRY(ws_arr(ctx, "tc.margin", rows_max, &margin));
     TRY(ws_arr(ctx, "tc.partial", (size_t)nitems_cap * kPartialSplit * kQueryTilePair * kPartialF4, &partial));
     TRY(ws_arr(ctx, "tc.rescan", (size_t)3 * rows_max, &rescan));
-    TRY(ws_arr(ctx, "tc.rcount", 1, &rcount));
+    TRY(ws_arr(ctx, "tc.rcount", 2, &rcount));  // [0] open rows, [1] rescan CTAs retired
     TRY(ws_arr(ctx, "tc.keys", rows_max, &keys));
-    FNL_CUDA_TRY(cudaMemsetAsync(rcount, 0, 4, s));
+    FNL_CUDA_TRY(cudaMemsetAsync(rcount, 0, 8, s));
     FNL_CUDA_TRY(cudaMemsetAsync(keys, 0xFF, (size_t)rows_max * 8, s));
 
     // ---- K2p plan
@@ -1934,20 +1950,21 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     // ---- K4' exact re-decision of rows left open (grid-stride over a device count)
     {
         RescanArgs r{rescan, rcount, qbuf, T.data, T.pair_bytes, T.cpr, tile_begin * kBTileRows,
-                     std::min(nt, tile_end * kBTileRows), dim, 4096u, keys, l2, ids, cap, rs};
+                     std::min(nt, tile_end * kBTileRows), dim, 4096u, keys, l2, ids, cap, rs,
+                     rcount + 1, out, min_dist, out_stride, shard_keys, pp};
         const uint32_t grid = 2 * (uint32_t)ctx_sm_count(ctx);
         ProfScope prof(ctx, FNL_KCLASS_RESCAN);
         if (dim == 24) {
-            if (l2) launch_rescan_mode<true, 24>(rs.mode, grid, r, out, min_dist, out_stride, shard_keys, pp, s);
-            else launch_rescan_mode<false, 24>(rs.mode, grid, r, out, min_dist, out_stride, shard_keys, pp, s);
+            if (l2) launch_rescan_mode<true, 24>(rs.mode, grid, r, s);
+            else launch_rescan_mode<false, 24>(rs.mode, grid, r, s);
         } else {
-            if (l2) launch_rescan_mode<true, 0>(rs.mode, grid, r, out, min_dist, out_stride, shard_keys, pp, s);
-            else launch_rescan_mode<false, 0>(rs.mode, grid, r, out, min_dist, out_stride, shard_keys, pp, s);
+            if (l2) launch_rescan_mode<true, 0>(rs.mode, grid, r, s);
+            else launch_rescan_mode<false, 0>(rs.mode, grid, r, s);
         }
         FNL_CUDA_TRY(cudaGetLastError());
     }
     if (debug_mode_trace_dump(ctx, s)) {}
-    ctx_count_launches(ctx, 6);
+    ctx_count_launches(ctx, 5);
     return FNL_OK;
 }
 
