@@ -1747,27 +1747,36 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a) {
         __syncthreads();
     }
     const uint32_t nslots = s_carry[0], ntp = s_carry[1];
-    if (tid == 0) {
-        uint32_t best = 1;
-        float best_cost = 3.0e38f;
+    if (warp == 0) {
+        // the split count with the smallest modelled makespan (first minimum,
+        // i.e. the fewest splits on ties), one candidate per lane
         const uint32_t smax = min(min(a.ntiles, 64u), ntp ? max(1u, a.nitems_cap / ntp) : 1u);
         // a unit spans at most kMaxUnitTiles target tiles (K3's sub-tile keys)
         const uint32_t sp_min = (a.ntiles + kMaxUnitTiles - 1) / kMaxUnitTiles;
-        best = sp_min;
-        for (uint32_t sp = sp_min; sp <= smax; ++sp) {
+        uint32_t best = sp_min;
+        float best_cost = 3.0e38f;
+        for (uint32_t sp = sp_min + lane; sp <= smax; sp += 32) {
             const float waves = (float)((ntp * sp + a.sms - 1) / a.sms);
             const float cost = waves * (float)((a.ntiles + sp - 1) / sp + a.switch_cost);
             if (cost < best_cost) best_cost = cost, best = sp;
         }
-        const uint32_t per = (a.ntiles + best - 1) / best;
-        const uint32_t splits = (a.ntiles + per - 1) / per;
-        s_split[0] = splits;
-        s_split[1] = per;
-        a.hdr[0] = nslots;
-        a.hdr[1] = ntp;
-        a.hdr[2] = ntp * splits;
-        a.hdr[3] = splits;
-        a.hdr[4] = per;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const float oc = __shfl_xor_sync(0xFFFFFFFFu, best_cost, o);
+            const uint32_t os = __shfl_xor_sync(0xFFFFFFFFu, best, o);
+            if (oc < best_cost || (oc == best_cost && os < best)) best_cost = oc, best = os;
+        }
+        if (lane == 0) {
+            const uint32_t per = (a.ntiles + best - 1) / best;
+            const uint32_t splits = (a.ntiles + per - 1) / per;
+            s_split[0] = splits;
+            s_split[1] = per;
+            a.hdr[0] = nslots;
+            a.hdr[1] = ntp;
+            a.hdr[2] = ntp * splits;
+            a.hdr[3] = splits;
+            a.hdr[4] = per;
+        }
     }
     __syncthreads();
     const uint32_t splits = s_split[0], per = s_split[1];
