@@ -697,11 +697,6 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
     const uint32_t max_calls = 2 * T + 1;
     TRY(dev_arr(ctx, "m.counters", (size_t)max_calls * npairs * 2, &counters));
     cudaStream_t s = ctx->stream;
-    FNL_CUDA_TRY(cudaMemsetAsync(m.used_i, 0, (size_t)npairs * m.words_i * 4, s));
-    FNL_CUDA_TRY(cudaMemsetAsync(m.used_j, 0, (size_t)npairs * m.words_j * 4, s));
-    FNL_CUDA_TRY(cudaMemsetAsync(m.n_done, 0, 4, s));
-    FNL_CUDA_TRY(cudaMemsetAsync(keys, 0xFF, pc * 8, s));
-    FNL_CUDA_TRY(cudaMemsetAsync(counters, 0, (size_t)max_calls * npairs * 16, s));
     FNL_CUDA_TRY(cudaMemsetAsync(bad, 0xFF, 16, s));
 
     // ---- K1: binary16 pack for the tensor route, or validate + (hybrid)
@@ -739,7 +734,6 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
     unsigned long long *near_ties = nullptr, *tsat = nullptr;
     TRY(dev_arr(ctx, "m.neartie", 2 * (size_t)npairs, &near_ties));
     TRY(dev_arr(ctx, "m.tsat", 2 * (size_t)npairs, &tsat));
-    FNL_CUDA_TRY(cudaMemsetAsync(near_ties, 0, (size_t)npairs * 16, s));
     FNL_CUDA_TRY(cudaMemsetAsync(tsat, 0, (size_t)npairs * 16, s));
     const bool fits = dim + (l2 ? 2u : 0u) <= fnl::kPackK;
     if ((tensor && fits) || (!tensor && fits && !force_cuda_core())) {
@@ -925,6 +919,13 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
     }
     // sampling, the memo reset and the first forward pass (src/reciprocal.cpp:128-139)
     auto prefix = [&]() -> int {
+        // loop state (inside the loop graph when it replays)
+        FNL_CUDA_TRY(cudaMemsetAsync(m.used_i, 0, (size_t)npairs * m.words_i * 4, s));
+        FNL_CUDA_TRY(cudaMemsetAsync(m.used_j, 0, (size_t)npairs * m.words_j * 4, s));
+        FNL_CUDA_TRY(cudaMemsetAsync(m.n_done, 0, 4, s));
+        FNL_CUDA_TRY(cudaMemsetAsync(keys, 0xFF, pc * 8, s));
+        FNL_CUDA_TRY(cudaMemsetAsync(counters, 0, (size_t)max_calls * npairs * 16, s));
+        FNL_CUDA_TRY(cudaMemsetAsync(near_ties, 0, (size_t)npairs * 16, s));
         timer.begin(kPhaseSubsample);
         {
             fnl::ProfScope prof(ctx, FNL_KCLASS_HARVEST);
