@@ -278,3 +278,30 @@ def test_loop_graph_replay_matches_reference(fnl, ref, npairs, max_iters, backen
     # every later call replays the graph (the fourth on new maps)
     replays = [ln for ln in capfd.readouterr().err.splitlines() if ln.startswith("fnl loop graph: replay")]
     assert len(replays) == 5 and all(ln.startswith("fnl loop graph: replay 1") for ln in replays[1:]), replays
+
+
+def test_loop_graph_misspeculation_reruns(fnl, ref, monkeypatch, capfd):
+    # a cached loop graph is replayed ahead of the pack's route read-back; when
+    # the new maps take another route (here: norms too large for binary16
+    # accumulators, then saturating values that leave the tensor route) the
+    # call re-runs behind the speculative replay and still returns the
+    # reference's MatchSets
+    import torch
+    H, W, D = 64, 48, 24
+    d1 = torch.empty((2, H, W, D), dtype=torch.float32, device="cuda")
+    d2 = torch.empty_like(d1)
+    out = torch.empty((2, 48, 3), dtype=torch.int32, device="cuda")
+    cnt = torch.empty((2,), dtype=torch.int32, device="cuda")
+    base1 = np.stack([ref.gen_random(H, W, D, 900 + i) for i in range(2)])
+    base2 = np.stack([ref.gen_random(H, W, D, 950 + i) for i in range(2)])
+    for call, scale in enumerate([1.0, 1.0, 1.0, 300.0, 1.0, 70000.0, 1.0]):
+        a, b = base1 * np.float32(scale), base2 * np.float32(scale)
+        d1.copy_(torch.from_numpy(a))
+        d2.copy_(torch.from_numpy(b))
+        fnl.reciprocal_match_device(d1.data_ptr(), d2.data_ptr(), 2, H, W, D, out.data_ptr(), cnt.data_ptr(),
+                                    backend="single", metric="dot", with_stats=False)
+        torch.cuda.synchronize()
+        o, c = out.cpu().numpy(), cnt.cpu().numpy()
+        for i in range(2):
+            want, _ = ref.reciprocal_match(a[i], b[i], backend="single", metric="dot")
+            assert np.array_equal(o[i][: c[i]].astype(np.int64), np.asarray(want, np.int64)), (call, scale, i)
