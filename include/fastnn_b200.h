@@ -164,7 +164,7 @@ int fnl_reciprocal_match_batch(fnl_context* ctx, uint32_t npairs, const float* h
  * validate like the reference); they still take the route that keeps the
  * results identical to the reference's arithmetic on those values.  The maps
  * must be 16-byte aligned (FNL_EINVAL otherwise).  With h_stats == NULL and
- * npairs <= 16 the second call with the same buffers and configuration
+ * npairs <= 64 the second call with the same buffers and configuration
  * captures the reciprocal loop as one CUDA graph (a WHILE node whose
  * condition the device sets) and later calls replay it: no per-iteration
  * host read, one graph launch after the pack's route read-back

@@ -643,7 +643,12 @@ int check_cfg(const fnl_match_config* cfg) {
 }
 
 // batches up to this many pairs replay the reciprocal loop as a CUDA graph
-constexpr uint32_t kLoopGraphMaxPairs = 16;
+// (FNL_LOOP_GRAPH_MAX overrides)
+uint32_t loop_graph_max_pairs() {
+    static const uint32_t v =
+        getenv("FNL_LOOP_GRAPH_MAX") ? (uint32_t)atoi(getenv("FNL_LOOP_GRAPH_MAX")) : 64u;
+    return v;
+}
 
 // The device-resident matcher over npairs stacked pairs.  d_d1 / d_d2 are raw
 // fp32 maps on the device.  Results stay on the device in the MatchState.
@@ -777,7 +782,7 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
             FNL_CUDA_TRY(cudaMemcpyAsync(hn, T1.max_norm, npairs * 4, cudaMemcpyDeviceToHost, s));
             FNL_CUDA_TRY(cudaMemcpyAsync(hn + npairs, T2.max_norm, npairs * 4, cudaMemcpyDeviceToHost, s));
             if (graph_env && !validate && !shard && !h_stats && !ctx->profile_all && samples > 0 &&
-                npairs <= kLoopGraphMaxPairs && !ctx->graphs.empty()) {
+                npairs <= loop_graph_max_pairs() && !ctx->graphs.empty()) {
                 const std::vector<uint64_t> k = make_key(true, memo_env);
                 for (auto& g : ctx->graphs)
                     if (g.key == k) spec = &g;
@@ -981,7 +986,7 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
     bool replayed = false;
     std::vector<uint64_t> loop_key;
     const bool graph_ok = graph_env && tc && !sharded && !h_stats && !ctx->profile_all && samples > 0 &&
-                          npairs <= kLoopGraphMaxPairs;
+                          npairs <= loop_graph_max_pairs();
     if (graph_ok) {
         loop_key = make_key(acc16, memo);
         uint32_t* d_iter = nullptr;
