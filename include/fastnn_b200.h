@@ -341,6 +341,15 @@ enum {
 int fnl_kernel_profile(fnl_context* ctx, int enable, int reset, double* class_ms,
                        uint64_t* class_launches);
 
+/* Largest batch (pairs per call) whose reciprocal loop is captured and
+ * replayed as a CUDA graph (see fnl_reciprocal_match_batch_device); 0 turns
+ * the graph off for this context.  Kernels inside a replayed graph are not
+ * bracketed by the fnl_kernel_timing / fnl_kernel_profile events, so a
+ * caller that times the dominant kernel keeps its batches host-driven.
+ * max_pairs < 0 only queries; *previous (may be NULL) receives the value in
+ * force before the call (default 64, or FNL_LOOP_GRAPH_MAX). */
+int fnl_loop_graph_max_pairs(fnl_context* ctx, int max_pairs, int* previous);
+
 #ifdef __cplusplus
 }
 #endif

@@ -28,6 +28,7 @@ try:
         grid_subsample,
         kernel_profile,
         kernel_timing,
+        loop_graph_max_pairs,
         mutual_nn_exact,
         mutual_nn_tensor,
         nn_bruteforce,
@@ -74,6 +75,7 @@ __all__ = [
     "reciprocal_match_device",
     "kernel_timing",
     "kernel_profile",
+    "loop_graph_max_pairs",
     "flashmatch",
     "device_count",
     "set_device",

@@ -630,6 +630,15 @@ PYBIND11_MODULE(_fastnn, m) {
           py::arg("reset") = false,
           "device time and launch count of the dominant scoring kernel since the last reset");
 
+    m.def("loop_graph_max_pairs",
+          [](int max_pairs) {
+              int prev = 0;
+              fastnn::b200::check(fnl_loop_graph_max_pairs(fastnn::b200::context(), max_pairs, &prev));
+              return prev;
+          },
+          py::arg("max_pairs") = -1,
+          "Largest batch whose reciprocal loop replays as a CUDA graph on this thread's context (0: off; "
+          "negative: query only); returns the previous value.");
     m.def("kernel_profile",
           [](int enable, bool reset) {
               double ms[FNL_KCLASS_COUNT] = {};

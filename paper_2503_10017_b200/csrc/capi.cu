@@ -78,6 +78,7 @@ struct fnl_context {
     std::vector<LoopGraph> graphs;
     std::vector<uint64_t> last_key;  // loop key of the previous host-driven run
     std::vector<uint64_t> failed_key;  // a configuration whose capture failed (not retried)
+    int loop_graph_max = -1;           // fnl_loop_graph_max_pairs (-1: the default)
     cudaStream_t cap_stream = nullptr;
     cudaEvent_t route_ev = nullptr;  // the pack's route read-back landed (speculative replay)
 };
@@ -85,6 +86,14 @@ struct fnl_context {
 namespace {
 
 using fnl::fail_cuda;
+
+// batches up to this many pairs replay the reciprocal loop as a CUDA graph
+// (FNL_LOOP_GRAPH_MAX, or fnl_loop_graph_max_pairs per context)
+uint32_t loop_graph_max_pairs(const fnl_context* ctx) {
+    static const uint32_t v =
+        getenv("FNL_LOOP_GRAPH_MAX") ? (uint32_t)atoi(getenv("FNL_LOOP_GRAPH_MAX")) : 64u;
+    return ctx && ctx->loop_graph_max >= 0 ? (uint32_t)ctx->loop_graph_max : v;
+}
 
 int check_device(fnl_context* ctx) {
     if (!ctx) return fail(FNL_EINVAL, "fastnn_b200: null context");
@@ -441,6 +450,13 @@ extern "C" int fnl_kernel_timing(fnl_context* ctx, int reset, double* score_ms,
     return FNL_OK;
 }
 
+extern "C" int fnl_loop_graph_max_pairs(fnl_context* ctx, int max_pairs, int* previous) {
+    if (!ctx) return fail(FNL_EINVAL, "fastnn_b200: null context");
+    if (previous) *previous = (int)loop_graph_max_pairs(ctx);
+    if (max_pairs >= 0) ctx->loop_graph_max = max_pairs;
+    return FNL_OK;
+}
+
 extern "C" int fnl_kernel_profile(fnl_context* ctx, int enable, int reset, double* class_ms,
                                   uint64_t* class_launches) {
     TRY(check_device(ctx));
@@ -642,13 +658,7 @@ int check_cfg(const fnl_match_config* cfg) {
     return FNL_OK;
 }
 
-// batches up to this many pairs replay the reciprocal loop as a CUDA graph
-// (FNL_LOOP_GRAPH_MAX overrides)
-uint32_t loop_graph_max_pairs() {
-    static const uint32_t v =
-        getenv("FNL_LOOP_GRAPH_MAX") ? (uint32_t)atoi(getenv("FNL_LOOP_GRAPH_MAX")) : 64u;
-    return v;
-}
+
 
 // The device-resident matcher over npairs stacked pairs.  d_d1 / d_d2 are raw
 // fp32 maps on the device.  Results stay on the device in the MatchState.
@@ -782,7 +792,7 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
             FNL_CUDA_TRY(cudaMemcpyAsync(hn, T1.max_norm, npairs * 4, cudaMemcpyDeviceToHost, s));
             FNL_CUDA_TRY(cudaMemcpyAsync(hn + npairs, T2.max_norm, npairs * 4, cudaMemcpyDeviceToHost, s));
             if (graph_env && !validate && !shard && !h_stats && !ctx->profile_all && samples > 0 &&
-                npairs <= loop_graph_max_pairs() && !ctx->graphs.empty()) {
+                npairs <= loop_graph_max_pairs(ctx) && !ctx->graphs.empty()) {
                 const std::vector<uint64_t> k = make_key(true, memo_env);
                 for (auto& g : ctx->graphs)
                     if (g.key == k) spec = &g;
@@ -986,7 +996,7 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
     bool replayed = false;
     std::vector<uint64_t> loop_key;
     const bool graph_ok = graph_env && tc && !sharded && !h_stats && !ctx->profile_all && samples > 0 &&
-                          npairs <= loop_graph_max_pairs();
+                          npairs <= loop_graph_max_pairs(ctx);
     if (graph_ok) {
         loop_key = make_key(acc16, memo);
         uint32_t* d_iter = nullptr;
