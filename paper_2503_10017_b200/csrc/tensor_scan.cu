@@ -710,7 +710,9 @@ __device__ __forceinline__ float tile_max64_h(const Frag& f, uint32_t sub, uint3
 // dot metric only, margin widened in K2): a warp reads its 128 columns with
 // ONE packed tcgen05.ld (64 registers), releases the accumulator at once and
 // reduces afterwards with max.f16x2 trees.
-template <bool kF16>
+// kDebug: the profiling aids of TcArgs::debug (clock trace, unread release)
+// are compiled in; the production instantiation carries none of them.
+template <bool kF16, bool kDebug>
 __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
     constexpr uint32_t kIdesc = kF16 ? (kIdescF16M128N128 & ~(1u << 4)) : kIdescF16M128N128;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -727,7 +729,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t G = gridDim.x;
-    const bool trace = (a.debug & 16) && blockIdx.x == 0;
+    const bool trace = kDebug && (a.debug & 16) && blockIdx.x == 0;
     const uint32_t nitems = *a.nitems;
     if (blockIdx.x >= nitems) return;  // CTA-uniform, before any barrier or TMEM allocation
 
@@ -901,7 +903,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
                 // chain (qt 0, half 0): every quadrant's wake and release (k < 1024)
                 const bool tq = kF16 && trace && e < 4 && k < 1024;  // (binary16 path only: registers)
                 if (tq && lane == 0) a.trace[16384 + quad * 1024 + k] = clock64();
-                if (!warp_real || (a.debug & 1)) {  // nothing to score: hand the buffer straight back
+                if (!warp_real || (kDebug && (a.debug & 1))) {  // nothing to score: hand the buffer straight back
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&accfree[qt * 2 + h]);
                     continue;
@@ -1612,8 +1614,10 @@ int ensure_attrs() {
     FNL_CUDA_TRY(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lk(attr_mu);
     if (dev >= 0 && dev < 64 && attr_done[dev]) return FNL_OK;
-    FNL_CUDA_TRY(cudaFuncSetAttribute(tc_scan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal));
-    FNL_CUDA_TRY(cudaFuncSetAttribute(tc_scan_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal));
+    FNL_CUDA_TRY(cudaFuncSetAttribute(tc_scan_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal));
+    FNL_CUDA_TRY(cudaFuncSetAttribute(tc_scan_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal));
+    FNL_CUDA_TRY(cudaFuncSetAttribute(tc_scan_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal));
+    FNL_CUDA_TRY(cudaFuncSetAttribute(tc_scan_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal));
     FNL_CUDA_TRY(cudaFuncSetAttribute(selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal));
     FNL_CUDA_TRY(cudaFuncSetAttribute(pack_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kPackStages * kPackTileRows * kPackK * 4));
@@ -1935,8 +1939,13 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
         const uint32_t grid = std::min<uint32_t>(nitems_cap, sms);
         cudaEvent_t end_ev;
         ctx_score_begin(ctx, &end_ev);
-        if (acc16) tc_scan_kernel<true><<<grid, kScanThreads, kSmemTotal, s>>>(t);
-        else tc_scan_kernel<false><<<grid, kScanThreads, kSmemTotal, s>>>(t);
+        if (debug_mode) {
+            if (acc16) tc_scan_kernel<true, true><<<grid, kScanThreads, kSmemTotal, s>>>(t);
+            else tc_scan_kernel<false, true><<<grid, kScanThreads, kSmemTotal, s>>>(t);
+        } else {
+            if (acc16) tc_scan_kernel<true, false><<<grid, kScanThreads, kSmemTotal, s>>>(t);
+            else tc_scan_kernel<false, false><<<grid, kScanThreads, kSmemTotal, s>>>(t);
+        }
         ctx_score_end(ctx, end_ev);
         FNL_CUDA_TRY(cudaGetLastError());
     }
