@@ -89,7 +89,7 @@ __device__ __forceinline__ float ex2(float x) {
 __device__ unsigned long long g_fm_trace[64];
 #define FM_STAMP(i)                                                         \
     do {                                                                    \
-        if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && \
+        if (kTrace && a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && \
             threadIdx.x == 0 && (i) < 64)                                   \
             g_fm_trace[(i)] = clock64();                                    \
     } while (0)
@@ -97,7 +97,7 @@ __device__ unsigned long long g_fm_trace[64];
 // same, from lane 0 of whichever warp executes it
 #define FM_STAMP_L(i)                                                                              \
     do {                                                                                           \
-        if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (threadIdx.x & 31) == 0) \
+        if (kTrace && a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (threadIdx.x & 31) == 0) \
             g_fm_trace[(i)] = clock64();                                                           \
     } while (0)
 
@@ -170,7 +170,8 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map
 // kH = threads per query row (2: 16 softmax warps, 64 key columns each, row
 // max / sum halves meet in shared memory; 1: 8 softmax warps, a whole
 // 128-column row per thread in 128 registers, no exchange).
-template <int kH>
+// kTrace: the FNL_FM_TRACE clock stamps are compiled in (profiling only)
+template <int kH, bool kTrace>
 __global__ void __launch_bounds__((8 * kH + 2) * 32, 1)
     flashmatch4_kernel(FmArgs a, const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                        const __grid_constant__ CUtensorMap tv) {
@@ -444,8 +445,10 @@ int flashmatch_forward(fnl_context* ctx, const fnl_attention_desc& d) {
         FNL_CUDA_TRY(cudaGetDevice(&dev));
         std::lock_guard<std::mutex> lk(fm_attr_mu);
         if (dev < 0 || dev >= 64 || !fm_attr_done[dev]) {
-            FNL_CUDA_TRY(cudaFuncSetAttribute(flashmatch4_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFm4));
-            FNL_CUDA_TRY(cudaFuncSetAttribute(flashmatch4_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFm4));
+            FNL_CUDA_TRY(cudaFuncSetAttribute(flashmatch4_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFm4));
+            FNL_CUDA_TRY(cudaFuncSetAttribute(flashmatch4_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFm4));
+            FNL_CUDA_TRY(cudaFuncSetAttribute(flashmatch4_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFm4));
+            FNL_CUDA_TRY(cudaFuncSetAttribute(flashmatch4_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFm4));
             if (dev >= 0 && dev < 64) fm_attr_done[dev] = true;
         }
     }
@@ -507,9 +510,9 @@ int flashmatch_forward(fnl_context* ctx, const fnl_attention_desc& d) {
         const int row_threads = force_rt == 1 || force_rt == 2 ? force_rt : (a.tiles == 1 ? 1 : 2);
         const dim3 grid4((d.nq + a.tiles * kBlockQ - 1) / (a.tiles * kBlockQ), d.heads, d.batch);
         if (row_threads == 1)
-            flashmatch4_kernel<1><<<grid4, (8 * 1 + 2) * 32, kSmemFm4, s>>>(a, tq, tk, tv);
+            (a.trace ? flashmatch4_kernel<1, true> : flashmatch4_kernel<1, false>)<<<grid4, (8 * 1 + 2) * 32, kSmemFm4, s>>>(a, tq, tk, tv);
         else
-            flashmatch4_kernel<2><<<grid4, (8 * 2 + 2) * 32, kSmemFm4, s>>>(a, tq, tk, tv);
+            (a.trace ? flashmatch4_kernel<2, true> : flashmatch4_kernel<2, false>)<<<grid4, (8 * 2 + 2) * 32, kSmemFm4, s>>>(a, tq, tk, tv);
     }
     FNL_CUDA_TRY(cudaGetLastError());
     ctx_count_launches(ctx, 1);
