@@ -985,14 +985,17 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
         }
         return FNL_OK;
     };
-    // ---- small batches: the loop is launch-bound (a pass is a few tens of
-    // microseconds of GPU work behind ~40 us of host launch cost), so it runs
-    // as ONE CUDA graph: a WHILE node whose body is an iteration (reverse
-    // pass, harvest, condition kernel, forward pass) and whose condition the
-    // device sets (some pair not done and t < T).  Captured on the second run
-    // with an identical configuration (same buffers, shapes, route and
-    // workspace), replayed afterwards; the forward pass after the last
-    // harvest sees every pair done and does nothing.
+    // ---- batches up to loop_graph_max_pairs (64): a small batch's loop is
+    // launch-bound (a pass is a few tens of microseconds of GPU work behind
+    // ~40 us of host launch cost), so it runs as ONE CUDA graph: the prefix
+    // (state reset, sampling, memo reset, first forward pass), then a WHILE
+    // node whose body is an iteration (reverse pass, harvest, condition
+    // kernel, forward pass) and whose condition the device sets (some pair not
+    // done and t < T).  Captured on the second run with an identical
+    // configuration (same buffers, shapes, route and workspace), replayed
+    // afterwards (speculatively, right behind the pack, when the route read
+    // back above matches); the forward pass after the last harvest sees every
+    // pair done and does nothing.
     bool replayed = false;
     std::vector<uint64_t> loop_key;
     const bool graph_ok = graph_env && tc && !sharded && !h_stats && !ctx->profile_all && samples > 0 &&
