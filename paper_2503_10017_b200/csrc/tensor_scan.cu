@@ -846,7 +846,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) tc_scan_kernel(TcArgs a) {
                 for (uint32_t h = 0; h < 2; ++h) {
                     // each 128-target half of the tile is its own accumulator chain,
                     // refilled as soon as its four epilogue warps drained it
-                    mbar_wait(&accfree[qt * 2 + h], (kq & 1u) ^ 1u);
+                    mbar_spin(&accfree[qt * 2 + h], (kq & 1u) ^ 1u);
                     if (trace && qt == 0 && lane == 0 && k < 4096) a.trace[8192 + h * 4096 + k] = clock64();
                     tc_fence_after();
                     if (elect_one()) {
