@@ -53,6 +53,7 @@ struct fnl_context {
     };
     std::map<std::string, Buf> dev;
     std::map<std::string, Buf> pinned;
+    std::map<std::string, std::pair<const void*, size_t>> initialised;  // ws_fresh
     // instrumentation of the dominant scoring kernel
     bool timing = true;
     bool profile_all = false;  // per-kernel-class breakdown (fnl_kernel_profile)
@@ -325,6 +326,12 @@ cudaStream_t ctx_stream(fnl_context* ctx) { return ctx->stream; }
 int ctx_sm_count(fnl_context* ctx) { return ctx->sm_count; }
 int ws_device(fnl_context* ctx, const char* name, size_t bytes, void** out) {
     return dev_buf(ctx, name, bytes, out);
+}
+bool ws_fresh(fnl_context* ctx, const char* name, const void* p, size_t bytes) {
+    auto& seen = ctx->initialised[name];
+    if (seen.first == p && seen.second == bytes) return false;
+    seen = {p, bytes};
+    return true;
 }
 int ws_pinned(fnl_context* ctx, const char* name, size_t bytes, void** out) {
     auto& b = ctx->pinned[name];

@@ -22,6 +22,9 @@ int ctx_sm_count(fnl_context* ctx);
 // grow-only named device / pinned-host workspace slots
 int ws_device(fnl_context* ctx, const char* name, size_t bytes, void** out);
 int ws_pinned(fnl_context* ctx, const char* name, size_t bytes, void** out);
+// true the first time workspace slot `name` is seen at address p with this
+// size (its contents still need their one-time initialisation)
+bool ws_fresh(fnl_context* ctx, const char* name, const void* p, size_t bytes);
 template <typename T>
 int ws_arr(fnl_context* ctx, const char* name, size_t count, T** out) {
     void* p = nullptr;

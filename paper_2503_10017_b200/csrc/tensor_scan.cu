@@ -1904,7 +1904,10 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     TRY(ws_arr(ctx, "tc.rcount", 2, &rcount));  // [0] open rows, [1] rescan CTAs retired
     TRY(ws_arr(ctx, "tc.keys", rows_max, &keys));
     FNL_CUDA_TRY(cudaMemsetAsync(rcount, 0, 8, s));
-    FNL_CUDA_TRY(cudaMemsetAsync(keys, 0xFF, (size_t)rows_max * 8, s));
+    // the rescan's finish hands every key it used back as ~0, so the key
+    // slots need their initialisation only once per allocation
+    if (ws_fresh(ctx, "tc.keys", keys, (size_t)rows_max * 8))
+        FNL_CUDA_TRY(cudaMemsetAsync(keys, 0xFF, (size_t)rows_max * 8, s));
 
     // ---- K2p plan
     {
