@@ -955,7 +955,8 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
     }
     auto reverse_pass = [&]() -> int {
         if (!memo) return nn_pass(P2, p2, m.active_v, P1, p1, m.back);
-        FNL_CUDA_TRY(cudaMemsetAsync(m.rev_n, 0, (size_t)npairs * 4, s));
+        // (rev_compact writes rev_n of every pair still running; a finished
+        // pair's count is never read, so no reset is needed)
         FNL_CUDA_TRY(fnl::launch_rev_lookup(m, s));
         TRY(nn_pass(P2, p2, m.rev_list, P1, p1, m.rev_out, m.rev_n));
         FNL_CUDA_TRY(fnl::launch_rev_fill(m, s));

@@ -1700,6 +1700,7 @@ struct PlanArgs {
     uint32_t* tp_row0;
     uint32_t* tp_qi0;
     TcItem* items;
+    unsigned int* rescan_ctr;  // [2] open-row count and retired rescan CTAs, zeroed here
 };
 
 constexpr int kPlanThreads = 1024;
@@ -1709,7 +1710,10 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a) {
     __shared__ uint32_t s_carry[2];
     __shared__ uint32_t s_split[2];
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_carry[0] = s_carry[1] = 0;
+    if (tid == 0) {
+        s_carry[0] = s_carry[1] = 0;
+        a.rescan_ctr[0] = a.rescan_ctr[1] = 0u;  // the pass's merge / rescan counters
+    }
     __syncthreads();
     for (uint32_t base = 0; base < a.npairs; base += kPlanThreads) {
         const uint32_t p = base + tid;
@@ -1903,7 +1907,6 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
     TRY(ws_arr(ctx, "tc.rescan", (size_t)3 * rows_max, &rescan));
     TRY(ws_arr(ctx, "tc.rcount", 2, &rcount));  // [0] open rows, [1] rescan CTAs retired
     TRY(ws_arr(ctx, "tc.keys", rows_max, &keys));
-    FNL_CUDA_TRY(cudaMemsetAsync(rcount, 0, 8, s));
     // the rescan's finish hands every key it used back as ~0, so the key
     // slots need their initialisation only once per allocation
     if (ws_fresh(ctx, "tc.keys", keys, (size_t)rows_max * 8))
@@ -1914,7 +1917,7 @@ int tensor_nn_pass(fnl_context* ctx, uint32_t npairs, const PackedMaps& Q, const
         static const uint32_t switch_cost =
             getenv("FNL_PLAN_SWITCH") ? (uint32_t)atoi(getenv("FNL_PLAN_SWITCH")) : 3u;
         PlanArgs pa{npairs, d_active, d_done, tile_begin, ntiles, sms, nitems_cap, switch_cost, d_hdr,
-                    d_slot_pair, d_slot_base, d_tp_pair, d_tp_row0, d_tp_qi0, d_items};
+                    d_slot_pair, d_slot_base, d_tp_pair, d_tp_row0, d_tp_qi0, d_items, rcount};
         ProfScope prof(ctx, FNL_KCLASS_GATHER);
         plan_kernel<<<1, kPlanThreads, 0, s>>>(pa);
         FNL_CUDA_TRY(cudaGetLastError());
