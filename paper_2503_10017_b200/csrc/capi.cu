@@ -975,9 +975,10 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
         FNL_CUDA_TRY(cudaMemsetAsync(m.used_i, 0, (size_t)npairs * m.words_i * 4, s));
         FNL_CUDA_TRY(cudaMemsetAsync(m.used_j, 0, (size_t)npairs * m.words_j * 4, s));
         FNL_CUDA_TRY(cudaMemsetAsync(m.n_done, 0, 4, s));
-        FNL_CUDA_TRY(cudaMemsetAsync(keys, 0xFF, pc * 8, s));
-        FNL_CUDA_TRY(cudaMemsetAsync(counters, 0, (size_t)max_calls * npairs * 16, s));
-        FNL_CUDA_TRY(cudaMemsetAsync(near_ties, 0, (size_t)npairs * 16, s));
+        // CUDA-core path state, and counters only the RunReport reads
+        if (!tc) FNL_CUDA_TRY(cudaMemsetAsync(keys, 0xFF, pc * 8, s));
+        if (!tc || h_stats) FNL_CUDA_TRY(cudaMemsetAsync(counters, 0, (size_t)max_calls * npairs * 16, s));
+        if (h_stats) FNL_CUDA_TRY(cudaMemsetAsync(near_ties, 0, (size_t)npairs * 16, s));
         timer.begin(kPhaseSubsample);
         {
             fnl::ProfScope prof(ctx, FNL_KCLASS_HARVEST);
