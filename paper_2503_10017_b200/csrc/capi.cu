@@ -721,7 +721,6 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
     const uint32_t max_calls = 2 * T + 1;
     TRY(dev_arr(ctx, "m.counters", (size_t)max_calls * npairs * 2, &counters));
     cudaStream_t s = ctx->stream;
-    FNL_CUDA_TRY(cudaMemsetAsync(bad, 0xFF, 16, s));
 
     // ---- K1: binary16 pack for the tensor route, or validate + (hybrid)
     // round for the CUDA-core exact scan.  Every backend takes the tensor
@@ -757,8 +756,15 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
     fnl::PackedMaps T1, T2;
     unsigned long long *near_ties = nullptr, *tsat = nullptr;
     TRY(dev_arr(ctx, "m.neartie", 2 * (size_t)npairs, &near_ties));
-    TRY(dev_arr(ctx, "m.tsat", 2 * (size_t)npairs, &tsat));
-    FNL_CUDA_TRY(cudaMemsetAsync(tsat, 0, (size_t)npairs * 16, s));
+    // the pack's per-pair outputs in one region, read back by one copy:
+    // [first non-finite index: 2n u64 (~0)][saturations: 2n u64 (0)]
+    // [norm maxima of map 1: 2n f32 (0)][of map 2: 2n f32 (0)]
+    unsigned long long* route = nullptr;
+    const size_t route_bytes = (size_t)npairs * 48;
+    TRY(dev_arr(ctx, "m.route", (size_t)npairs * 6, &route));
+    tsat = route + 2 * (size_t)npairs;
+    float* maxn = reinterpret_cast<float*>(route + 4 * (size_t)npairs);
+    FNL_CUDA_TRY(cudaMemsetAsync(tsat, 0, (size_t)npairs * 32, s));
     // loop-graph keys (see the graph block below); the replay can start right
     // behind the pack's route read-back when the configuration already has a
     // graph for the route it took last time (speculation: a different route
@@ -776,28 +782,26 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
     fnl_context::LoopGraph* spec = nullptr;  // replay launched ahead of the route decision
     const bool fits = dim + (l2 ? 2u : 0u) <= fnl::kPackK;
     if ((tensor && fits) || (!tensor && fits && !force_cuda_core())) {
-        unsigned long long* tbad;
-        TRY(dev_arr(ctx, "m.tbad", 2 * (size_t)npairs, &tbad));
+        unsigned long long* tbad = route;
         FNL_CUDA_TRY(cudaMemsetAsync(tbad, 0xFF, (size_t)npairs * 16, s));
-        TRY(fnl::tensor_pack(ctx, "m.t1", d_d1, npairs, p1, dim, l2, tbad, tsat, &T1));
-        TRY(fnl::tensor_pack(ctx, "m.t2", d_d2, npairs, p2, dim, l2, tbad + npairs, tsat + npairs, &T2));
+        TRY(fnl::tensor_pack(ctx, "m.t1", d_d1, npairs, p1, dim, l2, tbad, tsat, &T1, maxn));
+        TRY(fnl::tensor_pack(ctx, "m.t2", d_d2, npairs, p2, dim, l2, tbad + npairs, tsat + npairs, &T2,
+                             maxn + 2 * (size_t)npairs));
         tc = true;
         // The host reads the pack's per-pair finiteness / norms / saturations
         // (one small round trip): to validate like the reference FeatureMap
         // (host-buffer entry points), to check the route, and to choose the
         // K3 accumulator (binary16 when every pair's norms allow it).
         {
-            // pinned staging: the four copies are DMA'd back to back behind the
-            // packs and the host waits once (pageable copies each block)
+            // one pinned copy of the whole region behind the packs; the host
+            // waits once (pageable copies each block)
             void* pin = nullptr;
-            TRY(fnl::ws_pinned(ctx, "m.route", (size_t)npairs * (16 + 16 + 8), &pin));
+            TRY(fnl::ws_pinned(ctx, "m.route", route_bytes, &pin));
             unsigned long long* hb = static_cast<unsigned long long*>(pin);
             unsigned long long* hs = hb + 2 * (size_t)npairs;
-            float* hn = reinterpret_cast<float*>(hs + 2 * (size_t)npairs);
-            FNL_CUDA_TRY(cudaMemcpyAsync(hb, tbad, (size_t)npairs * 16, cudaMemcpyDeviceToHost, s));
-            FNL_CUDA_TRY(cudaMemcpyAsync(hs, tsat, (size_t)npairs * 16, cudaMemcpyDeviceToHost, s));
-            FNL_CUDA_TRY(cudaMemcpyAsync(hn, T1.max_norm, npairs * 4, cudaMemcpyDeviceToHost, s));
-            FNL_CUDA_TRY(cudaMemcpyAsync(hn + npairs, T2.max_norm, npairs * 4, cudaMemcpyDeviceToHost, s));
+            const float* hn1 = reinterpret_cast<const float*>(hs + 2 * (size_t)npairs);  // map 1 maxima
+            const float* hn2 = hn1 + 2 * (size_t)npairs;                                    // map 2 maxima
+            FNL_CUDA_TRY(cudaMemcpyAsync(hb, route, route_bytes, cudaMemcpyDeviceToHost, s));
             if (graph_env && !validate && !shard && !h_stats && !ctx->profile_all && samples > 0 &&
                 npairs <= loop_graph_max_pairs(ctx) && !ctx->graphs.empty()) {
                 const std::vector<uint64_t> k = make_key(true, memo_env);
@@ -821,10 +825,10 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
                     if (hb[npairs + p] != ~0ull) return fail(FNL_EINVAL, nonfinite_msg(hb[npairs + p]));
             }
             for (uint32_t p = 0; p < npairs && tc; ++p)
-                tc = fnl::tensor_route_ok(mode, l2, dim, hn[p], hn[npairs + p], hs[p] + hs[npairs + p],
+                tc = fnl::tensor_route_ok(mode, l2, dim, hn1[p], hn2[p], hs[p] + hs[npairs + p],
                                           std::min(hb[p], hb[npairs + p]));
             acc16 = tc;
-            for (uint32_t p = 0; p < npairs && acc16; ++p) acc16 = fnl::acc16_ok(l2, hn[p], hn[npairs + p]);
+            for (uint32_t p = 0; p < npairs && acc16; ++p) acc16 = fnl::acc16_ok(l2, hn1[p], hn2[p]);
         }
     }
     if (shard && !tc)
@@ -833,6 +837,7 @@ int run_match(fnl_context* ctx, uint32_t npairs, const float* d_d1, uint32_t h1,
     if (!tc) {
         // the tensor backend's contract is ref single on binary16-rounded
         // rows: K4 on the rounded rows, fp32 compare
+        FNL_CUDA_TRY(cudaMemsetAsync(bad, 0xFF, 16, s));
         TRY(prepare_maps(ctx, "m.p1", d_d1, npairs, p1, dim, hyb || tensor, validate, &P1, bad));
         TRY(prepare_maps(ctx, "m.p2", d_d2, npairs, p2, dim, hyb || tensor, validate, &P2, bad + 1));
         if (validate) {

@@ -1805,7 +1805,8 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a) {
 
 // ====================================================================== host
 int tensor_pack(fnl_context* ctx, const char* tag, const float* d_src, uint32_t npairs, uint32_t rows,
-                uint32_t dim, bool l2, unsigned long long* d_bad, unsigned long long* d_sat, PackedMaps* out) {
+                uint32_t dim, bool l2, unsigned long long* d_bad, unsigned long long* d_sat, PackedMaps* out,
+                float* d_max_norm) {
     if (dim == 0 || dim + (l2 ? 2u : 0u) > kPackK)
         return fail(FNL_EINVAL, "tensor backend: descriptor dim " + std::to_string(dim) + " exceeds " +
                                     std::to_string(l2 ? kPackK - 2 : kPackK) + " (" + (l2 ? "l2" : "dot") +
@@ -1816,10 +1817,14 @@ int tensor_pack(fnl_context* ctx, const char* tag, const float* d_src, uint32_t 
     const uint64_t pair_bytes = (uint64_t)(rows_pad / kTargetTileRows) * cpr * kChunkBytes;
     std::string t(tag);
     TRY(ws_arr(ctx, (t + ".packed").c_str(), (size_t)npairs * pair_bytes, &out->data));
-    TRY(ws_arr(ctx, (t + ".maxnorm").c_str(), 2 * (size_t)npairs, &out->max_norm));
-    out->max_norm_hi = out->max_norm + npairs;
     cudaStream_t s = ctx_stream(ctx);
-    FNL_CUDA_TRY(cudaMemsetAsync(out->max_norm, 0, 2 * (size_t)npairs * sizeof(float), s));
+    if (d_max_norm) {
+        out->max_norm = d_max_norm;  // [2 npairs], zeroed by the caller
+    } else {
+        TRY(ws_arr(ctx, (t + ".maxnorm").c_str(), 2 * (size_t)npairs, &out->max_norm));
+        FNL_CUDA_TRY(cudaMemsetAsync(out->max_norm, 0, 2 * (size_t)npairs * sizeof(float), s));
+    }
+    out->max_norm_hi = out->max_norm + npairs;
     out->pair_bytes = pair_bytes;
     out->cpr = cpr;
     out->rows = rows;

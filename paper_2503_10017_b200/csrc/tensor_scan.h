@@ -52,7 +52,7 @@ struct PackedMaps {
 // Saturations per pair added into d_sat[pair].
 int tensor_pack(fnl_context* ctx, const char* tag, const float* d_src, uint32_t npairs, uint32_t rows,
                 uint32_t dim, bool l2, unsigned long long* d_bad, unsigned long long* d_sat,
-                PackedMaps* out);
+                PackedMaps* out, float* d_max_norm = nullptr);
 
 // One NN pass of gathered query rows against target maps, batched over pairs.
 // Query rows of pair p: ids[p*cap + i] (or i when ids is null), i < d_active[p];
